@@ -1,0 +1,286 @@
+"""Seeded synthetic cone programs (test and benchmark inputs).
+
+These follow the reference generator *encodings* (row/column layout, cone
+blocks, planted objects) of ``conesplit.generators``
+(/root/reference/pkg/src/conesplit/generators.py) but draw from numpy's
+PCG64 so they vectorise; they are NOT bit-compatible with the reference's
+pure-Python xoshiro stream (the reference disclaims bit-compatibility too,
+rng.py:7-9).  Every function returns ``(colptr, rowidx, vals, b, c, cone)``
+with CSC arrays in the reference layout (int64 colptr/rowidx, fp64 vals,
+rows strictly increasing per column) and ``cone`` a dict
+``{"z","l","q","s","ep"}`` (fileio.py:68-73 plus the exp-cone count).
+
+Huge LASSO instances (1e8-1e9 nnz) come from the multithreaded C generator
+``scs_gen_lasso`` in the native library (see ``paper_1312_3039_b200.native``).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def _csc_from_triplets(m, n, rows, cols, vals):
+    """Sorted CSC, duplicates summed (sparse_linalg.py:72-97 semantics)."""
+    rows = np.asarray(rows, np.int64)
+    cols = np.asarray(cols, np.int64)
+    vals = np.asarray(vals, np.float64)
+    key = cols * m + rows
+    order = np.argsort(key, kind="stable")
+    key, vals = key[order], vals[order]
+    if key.size:
+        first = np.ones(key.size, bool)
+        first[1:] = key[1:] != key[:-1]
+        starts = np.flatnonzero(first)
+        vals = np.add.reduceat(vals, starts)
+        key = key[starts]
+    cols, rows = np.divmod(key, m) if m else (key, key)
+    colptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(cols, minlength=n), out=colptr[1:])
+    return colptr, rows.astype(np.int64), vals
+
+
+def csc_matvec(colptr, rowidx, vals, m, x):
+    cols = np.repeat(np.arange(colptr.size - 1), np.diff(colptr))
+    return np.bincount(rowidx, weights=vals * x[cols], minlength=m)
+
+
+def csc_rmatvec(colptr, rowidx, vals, y):
+    n = colptr.size - 1
+    cols = np.repeat(np.arange(n), np.diff(colptr))
+    return np.bincount(cols, weights=vals * y[rowidx], minlength=n)
+
+
+def _random_columns(rng, m, n, per_col):
+    """per_col distinct random rows in every column (generators.py:289-299)."""
+    rows = rng.integers(0, m, size=(n, per_col))
+    for _ in range(100):
+        rows.sort(axis=1)
+        dup = np.any(rows[:, 1:] == rows[:, :-1], axis=1)
+        if not dup.any():
+            break
+        rows[dup] = rng.integers(0, m, size=(int(dup.sum()), per_col))
+    rows.sort(axis=1)
+    cols = np.repeat(np.arange(n), per_col)
+    return rows.ravel(), cols, rng.standard_normal(n * per_col)
+
+
+def gen_lp(kind, n, m, seed):
+    """LP over the nonnegative orthant with a planted optimum, Farkas
+    certificate or improving ray (generators.py:302-383 recipes)."""
+    if not m >= n >= 1:
+        raise ValueError("lp families need m >= n >= 1")
+    rng = np.random.default_rng(seed)
+    per_col = min(m, max(2, round(0.3 * m))) if m <= 60 else 8
+    rows, cols, vals = _random_columns(rng, m, n, per_col)
+    cone = {"z": 0, "l": m, "q": [], "s": [], "ep": 0}
+    if kind == "lp_feasible":
+        colptr, ri, va = _csc_from_triplets(m, n, rows, cols, vals)
+        x = rng.standard_normal(n)
+        tight = rng.permutation(m)[: max(1, m // 2)]
+        y = np.zeros(m)
+        y[tight] = 0.1 + rng.random(tight.size)
+        s = 0.1 + rng.random(m)
+        s[tight] = 0.0
+        b = csc_matvec(colptr, ri, va, m, x) + s
+        c = -csc_rmatvec(colptr, ri, va, y)
+        return colptr, ri, va, b, c, cone
+    if kind == "lp_infeasible":
+        r1 = int(rng.integers(m))
+        r2 = int(rng.integers(m - 1))
+        r2 += r2 >= r1
+        keep = rows != r2
+        mir = rows == r1
+        rows = np.concatenate([rows[keep], np.full(int(mir.sum()), r2)])
+        cols2 = np.concatenate([cols[keep], cols[mir]])
+        vals = np.concatenate([vals[keep], -vals[mir]])
+        colptr, ri, va = _csc_from_triplets(m, n, rows, cols2, vals)
+        b = rng.standard_normal(m)
+        b[r2] = -1.0 - b[r1]
+        c = -csc_rmatvec(colptr, ri, va, rng.random(m))
+        return colptr, ri, va, b, c, cone
+    if kind == "lp_unbounded":
+        present = np.zeros(m, bool)
+        present[rows] = True
+        miss = np.flatnonzero(~present)
+        rows = np.concatenate([rows, miss])
+        cols = np.concatenate([cols, rng.integers(0, n, miss.size)])
+        vals = np.concatenate([vals, rng.standard_normal(miss.size)])
+        x0 = 0.5 + rng.random(n)
+        slack = 0.1 + rng.random(m)
+        order = np.lexsort((cols, rows))
+        rows, cols, vals = rows[order], cols[order], vals[order]
+        reach = np.bincount(rows, weights=vals * x0[cols], minlength=m)
+        first = np.searchsorted(rows, np.arange(m))
+        vals[first] -= (reach + slack) / x0[cols[first]]
+        colptr, ri, va = _csc_from_triplets(m, n, rows, cols, vals)
+        c = rng.standard_normal(n)
+        j = int(rng.integers(n))
+        c[j] -= (c @ x0 + 1.0) / x0[j]
+        b = rng.random(m)
+        return colptr, ri, va, b, c, cone
+    raise ValueError(f"unknown LP family kind {kind!r}")
+
+
+def _planted_blocks(rng, cone):
+    """Complementary (s*, y*) per cone block: s in K, y in K*, s'y = 0."""
+    m = (cone["z"] + cone["l"] + sum(cone["q"])
+         + sum(k * (k + 1) // 2 for k in cone["s"]) + 3 * cone["ep"])
+    s = np.zeros(m)
+    y = np.zeros(m)
+    off = 0
+    z = cone["z"]
+    y[off:off + z] = rng.standard_normal(z)
+    off += z
+    ln = cone["l"]
+    tight = rng.random(ln) < 0.5
+    y[off:off + ln] = np.where(tight, 0.1 + rng.random(ln), 0.0)
+    s[off:off + ln] = np.where(tight, 0.0, 0.1 + rng.random(ln))
+    off += ln
+    for d in cone["q"]:
+        if d == 1:
+            s[off] = rng.random()
+        else:
+            u = rng.standard_normal(d - 1)
+            u /= np.linalg.norm(u)
+            a, bb = 0.5 + rng.random(), 0.5 + rng.random()
+            s[off], s[off + 1:off + d] = a, a * u
+            y[off], y[off + 1:off + d] = bb, -bb * u
+        off += d
+    for k in cone["s"]:
+        q, _ = np.linalg.qr(rng.standard_normal((k, k)))
+        lam = 0.5 + rng.random(k)
+        split = rng.random(k) < 0.5
+        S = (q * np.where(split, lam, 0.0)) @ q.T
+        Y = (q * np.where(split, 0.0, lam)) @ q.T
+        rows, cols = np.tril_indices(k)
+        order = np.lexsort((rows, cols))  # column-major lower triangle
+        rows, cols = rows[order], cols[order]
+        scale = np.where(rows == cols, 1.0, math.sqrt(2.0))
+        ln2 = k * (k + 1) // 2
+        s[off:off + ln2] = S[rows, cols] * scale
+        y[off:off + ln2] = Y[rows, cols] * scale
+        off += ln2
+    for _ in range(cone["ep"]):
+        rho = rng.uniform(-1.0, 1.0)
+        a, bb = 0.5 + rng.random(), 0.5 + rng.random()
+        s[off:off + 3] = a * np.array([rho, 1.0, math.exp(rho)])
+        y[off:off + 3] = bb * np.array([-1.0, rho - 1.0, math.exp(-rho)])
+        off += 3
+    return s, y
+
+
+def gen_planted(m_cone, n, density, seed, nnz_per_col=None):
+    """Feasible cone program with a planted complementary optimum.
+
+    ``m_cone`` is a cone dict; A (m x n) has uniformly random positions at the
+    given density (or ``nnz_per_col`` random rows per column) and N(0,1)
+    values; b = A x* + s*, c = -A^T y* (generators.py:321-334 extended to
+    SOC/PSD/exp blocks).  This is config 1 (LP+SOC) and the C4 cone mix.
+    """
+    cone = {"z": 0, "l": 0, "q": [], "s": [], "ep": 0}
+    cone.update({k: v for k, v in m_cone.items()})
+    rng = np.random.default_rng(seed)
+    s, y = _planted_blocks(rng, cone)
+    m = s.size
+    if nnz_per_col is None:
+        nnz = max(1, int(round(density * m * n)))
+        lin = np.unique(rng.integers(0, m * n, size=int(nnz * 1.02) + 8))
+        lin = rng.permutation(lin)[:nnz]
+        cols, rows = np.divmod(lin, m)
+    else:
+        rows, cols, _ = _random_columns(rng, m, n, nnz_per_col)
+    vals = rng.standard_normal(rows.size)
+    colptr, ri, va = _csc_from_triplets(m, n, rows, cols, vals)
+    x = rng.standard_normal(n)
+    b = csc_matvec(colptr, ri, va, m, x) + s
+    c = -csc_rmatvec(colptr, ri, va, y)
+    return colptr, ri, va, b, c, cone
+
+
+def gen_lp_soc(m=3000, n=1000, density=0.01, n_soc=100, soc_dim=10, seed=0):
+    """Config 1: LP+SOC, l = m - n_soc*soc_dim, q = [soc_dim]*n_soc."""
+    cone = {"l": m - n_soc * soc_dim, "q": [soc_dim] * n_soc}
+    return gen_planted(cone, n, density, seed)
+
+
+def gen_lasso(p, q, nnz_f, seed, mu=None):
+    """Sparse-F LASSO in gen_lasso's standard form (generators.py:81-120).
+
+    F is q x p with ``nnz_f`` N(0,1) entries spread evenly over its columns at
+    uniformly random rows; variables (z, t, w): n = 2p+1, m = 2p+q+2,
+    cone {l: 2p, q: [q+2]}.
+    """
+    rng = np.random.default_rng(seed)
+    per = np.full(p, nnz_f // p, np.int64)
+    per[: nnz_f % p] += 1
+    per = np.minimum(per, q)
+    fr = []
+    for j in range(p):
+        fr.append(np.sort(rng.choice(q, int(per[j]), replace=False)))
+    frows = np.concatenate(fr) if fr else np.zeros(0, np.int64)
+    fcols = np.repeat(np.arange(p), per)
+    fvals = rng.standard_normal(frows.size)
+    zhat = np.zeros(p)
+    sup = rng.choice(p, max(1, p // 10), replace=False)
+    zhat[sup] = rng.standard_normal(sup.size)
+    g = np.bincount(frows, weights=fvals * zhat[fcols], minlength=q) + \
+        rng.standard_normal(q) * math.sqrt(0.1)
+    if mu is None:
+        mu = 0.1 * np.max(np.abs(np.bincount(fcols, weights=fvals * g[frows], minlength=p)))
+    n, m = 2 * p + 1, 2 * p + q + 2
+    idx = np.arange(p)
+    r0 = 2 * p
+    rows = np.concatenate([idx, idx, p + idx, p + idx, [r0, r0 + 1], r0 + 2 + frows])
+    cols = np.concatenate([idx, p + idx, idx, p + idx, [2 * p, 2 * p], fcols])
+    vals = np.concatenate([np.ones(p), -np.ones(p), -np.ones(p), -np.ones(p),
+                           [-1.0, 1.0], 2.0 * fvals])
+    b = np.zeros(m)
+    b[r0] = b[r0 + 1] = 1.0
+    b[r0 + 2:] = 2.0 * g
+    c = np.concatenate([np.zeros(p), mu * np.ones(p), [0.5]])
+    colptr, ri, va = _csc_from_triplets(m, n, rows, cols, vals)
+    return colptr, ri, va, b, c, {"z": 0, "l": 2 * p, "q": [q + 2], "s": [], "ep": 0}
+
+
+def gen_portfolio(p, q, seed, gamma=10.0):
+    """Long-only factor-model portfolio SOCP (generators.py:123-194)."""
+    rng = np.random.default_rng(seed)
+    mu_ret = np.exp(rng.standard_normal(p))
+    F = rng.standard_normal((p, q))
+    d = 2.0 * rng.random(p)
+    n, m = p + 4, 2 * p + q + 9
+    t_col, s_col, u_col, v_col = p, p + 1, p + 2, p + 3
+    idx = np.arange(p)
+    r0 = 1 + p
+    r1 = r0 + p + 1
+    r2 = r1 + q + 1
+    r3 = r2 + 3
+    fr, fc = np.nonzero(F.T)
+    rows = np.concatenate([np.zeros(p, np.int64), 1 + idx, [r0], r0 + 1 + idx, [r1],
+                           r1 + 1 + fr, [r2, r2 + 1, r2 + 2, r3, r3 + 1, r3 + 2]])
+    cols = np.concatenate([idx, idx, [u_col], idx, [v_col], fc,
+                           [t_col, t_col, u_col, s_col, s_col, v_col]])
+    vals = np.concatenate([np.ones(p), -np.ones(p), [-1.0], -np.sqrt(d), [-1.0],
+                           -F.T[fr, fc], [-1.0, 1.0, -2.0, -1.0, 1.0, -2.0]])
+    b = np.zeros(m)
+    b[0] = 1.0
+    b[r2] = b[r2 + 1] = b[r3] = b[r3 + 1] = 1.0
+    c = np.zeros(n)
+    c[:p] = -mu_ret
+    c[t_col] = c[s_col] = gamma
+    colptr, ri, va = _csc_from_triplets(m, n, rows, cols, vals)
+    cone = {"z": 1, "l": p, "q": [p + 1, q + 1, 3, 3], "s": [], "ep": 0}
+    return colptr, ri, va, b, c, cone
+
+
+def gen_cone_mix(n_psd=50, psd_sides=(3, 4, 5, 6, 7, 8), n_exp=50, n_soc=20,
+                 soc_dim=6, l=200, z=10, n=400, nnz_per_col=8, seed=0):
+    """Config 4 cone mix: zero + nonneg + SOC + many small PSD + exp cones
+    with a planted optimum (exp part parity-unpinned)."""
+    rng = np.random.default_rng(seed + 1)
+    sides = [int(psd_sides[i % len(psd_sides)]) for i in range(n_psd)]
+    rng.shuffle(sides)
+    cone = {"z": z, "l": l, "q": [soc_dim] * n_soc, "s": sides, "ep": n_exp}
+    return gen_planted(cone, n, None, seed, nnz_per_col=nnz_per_col)
