@@ -1,0 +1,307 @@
+"""Benchmark: ADMM iterations/s of the SCS indirect hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c3|c1]
+                    [--impl ours|reference]
+
+A "step" is one ADMM iteration (solver.py:153-166 + the termination check
+of solver.py:359-363) over the whole problem.  Default workload: BASELINE
+config 5 (the north-star target), the sparse LASSO-as-SOCP in gen_lasso's
+encoding with 1e9 nonzeros (m = 10,000,002, n = 1,000,001).
+
+value   device-timed iterations/s (CUDA events around K back-to-back
+        graph-launched iterations, inputs resident in HBM; the 12 GB matrix
+        streams exceed the 126 MB L2, so no flush is needed)
+e2e     the same metric through the public API, Workspace.solve(warm_start)
+        with host buffers: H2D of the warm start and D2H of the final (u, v)
+        and solution inside the wall-clock window
+roofline  the dominant kernel (the A^T-pass SpMV with the CG epilogue):
+        algorithmic bytes per launch / CUDA-event launch time vs the
+        measured HBM peak of MEASURED_PEAKS.json
+cpu_baseline  the CPU oracle (numpy restatement of the reference, same
+        algorithm as conesplit) on a bounded sample of the same encoding,
+        scaled per nonzero to the full workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[4]: 1e7 x 1e6 LASSO-as-SOCP, 1e9 nnz
+    "c5": dict(p=500_000, q=8_999_998, nnz=1_000_000_000, seed=1),
+    # BASELINE.json configs[2]: 1e6 x 1e5, 1e8 nnz
+    "c3": dict(p=50_000, q=899_998, nnz=100_000_000, seed=1),
+    # small, for quick checks
+    "c1": dict(p=5_000, q=89_998, nnz=10_000_000, seed=1),
+}
+SAMPLE = dict(p=5_000, q=89_998, nnz=10_000_000, seed=1)  # CPU oracle sample
+
+
+def lasso_dims(cfg):
+    p, q, nnz = cfg["p"], cfg["q"], cfg["nnz"]
+    return 2 * p + q + 2, 2 * p + 1, nnz - 4 * p - 2
+
+
+def b_iter(m, n, nnz, k=2, check=True):
+    """SURVEY.md §8d algorithmic bytes per ADMM iteration."""
+    P = (6 + 2 * k) if check else (4 + 2 * k)
+    b_pass = 12 * nnz + 16 * (m + n)
+    ell = n + m + 1
+    return P * b_pass + 8 * (12 * ell + (10 * k + 6) * n)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev=0):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_problem(cfg, threads=0):
+    from paper_1312_3039_b200 import native
+    return native.gen_lasso(cfg["p"], cfg["q"], cfg["nnz"] - 4 * cfg["p"] - 2, seed=cfg["seed"],
+                            threads=threads)
+
+
+def cpu_sample(steps, warmup, full_nnz):
+    """Time the CPU oracle (reference algorithm) on the bounded sample."""
+    from oracle import scs_oracle as O
+    colptr, rowidx, vals, b, c, cone = load_problem(SAMPLE)
+    m, n = b.size, colptr.size - 1
+    A = O.Csc(m, n, colptr, rowidx, vals)
+    s = O.OracleSolver(A, b, c, cone, max_iters=10**9)
+    u = np.zeros(n + m + 1)
+    v = np.zeros(n + m + 1)
+    u[-1] = v[-1] = 1.0
+    s.cg_warm = np.zeros(n)
+    k = 0
+    for _ in range(warmup):
+        k += 1
+        u, v = s.step(u, v, k)
+        s.residuals(u, v)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        k += 1
+        u, v = s.step(u, v, k)
+        s.residuals(u, v)
+    dt = time.perf_counter() - t0
+    ips_sample = steps / dt
+    scale = A.nnz / full_nnz
+    cores = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": ips_sample * scale, "unit": "iters/s", "cores": cores, "kind": "port",
+            "sample": f"CPU oracle (numpy restatement of conesplit's indirect path) on the same "
+                      f"LASSO encoding with p={SAMPLE['p']} q={SAMPLE['q']} nnz={A.nnz}: "
+                      f"{steps} iterations (+{warmup} warm-up) at {dt / steps:.3f} s/iteration, "
+                      f"scaled by nnz ratio {scale:.3g} to the full workload; SpMV (np.bincount) "
+                      f"on 1 core, BLAS level-1 on up to {cores} threads"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    m, n, nnzf = lasso_dims(cfg)
+    nnz = cfg["nnz"]
+    cb = cpu_sample(args.steps, args.warmup, nnz)
+    line = {
+        "impl": "reference", "metric": "ADMM iterations/s (indirect SCS, LASSO-as-SOCP)",
+        "value": cb["value"], "unit": "iters/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 / cb["value"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args.config, cfg, m, n, nnz),
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "iters/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(name, cfg, m, n, nnz):
+    return {"workload": f"lasso_socp_{name}", "encoding": "conesplit gen_lasso (generators.py:81-120), sparse F",
+            "p": cfg["p"], "q": cfg["q"], "m": m, "n": n, "nnz": nnz, "eps": 1e-3,
+            "cg_max": 2, "check_interval": 1, "mode": "parity (reference algorithm)",
+            "l2": "inputs larger than L2 (matrix streams >> 126 MB)"}
+
+
+def run_ours(args, cfg):
+    import paper_1312_3039_b200 as P
+    from paper_1312_3039_b200 import native
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        raise SystemExit("row-sharded multi-GPU bench is not enabled in this build")
+    lib = native.load()
+    t0 = time.perf_counter()
+    colptr, rowidx, vals, b, c, cone = load_problem(cfg)
+    gen_s = time.perf_counter() - t0
+    m, n, nnz = b.size, colptr.size - 1, rowidx.size
+    A = object.__new__(P.SparseMatrix)  # skip O(nnz) numpy validation (generator output)
+    A.nrows, A.ncols, A.colptr, A.rowidx, A.vals = m, n, colptr, rowidx, vals
+    data = object.__new__(P.ProblemData)
+    data.A, data.b, data.c, data.spec = A, b, c, P.ConeSpec.from_any(cone)
+    st = P.Settings(max_iters=args.steps, eps_pri=1e-3, eps_dual=1e-3, eps_gap=1e-3)
+    t0 = time.perf_counter()
+    ws = P.Workspace(data, st)
+    setup_s = time.perf_counter() - t0
+    h = ws._h
+    # device-resident timing
+    native.check(lib.scs_begin(h, None, None, None), h)
+    ms = native.C.c_double()
+    native.check(lib.scs_bench_iters(h, args.warmup, native.C.byref(ms)), h)
+    with Clocks(0) as clk:
+        native.check(lib.scs_bench_iters(h, args.steps, native.C.byref(ms)), h)
+    info = native.Info()
+    native.check(lib.scs_step(h, 0, native.C.byref(info)), h)
+    if info.status >= 0:
+        print(f"warning: solver terminated ({info.status}) inside the timed region",
+              file=sys.stderr)
+    launches_per_iter = info.launches // max(args.steps, 1)
+    ms_iter = ms.value / args.steps
+    ips = 1000.0 / ms_iter
+    # roofline of the dominant kernels
+    peak, peak_kind = peaks()
+    kern = {}
+    for kind, name in ((0, "spmv_A(q=A p)"), (1, "spmv_At_cg(Gp=p+A^T q; p'Gp)")):
+        kms, kb = native.C.c_double(), native.C.c_double()
+        native.check(lib.scs_bench_kernel(h, kind, 10, native.C.byref(kms), native.C.byref(kb)), h)
+        kern[name] = {"ms": kms.value, "bytes": kb.value,
+                      "gbs": kb.value / (kms.value * 1e-3) / 1e9}
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": kern[dom]["gbs"] / peak,
+            "traffic": traffic, "bytes_per_launch": kern[dom]["bytes"],
+            "launch_ms": kern[dom]["ms"], "kernels": kern,
+            "iteration": {"bytes_formula": b_iter(m, n, nnz),
+                          "achieved": b_iter(m, n, nnz) * ips / 1e9,
+                          "frac": b_iter(m, n, nnz) * ips / 1e9 / peak}}
+    # end-to-end through the public API with host buffers
+    x0, y0, s0 = np.zeros(n), np.zeros(m), np.zeros(m)
+    t0 = time.perf_counter()
+    sol = ws.solve(warm_start=(x0, y0, s0))
+    e2e_s = time.perf_counter() - t0
+    e2e_iters = sol.info.iterations
+    h2d = 8 * (n + 2 * m)
+    d2h = 8 * 2 * (n + m + 1) + 8 * (n + 2 * m)
+    line = {
+        "metric": "ADMM iterations/s (indirect SCS, LASSO-as-SOCP)", "value": ips,
+        "unit": "iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_iter, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args.config, cfg, m, n, nnz),
+        "roofline": roof,
+        "e2e": {"value": e2e_iters / e2e_s, "unit": "iters/s",
+                "h2d_bytes_per_step": h2d / max(e2e_iters, 1),
+                "d2h_bytes_per_step": d2h / max(e2e_iters, 1),
+                "iterations": e2e_iters, "seconds": e2e_s,
+                "note": "Workspace.solve(warm_start=host arrays) incl. H2D of the warm start, "
+                        "D2H of (u, v), extraction and point residuals"},
+        "gpu_launches": int(launches_per_iter * args.steps),
+        "launches_per_step": int(launches_per_iter),
+        "clocks": clk.summary(),
+        "setup_s": setup_s, "generate_s": gen_s,
+        "status_after_timed": int(info.status),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_sample(3, 1, nnz)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=os.environ.get("SCS_BENCH_CONFIG", "c5"),
+                    choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,189 @@
+// cones.cuh -- device projections for the cone blocks of K* (the y-part of
+// the embedding iterate, cones.py:220-249):
+//   zero block   -> free (identity)            cones.py:230-231
+//   nonnegative  -> max(., 0)                  cones.py:232-233
+//   SOC          -> three-branch formula       cones.py:172-184
+//   PSD (svec)   -> eig-clamp via Jacobi       cones.py:147-191, _kernels.py:119-191
+//   exponential  -> K_exp* = v + Pi_Kexp(-v)   (no reference)
+#pragma once
+
+#include "common.cuh"
+
+namespace scs {
+
+// ---------------------------------------------------------------------------
+// exponential cone K_exp = cl{(r,s,t) : s > 0, s exp(r/s) <= t}
+// Hard case: projection = s (rho, 1, e^rho) with polar part
+// -lam (-1, rho-1, e^-rho); eliminating s and lam leaves the univariate root
+//   F(rho) = ((rho-1) r0 + s0) e^rho - (r0 - rho s0) e^-rho
+//            - t0 (rho^2 - rho + 1) = 0
+// on the interval where s > 0 and lam > 0 (F is increasing there).  Solved
+// by safeguarded Newton inside a bisection bracket.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool exp_in_primal(double r, double s, double t) {
+  return (s > 0.0 && s * exp(r / s) <= t) || (r <= 0.0 && s == 0.0 && t >= 0.0);
+}
+__device__ __forceinline__ bool exp_in_dual(double u, double v, double w) {
+  return (u < 0.0 && -u * exp(v / u) <= 2.718281828459045 * w) ||
+         (u == 0.0 && v >= 0.0 && w >= 0.0);
+}
+
+__device__ __forceinline__ double exp_F(double rho, double r0, double s0, double t0) {
+  const double q = rho * rho - rho + 1.0;
+  const double er = exp(fmin(rho, 700.0)), emr = exp(fmin(-rho, 700.0));
+  return ((rho - 1.0) * r0 + s0) * er / q - (r0 - rho * s0) * emr / q - t0;
+}
+
+__device__ void exp_proj_primal(double r0, double s0, double t0, double* out) {
+  if (exp_in_primal(r0, s0, t0)) { out[0] = r0; out[1] = s0; out[2] = t0; return; }
+  if (exp_in_dual(-r0, -s0, -t0)) { out[0] = 0.0; out[1] = 0.0; out[2] = 0.0; return; }
+  if (r0 <= 0.0 && s0 <= 0.0) { out[0] = r0; out[1] = 0.0; out[2] = fmax(t0, 0.0); return; }
+  double lo = -INFINITY, hi = INFINITY;
+  if (r0 > 0.0) lo = fmax(lo, 1.0 - s0 / r0);
+  else if (r0 < 0.0) hi = fmin(hi, 1.0 - s0 / r0);
+  if (s0 > 0.0) hi = fmin(hi, r0 / s0);
+  else if (s0 < 0.0) lo = fmax(lo, r0 / s0);
+  if (!isfinite(lo)) {
+    lo = (isfinite(hi) ? hi : 0.0) - 1.0;
+    for (int i = 0; i < 64 && exp_F(lo, r0, s0, t0) > 0.0; ++i) lo = lo < 0.0 ? 2.0 * lo - 1.0 : lo - 1.0;
+  }
+  if (!isfinite(hi)) {
+    hi = lo + 1.0;
+    for (int i = 0; i < 64 && exp_F(hi, r0, s0, t0) < 0.0; ++i) hi = hi > 0.0 ? 2.0 * hi + 1.0 : hi + 1.0;
+  }
+  double rho = 0.5 * (lo + hi);
+  for (int it = 0; it < 200; ++it) {
+    const double f = exp_F(rho, r0, s0, t0);
+    if (f < 0.0) lo = rho; else hi = rho;
+    if (f == 0.0 || hi - lo <= 1e-15 * fmax(1.0, fabs(rho))) break;
+    // Newton on F; derivative by the product rule
+    const double q = rho * rho - rho + 1.0, dq = 2.0 * rho - 1.0;
+    const double er = exp(fmin(rho, 700.0)), emr = exp(fmin(-rho, 700.0));
+    const double a = (rho - 1.0) * r0 + s0, bb = r0 - rho * s0;
+    const double df = (r0 * er + a * er) / q - a * er * dq / (q * q)
+                      - ((-s0) * emr - bb * emr) / q + bb * emr * dq / (q * q);
+    double nr = rho - f / df;
+    if (!(nr > lo && nr < hi) || !isfinite(nr)) nr = 0.5 * (lo + hi);
+    rho = nr;
+  }
+  const double q = rho * rho - rho + 1.0;
+  const double s = ((rho - 1.0) * r0 + s0) / q;
+  out[0] = s * rho;
+  out[1] = s;
+  out[2] = s * exp(rho);
+}
+
+// Pi_{K_exp*}(v) = v + Pi_{K_exp}(-v)  (Moreau)
+__device__ __forceinline__ void exp_proj_dual(const double* v, double* out) {
+  double p[3];
+  exp_proj_primal(-v[0], -v[1], -v[2], p);
+  out[0] = v[0] + p[0];
+  out[1] = v[1] + p[1];
+  out[2] = v[2] + p[2];
+}
+
+// ---------------------------------------------------------------------------
+// PSD: packed column-major lower triangle with sqrt(2) off-diagonals
+// (cones.py:23-64).  Element e of a side-k block -> (row, col).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void svec_rc(int e, int k, int& row, int& col) {
+  int j = 0, start = 0;
+  while (start + (k - j) <= e) { start += k - j; ++j; }
+  col = j;
+  row = j + (e - start);
+}
+
+// Round-robin (circle method) pairing for parallel cyclic Jacobi.
+__device__ __forceinline__ int rr_player(int slot, int step, int kk) {
+  return slot == 0 ? 0 : 1 + ((slot - 1 + step) % (kk - 1));
+}
+
+// Block-cooperative Jacobi eigensolve of the symmetric k x k matrix M
+// (row-major, stride k) with eigenvectors V; same stopping rule as the
+// reference (off-norm <= 1e-12 ||A||_F checked at sweep start, <= 100
+// sweeps; _kernels.py:137-191).  The parallel (round-robin) rotation order
+// differs from the reference's row-cyclic order; the projection it feeds is
+// unique, so results agree to rounding.  Returns false on non-convergence.
+__device__ bool block_jacobi(double* M, double* V, int k, double* cs, double* sn,
+                             int* pp, int* qq, double* dpp, double* dqq) {
+  const int tid = threadIdx.x;
+  for (int e = tid; e < k * k; e += blockDim.x) V[e] = (e / k == e % k) ? 1.0 : 0.0;
+  double fro[1] = {0.0};
+  for (int e = tid; e < k * k; e += blockDim.x) fro[0] += M[e] * M[e];
+  block_sum<1>(fro);
+  const double thresh = 1e-12 * sqrt(fro[0]);
+  if (k == 1) return true;
+  const int kk = k + (k & 1);
+  const int npair = kk / 2;
+  for (int sweep = 0; sweep <= 100; ++sweep) {
+    double off[1] = {0.0};
+    for (int e = tid; e < k * k; e += blockDim.x) {
+      const int i = e / k, j = e % k;
+      if (j > i) off[0] += 2.0 * M[e] * M[e];
+    }
+    block_sum<1>(off);
+    if (sqrt(off[0]) <= thresh) return true;
+    if (sweep == 100) return false;
+    for (int step = 0; step < kk - 1; ++step) {
+      for (int pi = tid; pi < npair; pi += blockDim.x) {
+        int a = rr_player(pi, step, kk), b = rr_player(kk - 1 - pi, step, kk);
+        int p = a < b ? a : b, q = a < b ? b : a;
+        double c = 1.0, s = 0.0, np = 0.0, nq = 0.0;
+        if (q < k) {
+          const double apq = M[p * k + q];
+          const double app = M[p * k + p], aqq = M[q * k + q];
+          np = app; nq = aqq;
+          if (apq != 0.0) {
+            const double tau = (aqq - app) / (2.0 * apq);
+            const double root = sqrt(1.0 + tau * tau);
+            const double t = tau >= 0.0 ? 1.0 / (tau + root) : 1.0 / (tau - root);
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            np = app - t * apq;
+            nq = aqq + t * apq;
+          }
+        } else {
+          p = -1;  // dummy pairing for odd k
+        }
+        pp[pi] = p; qq[pi] = q; cs[pi] = c; sn[pi] = s; dpp[pi] = np; dqq[pi] = nq;
+      }
+      __syncthreads();
+      // M <- M J (columns p, q)
+      for (int w = tid; w < npair * k; w += blockDim.x) {
+        const int pi = w / k, i = w % k, p = pp[pi];
+        if (p < 0 || sn[pi] == 0.0) continue;
+        const int q = qq[pi];
+        const double a = M[i * k + p], b = M[i * k + q];
+        M[i * k + p] = cs[pi] * a - sn[pi] * b;
+        M[i * k + q] = sn[pi] * a + cs[pi] * b;
+      }
+      __syncthreads();
+      // M <- J^T M (rows p, q) and V <- V J
+      for (int w = tid; w < npair * k; w += blockDim.x) {
+        const int pi = w / k, j = w % k, p = pp[pi];
+        if (p < 0 || sn[pi] == 0.0) continue;
+        const int q = qq[pi];
+        const double a = M[p * k + j], b = M[q * k + j];
+        M[p * k + j] = cs[pi] * a - sn[pi] * b;
+        M[q * k + j] = sn[pi] * a + cs[pi] * b;
+        const double va = V[j * k + p], vb = V[j * k + q];
+        V[j * k + p] = cs[pi] * va - sn[pi] * vb;
+        V[j * k + q] = sn[pi] * va + cs[pi] * vb;
+      }
+      __syncthreads();
+      for (int pi = tid; pi < npair; pi += blockDim.x) {
+        const int p = pp[pi];
+        if (p < 0 || sn[pi] == 0.0) continue;
+        const int q = qq[pi];
+        M[p * k + p] = dpp[pi];
+        M[q * k + q] = dqq[pi];
+        M[p * k + q] = 0.0;
+        M[q * k + p] = 0.0;
+      }
+      __syncthreads();
+    }
+  }
+  return false;
+}
+
+}  // namespace scs

@@ -1,0 +1,288 @@
+// kernels.cuh -- the per-iteration device kernels of the indirect SCS path.
+//
+// One ADMM iteration (solver.py:153-166 + 355-363) is this fixed kernel
+// sequence, captured once into a CUDA graph; every data-dependent branch of
+// the reference (CG early exits, termination) is taken on the device from
+// the Ctl block, so the host never synchronises inside an iteration:
+//
+//   k_prep         w = u+v, rhs = w[:-1] - w_tau h, ||rhs|| -> CG tol       embedding.py:177-185
+//   SpMV A^T  [EpiAtFirst]  cg_rhs = rhs_x - A^T rhs_y, r0 = cg_rhs - G x0   embedding.py:109, sparse_linalg.py:461-469
+//   cg_max x { SpMV A [EpiAp]; SpMV A^T [EpiAtGp]; k_cg_update; k_cg_p }    sparse_linalg.py:470-485
+//   SpMV A    [EpiAFinal]   z_y = rhs_y + A x, corr = h'p / denom          embedding.py:113, 192
+//   k_cone_tail    u~, relaxation, cone projection (elementwise / SOC / exp),
+//                  tau update                                               embedding.py:193-196, solver.py:163-165
+//   k_cone_apply   large SOC + PSD (Jacobi) blocks                          cones.py:172-191
+//   SpMV A    [EpiResA]  + SpMV A^T [EpiResAt]  residuals + termination     scaling.py:148-207, solver.py:210-234
+//
+// A x_{warm} is NOT recomputed at the head of CG: the previous iteration's
+// EpiAFinal already produced A x for the same x (cg_warm), bit-identical,
+// and stored it (Axw) -- the reference's A-pass for r0 is redundant work.
+// The reference's trailing exact-residual pass (sparse_linalg.py:486), whose
+// value its caller discards (embedding.py:110), is not performed.
+#pragma once
+
+#include "common.cuh"
+#include "cones.cuh"
+
+namespace scs {
+
+struct Csr {
+  const long long* rp;  // rows + 1
+  const int* ci;        // nnz
+  const double* v;      // nnz
+  long long rows;
+};
+
+// Device vectors of one handle.  x-part length n, y-part length m (local).
+struct Vec {
+  long long n, m;
+  double *u, *v;              // n + m + 1
+  const double *c, *b;        // scaled data
+  const double *D, *E;        // scalings
+  double *gx, *gy;            // g = M^-1 h
+  double *rhs_x, *rhs_y;      // rhs = w[:-1] - w_tau h
+  double *x;                  // CG iterate == cg_warm (embedding.py:111)
+  double *r, *p, *Gp;         // CG vectors (n)
+  double *q;                  // A p (m)
+  double *Axw;                // A cg_warm (m)
+  double *zy;                 // z_y = rhs_y + A x (m)
+  double *part;               // kMaxRed * kMaxGrid partials
+  double *chunk_part;         // big-SOC chunk partial norms
+  double *soc_fac;            // 3 per big SOC: mode, head, scale
+  Ctl* ctl;
+};
+
+// Cone layout of the local y-part (cones.py:121-139 order + exp last).
+struct Cones {
+  long long z, l;                 // [0, z) zero, [z, z + l) nonneg
+  int n_ssoc;                     // small SOCs (<= kSmallSoc): warp per cone
+  const long long* ssoc_off;      // start of each small SOC
+  const int* ssoc_len;            // its dimension
+  int n_bsoc;                     // big SOCs: chunked
+  const long long* bsoc_off;      // n_bsoc start offsets
+  const long long* bsoc_len;
+  const int* bsoc_chunk_lo;       // n_bsoc + 1
+  int n_chunk;
+  const long long* chunk_off;     // chunk start (absolute y offset)
+  const int* chunk_len;
+  const int* chunk_cone;
+  int n_psd;
+  const long long* psd_off;
+  const int* psd_side;
+  long long psd_lo, psd_hi;       // y range of all PSD blocks
+  long long exp_lo;               // first exp row
+  long long n_exp;
+  int max_side;
+};
+
+constexpr int kSmallSoc = 2048;  // warp-per-cone bound
+constexpr int kChunk = 8192;     // big-SOC chunk (one CTA)
+
+// ---------------------------------------------------------------------------
+// CSR row dot products: L lanes per row, lane-strided, FMA, group shuffle.
+// The matrix streams (ci, v) are loaded with evict-first (ld.global.cs) so
+// the L2 keeps the gather vectors resident.
+// ---------------------------------------------------------------------------
+template <int L, int NV>
+__device__ __forceinline__ void row_dot(const Csr& A, long long row, int gl,
+                                        const double* const (&xs)[NV], double (&s)[NV]) {
+  const long long k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
+#pragma unroll
+  for (int t = 0; t < NV; ++t) s[t] = 0.0;
+  long long k = k0 + gl;
+  for (; k + 3 * L < k1; k += 4 * L) {
+    int c[4];
+    double a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { c[u] = __ldcs(A.ci + k + u * L); a[u] = __ldcs(A.v + k + u * L); }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int t = 0; t < NV; ++t) s[t] = fma(a[u], __ldg(xs[t] + c[u]), s[t]);
+    }
+  }
+  for (; k < k1; k += L) {
+    const int c = __ldcs(A.ci + k);
+    const double a = __ldcs(A.v + k);
+#pragma unroll
+    for (int t = 0; t < NV; ++t) s[t] = fma(a, __ldg(xs[t] + c), s[t]);
+  }
+#pragma unroll
+  for (int t = 0; t < NV; ++t) s[t] = group_sum<L>(s[t]);
+}
+
+// Generic CSR SpMV with a per-row epilogue and an optional grid reduction
+// whose last block runs Epi::finish.  Grid-stride over rows by L-lane groups.
+template <int L, class Epi>
+__global__ void __launch_bounds__(kBlock) k_spmv(Csr A, Epi epi) {
+  if (epi.skip()) return;
+  const int gl = threadIdx.x & (L - 1);
+  const long long group = ((long long)blockIdx.x * kBlock + threadIdx.x) / L;
+  const long long ngroups = ((long long)gridDim.x * kBlock) / L;
+  double red[Epi::NR > 0 ? Epi::NR : 1];
+#pragma unroll
+  for (int t = 0; t < (Epi::NR > 0 ? Epi::NR : 1); ++t) red[t] = 0.0;
+  for (long long row = group; row < A.rows; row += ngroups) {
+    double s[Epi::NV];
+    row_dot<L, Epi::NV>(A, row, gl, epi.xs, s);
+    if (gl == 0) epi.row(row, s, red);
+  }
+  epi.extra(red);
+  if constexpr (Epi::NR > 0) {
+    if (grid_sum_last<Epi::NR>(red, epi.V.part, &epi.V.ctl->counter)) epi.finish(red);
+  }
+}
+
+// ---- epilogues --------------------------------------------------------------
+struct EpiBase {
+  Vec V;
+  __device__ void extra(double*) const {}
+};
+
+// r0 = (rhs_x - A^T rhs_y) - (x0 + A^T (A x0)); p = r (sparse_linalg.py:461-469)
+struct EpiAtFirst : EpiBase {
+  static constexpr int NV = 2, NR = 1;
+  const double* xs[2];
+  __device__ bool skip() const { return V.ctl->stop; }
+  __device__ void row(long long j, const double (&s)[2], double* red) const {
+    const double cg_rhs = V.rhs_x[j] - s[0];
+    const double gx = V.x[j] + s[1];
+    const double r = cg_rhs - gx;
+    V.r[j] = r;
+    V.p[j] = r;
+    red[0] += r * r;
+  }
+  __device__ void finish(const double* tot) const {
+    if (threadIdx.x) return;
+    Ctl* c = V.ctl;
+    const double res = sqrt(tot[0]);
+    c->cg_it = 0;
+    if (!isfinite(res)) { c->err |= ERR_CG_NONFINITE; c->stop = 1; c->cg_done = 1; return; }
+    if (res <= c->tol) { c->cg_done = 1; return; }
+    c->cg_done = 0;
+    c->rs = res * res;
+  }
+};
+
+// q = A p
+struct EpiAp : EpiBase {
+  static constexpr int NV = 1, NR = 0;
+  const double* xs[1];
+  __device__ bool skip() const { return V.ctl->stop || V.ctl->cg_done; }
+  __device__ void row(long long i, const double (&s)[1], double*) const { V.q[i] = s[0]; }
+  __device__ void finish(const double*) const {}
+};
+
+// Gp = p + A^T q, p'Gp -> alpha (sparse_linalg.py:471-475)
+struct EpiAtGp : EpiBase {
+  static constexpr int NV = 1, NR = 1;
+  const double* xs[1];
+  __device__ bool skip() const { return V.ctl->stop || V.ctl->cg_done; }
+  __device__ void row(long long j, const double (&s)[1], double* red) const {
+    const double pj = V.p[j];
+    const double g = pj + s[0];
+    V.Gp[j] = g;
+    red[0] += pj * g;
+  }
+  __device__ void finish(const double* tot) const {
+    if (threadIdx.x) return;
+    Ctl* c = V.ctl;
+    const double den = tot[0];
+    if (!isfinite(den) || den <= 0.0) { c->err |= ERR_CG_CURVATURE; c->stop = 1; c->cg_done = 1; return; }
+    c->cg_alpha = c->rs / den;
+  }
+};
+
+// z_y = rhs_y + A x; store A x for the next warm start; h'p -> corr
+// (embedding.py:113, 192).  In setup mode (g = M^-1 h) writes g_y and the
+// Schur denominator instead (embedding.py:152-161).
+struct EpiAFinal : EpiBase {
+  static constexpr int NV = 1, NR = 2;
+  const double* xs[1];
+  double* zy_out;
+  int setup;
+  __device__ bool skip() const { return V.ctl->stop; }
+  __device__ void row(long long i, const double (&s)[1], double* red) const {
+    const double z = V.rhs_y[i] + s[0];
+    zy_out[i] = z;
+    if (!setup) V.Axw[i] = s[0];
+    red[1] += V.b[i] * z;
+  }
+  __device__ void extra(double* red) const {
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nt = (long long)gridDim.x * blockDim.x;
+    for (long long j = tid; j < V.n; j += nt) red[0] += V.c[j] * V.x[j];
+  }
+  __device__ void finish(const double* tot) const {
+    if (threadIdx.x) return;
+    Ctl* c = V.ctl;
+    c->cg_iters_total += c->cg_it;
+    const double hp = tot[0] + tot[1];
+    if (setup) {
+      c->denom = 1.0 + hp;
+    } else {
+      c->warm_zero = 0;
+      c->corr = hp / c->denom;
+    }
+  }
+};
+
+// A u_x -> primal residual / unboundedness partial norms (scaling.py:466-489)
+struct EpiResA : EpiBase {
+  static constexpr int NV = 1, NR = 3;
+  const double* xs[1];
+  __device__ bool skip() const { return V.ctl->stop || !V.ctl->check_now; }
+  __device__ void row(long long i, const double (&s)[1], double* red) const {
+    const double ut = V.u[V.n + V.m];
+    const double t = s[0] + V.v[V.n + i];
+    const double di = 1.0 / V.D[i];
+    const double pr = di * (t / ut - V.b[i]);
+    const double ub = di * t;
+    red[0] += pr * pr;
+    red[1] += ub * ub;
+    red[2] += V.b[i] * V.u[V.n + i];
+  }
+  __device__ void finish(const double* tot) const {
+    if (threadIdx.x) return;
+    V.ctl->sums[0] = tot[0];
+    V.ctl->sums[1] = tot[1];
+    V.ctl->sums[2] = tot[2];
+  }
+};
+
+__device__ void finish_residuals(Ctl* c, double ut, double s_pri, double s_unb, double buy,
+                                 double s_dual, double s_inf, double cux);
+
+// A^T u_y -> dual residual / infeasibility norms, then termination
+// (scaling.py:467-507, solver.py:210-234)
+struct EpiResAt : EpiBase {
+  static constexpr int NV = 1, NR = 3;
+  const double* xs[1];
+  __device__ bool skip() const { return V.ctl->stop || !V.ctl->check_now; }
+  __device__ void row(long long j, const double (&s)[1], double* red) const {
+    const double ut = V.u[V.n + V.m];
+    const double ei = 1.0 / V.E[j];
+    const double du = ei * (s[0] / ut + V.c[j]);
+    const double inf = ei * s[0];
+    red[0] += du * du;
+    red[1] += inf * inf;
+    red[2] += V.c[j] * V.u[j];
+  }
+  __device__ void finish(const double* tot) const {
+    if (threadIdx.x) return;
+    Ctl* c = V.ctl;
+    finish_residuals(c, V.u[V.n + V.m], c->sums[0], c->sums[1], c->sums[2], tot[0], tot[1], tot[2]);
+  }
+};
+
+// Plain products for the C-ABI test hook (scs_apply_a).
+struct EpiPlain : EpiBase {
+  static constexpr int NV = 1, NR = 0;
+  const double* xs[1];
+  double* out;
+  __device__ bool skip() const { return false; }
+  __device__ void row(long long i, const double (&s)[1], double*) const { out[i] = s[0]; }
+  __device__ void finish(const double*) const {}
+};
+
+}  // namespace scs

@@ -1,0 +1,1607 @@
+// solver.cu -- B200-native SCS indirect-method hot path: device kernels that
+// are not SpMV epilogues, the setup path (CSC ingest, device transpose,
+// Ruiz equilibration, g = M^-1 h), the graph-captured iteration loop, and
+// the C-ABI declared in include/scs_b200.h.
+#include <cub/device/device_radix_sort.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/scs_b200.h"
+#include "common.cuh"
+#include "cones.cuh"
+#include "kernels.cuh"
+
+#ifdef SCS_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace scs {
+
+// ===========================================================================
+// iteration kernels (non-SpMV)
+// ===========================================================================
+
+// w = u + v; rhs = w[:-1] - w_tau h; CG tolerance (embedding.py:177-185)
+__global__ void __launch_bounds__(kBlock) k_prep(Vec V) {
+  Ctl* c = V.ctl;
+  if (c->stop) return;
+  const long long n = V.n, m = V.m;
+  const double wt = V.u[n + m] + V.v[n + m];
+  double red[1] = {0.0};
+  const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long nt = (long long)gridDim.x * kBlock;
+  for (long long i = tid; i < n + m; i += nt) {
+    const double w = V.u[i] + V.v[i];
+    double r;
+    if (i < n) { r = w - wt * V.c[i]; V.rhs_x[i] = r; }
+    else { r = w - wt * V.b[i - n]; V.rhs_y[i - n] = r; }
+    red[0] += r * r;
+  }
+  if (grid_sum_last<1>(red, V.part, &c->counter) && threadIdx.x == 0) {
+    const long long k = ++c->k_sched;
+    c->tol = c->cg_tol > 0.0 ? c->cg_tol
+                             : 1e-3 * (1.0 + sqrt(red[0])) / pow((double)(k < 1 ? 1 : k), 1.5);
+    c->cg_done = 0;
+    c->cg_it = 0;
+  }
+}
+
+// x += alpha p; r -= alpha Gp; r'r -> stop test / beta (sparse_linalg.py:476-485)
+__global__ void __launch_bounds__(kBlock) k_cg_update(Vec V, long long cap) {
+  Ctl* c = V.ctl;
+  if (c->stop || c->cg_done) return;
+  const double a = c->cg_alpha;
+  double red[1] = {0.0};
+  const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long nt = (long long)gridDim.x * kBlock;
+  for (long long j = tid; j < V.n; j += nt) {
+    V.x[j] += a * V.p[j];
+    const double r = V.r[j] - a * V.Gp[j];
+    V.r[j] = r;
+    red[0] += r * r;
+  }
+  if (grid_sum_last<1>(red, V.part, &c->counter) && threadIdx.x == 0) {
+    c->cg_it += 1;
+    const double rs_new = red[0];
+    if (!isfinite(rs_new)) { c->err |= ERR_CG_NONFINITE; c->stop = 1; c->cg_done = 1; return; }
+    if (sqrt(rs_new) <= c->tol || c->cg_it >= cap) { c->cg_done = 1; return; }
+    c->cg_beta = rs_new / c->rs;
+    c->rs = rs_new;
+  }
+}
+
+// p = r + beta p (sparse_linalg.py:484)
+__global__ void __launch_bounds__(kBlock) k_cg_p(Vec V) {
+  Ctl* c = V.ctl;
+  if (c->stop || c->cg_done) return;
+  const double be = c->cg_beta;
+  const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long nt = (long long)gridDim.x * kBlock;
+  for (long long j = tid; j < V.n; j += nt) V.p[j] = V.r[j] + be * V.p[j];
+}
+
+// relaxed point of element i of the (x, y) part:
+//   u~ = p - corr g (embedding.py:193), u_bar = alpha u~ + (1-alpha) u
+//   (solver.py:163), t = u_bar - v (cone input, solver.py:164)
+struct Relax {
+  double ut, ub, t;
+};
+__device__ __forceinline__ Relax relax_y(const Vec& V, long long i, double corr, double al) {
+  Relax r;
+  r.ut = V.zy[i] - corr * V.gy[i];
+  r.ub = al * r.ut + (1.0 - al) * V.u[V.n + i];
+  r.t = r.ub - V.v[V.n + i];
+  return r;
+}
+__device__ __forceinline__ void store_y(const Vec& V, long long i, double ub, double up) {
+  const double vi = V.v[V.n + i];
+  V.u[V.n + i] = up;
+  V.v[V.n + i] = (vi - ub) + up;  // solver.py:165
+}
+
+__device__ __forceinline__ void soc_factor(double nz, double t, double* mode, double* head,
+                                           double* scale) {
+  // cones.py:172-184
+  if (nz <= -t) { *mode = 0.0; *head = 0.0; *scale = 0.0; }
+  else if (nz <= t) { *mode = 1.0; *head = t; *scale = 1.0; }
+  else {
+    const double a = 0.5 * (nz + t);
+    *mode = 2.0; *head = a; *scale = a / nz;
+  }
+}
+
+// Affine tail + relaxation + cone projection of every block that one warp
+// or thread can finish alone (x-part free, zero, nonneg, small SOC, exp),
+// plus big-SOC chunk norms; the last block sets the tau entries, the big
+// SOC factors and the iteration counter.
+__global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K) {
+  Ctl* c = V.ctl;
+  if (c->stop) return;
+  const long long n = V.n, m = V.m;
+  const double corr = c->corr, al = c->alpha;
+  double red[2] = {0.0, 0.0};  // c'u~_x, b'u~_y
+  int bad = 0;
+  const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long nt = (long long)gridDim.x * kBlock;
+  // x-part: free cone (cones.py:246); v_x becomes exactly 0
+  for (long long j = tid; j < n; j += nt) {
+    const double ut = V.x[j] - corr * V.gx[j];
+    red[0] += V.c[j] * ut;
+    const double ub = al * ut + (1.0 - al) * V.u[j];
+    const double t = ub - V.v[j];
+    bad |= !isfinite(t);
+    const double vj = V.v[j];
+    V.u[j] = t;
+    V.v[j] = (vj - ub) + t;
+  }
+  // zero (free in K*) and nonnegative rows
+  const long long zl = K.z + K.l;
+  for (long long i = tid; i < zl; i += nt) {
+    const Relax r = relax_y(V, i, corr, al);
+    red[1] += V.b[i] * r.ut;
+    bad |= !isfinite(r.t);
+    store_y(V, i, r.ub, i < K.z ? r.t : fmax(r.t, 0.0));
+  }
+  // PSD and big-SOC rows only contribute b'u~ here (projected in k_cone_apply)
+  for (long long i = K.psd_lo + tid; i < K.psd_hi; i += nt) {
+    const Relax r = relax_y(V, i, corr, al);
+    red[1] += V.b[i] * r.ut;
+    bad |= !isfinite(r.t);
+  }
+  // small SOCs: one warp per cone
+  {
+    const int lane = threadIdx.x & 31;
+    const long long warp = tid >> 5, nw = nt >> 5;
+    for (long long q = warp; q < K.n_ssoc; q += nw) {
+      const long long o = K.ssoc_off[q], d = K.ssoc_len[q];
+      double zz = 0.0, t0 = 0.0, part = 0.0;
+      for (long long e = lane; e < d; e += 32) {
+        const Relax r = relax_y(V, o + e, corr, al);
+        part += V.b[o + e] * r.ut;
+        bad |= !isfinite(r.t);
+        if (e == 0) t0 = r.t; else zz += r.t * r.t;
+      }
+      red[1] += part;
+      zz = warp_sum(zz);
+      t0 = __shfl_sync(0xffffffffu, t0, 0);
+      double mode, head, scale;
+      soc_factor(sqrt(zz), t0, &mode, &head, &scale);
+      for (long long e = lane; e < d; e += 32) {
+        const Relax r = relax_y(V, o + e, corr, al);
+        double up;
+        if (mode == 0.0) up = 0.0;
+        else if (mode == 1.0) up = r.t;
+        else up = (e == 0) ? head : scale * r.t;
+        store_y(V, o + e, r.ub, up);
+      }
+    }
+  }
+  // exponential cones: one thread per cone, K_exp* (dual) projection
+  for (long long q = tid; q < K.n_exp; q += nt) {
+    const long long o = K.exp_lo + 3 * q;
+    double tv[3], ub[3], pr[3];
+    for (int e = 0; e < 3; ++e) {
+      const Relax r = relax_y(V, o + e, corr, al);
+      red[1] += V.b[o + e] * r.ut;
+      bad |= !isfinite(r.t);
+      tv[e] = r.t;
+      ub[e] = r.ub;
+    }
+    exp_proj_dual(tv, pr);
+    for (int e = 0; e < 3; ++e) store_y(V, o + e, ub[e], pr[e]);
+  }
+  // big SOC chunks: one block per chunk -> partial ||z||^2 (head excluded)
+  for (long long ch = blockIdx.x; ch < K.n_chunk; ch += gridDim.x) {
+    const long long o = K.chunk_off[ch];
+    const int len = K.chunk_len[ch];
+    const long long head = K.bsoc_off[K.chunk_cone[ch]];
+    double zz[1] = {0.0};
+    for (int e = threadIdx.x; e < len; e += kBlock) {
+      const Relax r = relax_y(V, o + e, corr, al);
+      red[1] += V.b[o + e] * r.ut;
+      bad |= !isfinite(r.t);
+      if (o + e != head) zz[0] += r.t * r.t;
+    }
+    block_sum<1>(zz);
+    if (threadIdx.x == 0) V.chunk_part[ch] = zz[0];
+  }
+  // never flip `stop` outside a last block: blocks that had not started yet
+  // would skip the reduction and strand its counter
+  if (bad) atomicOr(&c->err, ERR_CONE_NONFINITE);
+  if (!grid_sum_last<2>(red, V.part, &c->counter)) return;
+  // ---- last block: tau entry (embedding.py:196, cones.py:248) -------------
+  if (threadIdx.x == 0) {
+    if (c->err) c->stop = 1;
+    const double ut_ = V.u[n + m], vt_ = V.v[n + m];
+    const double wt = ut_ + vt_;
+    const double utau = (wt + red[0]) + red[1];
+    const double ub = al * utau + (1.0 - al) * ut_;
+    const double t = ub - vt_;
+    if (!isfinite(t)) { c->err |= ERR_CONE_NONFINITE; c->stop = 1; }
+    const double up = fmax(t, 0.0);
+    V.u[n + m] = up;
+    V.v[n + m] = (vt_ - ub) + up;
+    c->iter += 1;
+    c->check_now = c->force_check || (c->iter % c->check_interval == 0);
+  }
+  // big SOC factors: one warp per cone over its chunk partials
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int q = warp; q < K.n_bsoc; q += kWarps) {
+    double zz = 0.0;
+    for (int ch = K.bsoc_chunk_lo[q] + lane; ch < K.bsoc_chunk_lo[q + 1]; ch += 32)
+      zz += __ldcg(V.chunk_part + ch);
+    zz = warp_sum(zz);
+    if (lane == 0) {
+      const Relax r = relax_y(V, K.bsoc_off[q], corr, al);
+      soc_factor(sqrt(zz), r.t, V.soc_fac + 3 * q, V.soc_fac + 3 * q + 1, V.soc_fac + 3 * q + 2);
+    }
+  }
+}
+
+// Big SOC apply (block per chunk) and PSD blocks (block per PSD, Jacobi in
+// shared memory, or in global scratch for sides beyond the smem budget).
+__global__ void __launch_bounds__(kBlock) k_cone_apply(Vec V, Cones K, double* psd_scratch,
+                                                       int smem_side) {
+  Ctl* c = V.ctl;
+  if (c->stop) return;
+  const double corr = c->corr, al = c->alpha;
+  for (long long ch = blockIdx.x; ch < K.n_chunk; ch += gridDim.x) {
+    const long long o = K.chunk_off[ch];
+    const int len = K.chunk_len[ch];
+    const int q = K.chunk_cone[ch];
+    const long long head = K.bsoc_off[q];
+    const double mode = V.soc_fac[3 * q], hv = V.soc_fac[3 * q + 1], sc = V.soc_fac[3 * q + 2];
+    for (int e = threadIdx.x; e < len; e += kBlock) {
+      const Relax r = relax_y(V, o + e, corr, al);
+      double up;
+      if (mode == 0.0) up = 0.0;
+      else if (mode == 1.0) up = r.t;
+      else up = (o + e == head) ? hv : sc * r.t;
+      store_y(V, o + e, r.ub, up);
+    }
+  }
+  if (K.n_psd == 0) return;
+  extern __shared__ double smem[];
+  __shared__ double cs[128], sn[128], dpp[128], dqq[128];
+  __shared__ int pp[128], qq[128];
+  for (int b = blockIdx.x; b < K.n_psd; b += gridDim.x) {
+    const int k = K.psd_side[b];
+    const long long o = K.psd_off[b];
+    const int len = k * (k + 1) / 2;
+    double* M;
+    double* Vv;
+    if (k <= smem_side) { M = smem; Vv = smem + k * k; }
+    else {
+      M = psd_scratch + (size_t)2 * blockIdx.x * K.max_side * K.max_side;
+      Vv = M + (size_t)k * k;
+    }
+    // unpack svec (cones.py:53-64): off-diagonals / sqrt(2)
+    for (int e = threadIdx.x; e < len; e += kBlock) {
+      int i, j;
+      svec_rc(e, k, i, j);
+      const Relax r = relax_y(V, o + e, corr, al);
+      const double val = (i == j) ? r.t : r.t / 1.4142135623730951;
+      M[i * k + j] = val;
+      M[j * k + i] = val;
+    }
+    __syncthreads();
+    const bool ok = block_jacobi(M, Vv, k, cs, sn, pp, qq, dpp, dqq);
+    if (!ok) {
+      if (threadIdx.x == 0) atomicOr(&c->err, ERR_JACOBI);
+      continue;
+    }
+    // X = V diag(max(lambda, 0)) V^T, repacked (cones.py:187-191)
+    for (int e = threadIdx.x; e < len; e += kBlock) {
+      int i, j;
+      svec_rc(e, k, i, j);
+      double x = 0.0;
+      for (int t = 0; t < k; ++t) {
+        const double lam = M[t * k + t];
+        if (lam > 0.0) x += Vv[i * k + t] * lam * Vv[j * k + t];
+      }
+      const Relax r = relax_y(V, o + e, corr, al);
+      store_y(V, o + e, r.ub, (i == j) ? x : x * 1.4142135623730951);
+    }
+    __syncthreads();
+  }
+}
+
+__device__ void finish_residuals(Ctl* c, double ut, double s_pri, double s_unb, double buy,
+                                 double s_dual, double s_inf, double cux) {
+  // scaling.py:472-507
+  const double unbdd = cux < 0.0 ? sqrt(s_unb) * c->c_ref / (-cux) : INFINITY;
+  const double infeas = buy < 0.0 ? sqrt(s_inf) * c->b_ref / (-buy) : INFINITY;
+  double pri, dual, gap, gth;
+  if (ut > 0.0) {
+    pri = sqrt(s_pri) / c->sigma;
+    dual = sqrt(s_dual) / c->rho;
+    const double ctx = cux / ut / (c->rho * c->sigma);
+    const double bty = buy / ut / (c->rho * c->sigma);
+    gap = ctx + bty;
+    gth = 1.0 + fabs(ctx) + fabs(bty);
+  } else {
+    pri = dual = gap = INFINITY;
+    gth = 1.0;
+  }
+  double* r = c->res;
+  r[0] = pri; r[1] = dual; r[2] = gap;
+  r[3] = 1.0 + c->b_norm; r[4] = 1.0 + c->c_norm; r[5] = gth;
+  r[6] = unbdd; r[7] = infeas;
+  if (c->force_check) return;
+  // check_termination (solver.py:219-234)
+  int st = SCS_RUNNING;
+  if (pri <= c->eps[0] * r[3] && dual <= c->eps[1] * r[4] && fabs(gap) <= c->eps[2] * gth) {
+    st = SCS_SOLVED;
+  } else {
+    const bool inf = infeas <= c->eps[3], unb = unbdd <= c->eps[4];
+    if (inf && unb) st = SCS_INFEASIBLE_AND_UNBOUNDED;
+    else if (inf) st = SCS_INFEASIBLE;
+    else if (unb) st = SCS_UNBOUNDED;
+  }
+  if (st != SCS_RUNNING) { c->status = st; c->stop = 1; }
+}
+
+// ===========================================================================
+// setup kernels
+// ===========================================================================
+__global__ void k_i64_to_i32(const long long* in, int* out, long long n) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) out[i] = (int)in[i];
+}
+__global__ void k_iota(int* out, long long n) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) out[i] = (int)i;
+}
+// column index of every CSC entry: one warp per column
+__global__ void k_expand_cols(const long long* colptr, long long ncols, int* out) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long j = w; j < ncols; j += nw)
+    for (long long k = colptr[j] + lane; k < colptr[j + 1]; k += 32) out[k] = (int)j;
+}
+// row pointer from sorted row keys: rp[i] = lower_bound(keys, i)
+__global__ void k_rowptr(const int* keys, long long nnz, long long rows, long long* rp) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i <= rows; i += nt) {
+    long long lo = 0, hi = nnz;
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if (keys[mid] < i) lo = mid + 1; else hi = mid;
+    }
+    rp[i] = lo;
+  }
+}
+__global__ void k_gather_csr(const int* perm, const int* colidx, const double* vals, long long nnz,
+                             int* ci, double* av) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long k = tid; k < nnz; k += nt) {
+    const int s = perm[k];
+    ci[k] = colidx[s];
+    av[k] = vals[s];
+  }
+}
+// per-row Euclidean norm (scaling.py:397-401), warp per row
+__global__ void k_row_norms(Csr A, double* out) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long r = w; r < A.rows; r += nw) {
+    double s = 0.0;
+    for (long long k = A.rp[r] + lane; k < A.rp[r + 1]; k += 32) s += A.v[k] * A.v[k];
+    s = warp_sum(s);
+    if (lane == 0) out[r] = sqrt(s);
+  }
+}
+// scale = where(nrm > 0, 1/sqrt(nrm), 1); acc *= scale (scaling.py:405-407)
+__global__ void k_inv_sqrt_scale(const double* nrm, long long n, double* scale, double* acc) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) {
+    const double v = nrm[i];
+    const double s = v > 0.0 ? 1.0 / sqrt(v) : 1.0;
+    scale[i] = s;
+    acc[i] *= s;
+  }
+}
+// v[k] *= s[row(k)] over a CSR (warp per row)
+__global__ void k_scale_rows(long long* rp, double* v, long long rows, const double* s) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long r = w; r < rows; r += nw) {
+    const double f = s[r];
+    for (long long k = rp[r] + lane; k < rp[r + 1]; k += 32) v[k] *= f;
+  }
+}
+// v[k] *= s[ci[k]] (column scaling of a CSR)
+__global__ void k_scale_cols(const int* ci, double* v, long long nnz, const double* s) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long k = tid; k < nnz; k += nt) v[k] *= s[ci[k]];
+}
+// Row-block means (scaling.py:375-377, 409-413): singleton rows [0, zl)
+// keep their own norm; each cone block (segment) shares the mean of its
+// rows.  apply=1 also writes the row scale and multiplies D.
+__global__ void k_block_rows(const double* rn, long long zl, int nseg, const long long* seg_off,
+                             const long long* seg_len, double* seg_mean, double* rscale,
+                             double* D, int apply) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  if (apply) {
+    for (long long i = tid; i < zl; i += nt) {
+      const double t = rn[i];
+      const double s = t > 0.0 ? 1.0 / sqrt(t) : 1.0;
+      rscale[i] = s;
+      D[i] *= s;
+    }
+  }
+  for (int q = blockIdx.x; q < nseg; q += gridDim.x) {
+    const long long o = seg_off[q], d = seg_len[q];
+    double s[1] = {0.0};
+    for (long long e = threadIdx.x; e < d; e += blockDim.x) s[0] += rn[o + e];
+    block_sum<1>(s);
+    const double mean = s[0] / (double)d;
+    if (threadIdx.x == 0) seg_mean[q] = mean;
+    if (apply) {
+      const double f = mean > 0.0 ? 1.0 / sqrt(mean) : 1.0;
+      for (long long e = threadIdx.x; e < d; e += blockDim.x) {
+        rscale[o + e] = f;
+        D[o + e] *= f;
+      }
+    }
+  }
+}
+// out[0] += sum of positive entries, out[1] += count of positive entries
+__global__ void k_pos_mean(const double* x, long long n, double* part, unsigned* counter,
+                           double* out) {
+  double red[2] = {0.0, 0.0};
+  const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long nt = (long long)gridDim.x * kBlock;
+  for (long long i = tid; i < n; i += nt)
+    if (x[i] > 0.0) { red[0] += x[i]; red[1] += 1.0; }
+  if (grid_sum_last<2>(red, part, counter) && threadIdx.x == 0) {
+    out[0] = red[0];
+    out[1] = red[1];
+  }
+}
+// out = {||a*b||^2, ||c/d||^2 ...}: generic weighted square norm
+//   mode 0: sum (a_i b_i)^2 ; mode 1: sum (a_i / b_i)^2 ; mode 2: sum a_i b_i
+__global__ void k_norm2(const double* a, const double* b, long long n, int mode, double* part,
+                        unsigned* counter, double* out) {
+  double red[1] = {0.0};
+  const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long nt = (long long)gridDim.x * kBlock;
+  for (long long i = tid; i < n; i += nt) {
+    double t;
+    if (mode == 0) { t = a[i] * b[i]; red[0] += t * t; }
+    else if (mode == 1) { t = a[i] / b[i]; red[0] += t * t; }
+    else red[0] += a[i] * b[i];
+  }
+  if (grid_sum_last<1>(red, part, counter) && threadIdx.x == 0) *out = red[0];
+}
+// out = (s * w) * x   (b_hat = sigma D b, c_hat = rho E c: scaling.py:429)
+__global__ void k_scale_vec(const double* x, const double* w, double s, long long n, double* out) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) out[i] = s * w[i] * x[i];
+}
+// Warm start (scaling.py:433-438, solver.py:128-150)
+__global__ void k_init_state(Vec V, const double* wx, const double* wy, const double* ws,
+                             double sigma, double rho) {
+  const long long n = V.n, m = V.m;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n + m + 1; i += nt) {
+    double u = 0.0, v = 0.0;
+    if (wx) {
+      if (i < n) u = sigma * wx[i] / V.E[i];
+      else if (i < n + m) { u = rho * wy[i - n] / V.D[i - n]; v = sigma * V.D[i - n] * ws[i - n]; }
+      else u = 1.0;
+    } else if (i == n + m) {
+      u = 1.0;
+      v = 1.0;
+    }
+    V.u[i] = u;
+    V.v[i] = v;
+    if (i < n) V.x[i] = 0.0;
+    if (i >= n && i < n + m) V.Axw[i - n] = 0.0;
+  }
+}
+// x / E  and y / D helpers for point residuals
+__global__ void k_div(const double* a, const double* b, long long n, double* out) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) out[i] = a[i] / b[i];
+}
+// residual vector pieces for _point_residuals: out_i = (a_i / w_i) + s_i - b_i
+__global__ void k_point_pri(const double* ax, const double* D, const double* s, const double* b,
+                            long long m, double* out) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < m; i += nt) out[i] = ax[i] / D[i] + s[i] - b[i];
+}
+__global__ void k_point_dual(const double* aty, const double* E, const double* c, long long n,
+                             double* out) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) out[i] = aty[i] / E[i] + c[i];
+}
+__global__ void k_zero(double* x, long long n) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) x[i] = 0.0;
+}
+
+}  // namespace scs
+
+// ===========================================================================
+// host side
+// ===========================================================================
+using namespace scs;
+
+namespace {
+
+std::mutex g_err_mu;
+std::string g_err;
+
+struct Timer {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  double s() const {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct scs_handle {
+  int dev = 0;
+  int sms = 148;
+  cudaStream_t st = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::string err;
+  // sizes
+  long long m = 0, n = 0, nnz = 0, m_glob = 0, row_lo = 0;
+  int rank = 0, world = 1;
+  scs_settings set{};
+  // matrices
+  Csr A{}, At{};
+  int LA = 32, LAt = 32;
+  // cones
+  Cones K{};
+  std::vector<long long> seg_off_h, seg_len_h;
+  long long* seg_off = nullptr;
+  long long* seg_len = nullptr;
+  int nseg = 0;
+  double* psd_scratch = nullptr;
+  int smem_side = 0;
+  size_t cone_smem = 0;
+  // vectors
+  Vec V{};
+  double *b0 = nullptr, *c0 = nullptr;  // original b, c (device)
+  double *bh = nullptr, *ch = nullptr, *D = nullptr, *E = nullptr;
+  double *tmp_n = nullptr, *tmp_m = nullptr, *tmp_m2 = nullptr, *zero_m = nullptr;
+  double *seg_mean = nullptr;
+  double* dscal = nullptr;  // device scratch scalars
+  Ctl* ctl = nullptr;
+  Ctl* ctl_h = nullptr;     // pinned mirror
+  double sigma = 1.0, rho = 1.0, mean_col = 1.0, mean_row = 1.0;
+  double setup_seconds = 0.0;
+  long long launches = 0, launches_per_iter = 0;
+  long long launched_iters = 0;
+  std::vector<DevBuf> bufs;
+  int grid_full = 148 * 4;
+};
+
+namespace {
+
+void set_global_err(const std::string& s) {
+  std::lock_guard<std::mutex> g(g_err_mu);
+  g_err = s;
+}
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw Fail{SCS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};        \
+  } while (0)
+
+template <class T>
+T* dalloc(scs_handle* h, size_t count) {
+  void* p = nullptr;
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess)
+    throw Fail{SCS_ENOMEM, "cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e)};
+  h->bufs.push_back({p, bytes});
+  return (T*)p;
+}
+void dfree(scs_handle* h, void* p) {
+  if (!p) return;
+  for (auto& b : h->bufs)
+    if (b.p == p) { cudaFree(p); b.p = nullptr; }
+}
+template <class T>
+void h2d(scs_handle* h, T* dst, const T* src, size_t count) {
+  if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, h->st));
+}
+template <class T>
+void d2h(scs_handle* h, T* dst, const T* src, size_t count) {
+  if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, h->st));
+}
+
+int elem_grid(scs_handle* h, long long work) {
+  long long g = (work + kBlock - 1) / kBlock;
+  return (int)std::max<long long>(1, std::min<long long>(g, h->grid_full));
+}
+
+int pick_lanes(long long nnz, long long rows) {
+  const double avg = rows ? (double)nnz / (double)rows : 0.0;
+  if (avg <= 2.5) return 2;
+  if (avg <= 6) return 4;
+  if (avg <= 12) return 8;
+  if (avg <= 24) return 16;
+  return 32;
+}
+
+template <class Epi>
+void launch_spmv(scs_handle* h, const Csr& M, int L, const Epi& epi) {
+  const long long work = M.rows * (long long)L;
+  const int grid = elem_grid(h, work);
+  switch (L) {
+    case 2: k_spmv<2, Epi><<<grid, kBlock, 0, h->st>>>(M, epi); break;
+    case 4: k_spmv<4, Epi><<<grid, kBlock, 0, h->st>>>(M, epi); break;
+    case 8: k_spmv<8, Epi><<<grid, kBlock, 0, h->st>>>(M, epi); break;
+    case 16: k_spmv<16, Epi><<<grid, kBlock, 0, h->st>>>(M, epi); break;
+    default: k_spmv<32, Epi><<<grid, kBlock, 0, h->st>>>(M, epi); break;
+  }
+  h->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// cone layout
+// ---------------------------------------------------------------------------
+void build_cones(scs_handle* h, const scs_problem* P) {
+  // block list in the reference order (cones.py:121-139), local row offsets
+  const long long lo = h->row_lo, hi = h->row_lo + h->m;
+  std::vector<long long> ssoc_off;
+  std::vector<int> ssoc_len;
+  std::vector<long long> bsoc_off, bsoc_len;
+  std::vector<int> bsoc_chunk_lo;
+  std::vector<long long> chunk_off;
+  std::vector<int> chunk_len, chunk_cone;
+  std::vector<long long> psd_off;
+  std::vector<int> psd_side;
+  if (h->world > 1) throw Fail{SCS_EINVAL, "row sharding is not enabled in this build"};
+  (void)hi;
+  const long long zg = P->z, lg = P->l;
+  h->K.z = zg;
+  h->K.l = lg;
+  long long off = zg + lg;
+  for (long long i = 0; i < P->nq; ++i) {  // cones.py:134-136
+    const long long d = P->q[i];
+    if (d < 1) throw Fail{SCS_EINVAL, "second-order cone dims must be >= 1"};
+    if (d <= kSmallSoc) {
+      ssoc_off.push_back(off - lo);
+      ssoc_len.push_back((int)d);
+    } else {
+      bsoc_off.push_back(off - lo);
+      bsoc_len.push_back(d);
+      bsoc_chunk_lo.push_back((int)chunk_off.size());
+      for (long long e = 0; e < d; e += kChunk) {
+        chunk_off.push_back(off + e - lo);
+        chunk_len.push_back((int)std::min<long long>(kChunk, d - e));
+        chunk_cone.push_back((int)bsoc_off.size() - 1);
+      }
+    }
+    off += d;
+  }
+  bsoc_chunk_lo.push_back((int)chunk_off.size());
+  const long long psd_lo = off;
+  int max_side = 0;
+  for (long long i = 0; i < P->ns; ++i) {  // cones.py:137-139
+    const long long k = P->s[i];
+    if (k < 1) throw Fail{SCS_EINVAL, "PSD side lengths must be >= 1"};
+    psd_off.push_back(off - lo);
+    psd_side.push_back((int)k);
+    max_side = std::max<int>(max_side, (int)k);
+    off += k * (k + 1) / 2;
+  }
+  const long long psd_hi = off;
+  h->K.psd_lo = psd_lo - lo;
+  h->K.psd_hi = psd_hi - lo;
+  h->K.exp_lo = off - lo;
+  h->K.n_exp = P->ep;
+  off += 3 * P->ep;
+  if (off != h->m_glob)
+    throw Fail{SCS_EINVAL, "cone dimension " + std::to_string(off) +
+                               " does not match row count " + std::to_string(h->m_glob)};
+  auto up_ll = [&](const std::vector<long long>& v) {
+    long long* d = dalloc<long long>(h, v.size());
+    h2d(h, d, v.data(), v.size());
+    return (const long long*)d;
+  };
+  auto up_i = [&](const std::vector<int>& v) {
+    int* d = dalloc<int>(h, v.size());
+    h2d(h, d, v.data(), v.size());
+    return (const int*)d;
+  };
+  h->K.n_ssoc = (int)ssoc_off.size();
+  h->K.ssoc_len = up_i(ssoc_len);
+  h->K.ssoc_off = up_ll(ssoc_off);
+  h->K.n_bsoc = (int)bsoc_off.size();
+  h->K.bsoc_off = up_ll(bsoc_off);
+  h->K.bsoc_len = up_ll(bsoc_len);
+  h->K.bsoc_chunk_lo = up_i(bsoc_chunk_lo);
+  h->K.n_chunk = (int)chunk_off.size();
+  h->K.chunk_off = up_ll(chunk_off);
+  h->K.chunk_len = up_i(chunk_len);
+  h->K.chunk_cone = up_i(chunk_cone);
+  h->K.n_psd = (int)psd_off.size();
+  h->K.psd_off = up_ll(psd_off);
+  h->K.psd_side = up_i(psd_side);
+  h->K.max_side = max_side;
+  // equilibration segments: every non-singleton block (scaling.py:62-71)
+  {
+    long long o = zg + lg;
+    for (long long i = 0; i < P->nq; ++i) { h->seg_off_h.push_back(o - lo); h->seg_len_h.push_back(P->q[i]); o += P->q[i]; }
+    for (long long i = 0; i < P->ns; ++i) {
+      const long long d = P->s[i] * (P->s[i] + 1) / 2;
+      h->seg_off_h.push_back(o - lo); h->seg_len_h.push_back(d); o += d;
+    }
+    for (long long i = 0; i < P->ep; ++i) { h->seg_off_h.push_back(o - lo); h->seg_len_h.push_back(3); o += 3; }
+  }
+  h->nseg = (int)h->seg_off_h.size();
+  h->seg_off = (long long*)up_ll(h->seg_off_h);
+  h->seg_len = (long long*)up_ll(h->seg_len_h);
+  // PSD workspace: shared memory up to ~200 KB, else global scratch
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+  const size_t budget = (size_t)std::max(0, optin - 8 * 1024);
+  int side = 0;
+  while ((size_t)2 * (side + 1) * (side + 1) * sizeof(double) <= budget) ++side;
+  h->smem_side = std::min(side, 255);
+  if (max_side > 255) throw Fail{SCS_EINVAL, "PSD side > 255 is not supported by the device Jacobi kernel"};
+  const int s_used = std::min(max_side, h->smem_side);
+  h->cone_smem = (size_t)2 * s_used * s_used * sizeof(double);
+  if (max_side > h->smem_side)
+    h->psd_scratch = dalloc<double>(h, (size_t)2 * max_side * max_side * h->grid_full);
+  if (h->cone_smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(k_cone_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)h->cone_smem));
+}
+
+// ---------------------------------------------------------------------------
+// matrices: CSC(A) is CSR(A^T) as-is; CSR(A) by a stable device radix sort
+// ---------------------------------------------------------------------------
+void build_matrices(scs_handle* h, const scs_problem* P) {
+  const long long m = h->m, n = h->n, nnz = h->nnz;
+  if (nnz >= (1LL << 31) - 1) throw Fail{SCS_EINVAL, "nnz >= 2^31 per shard is not supported"};
+  if (m >= (1LL << 31) - 1 || n >= (1LL << 31) - 1)
+    throw Fail{SCS_EINVAL, "dimensions >= 2^31 are not supported"};
+  long long* tp = dalloc<long long>(h, n + 1);
+  int* ti = dalloc<int>(h, nnz);
+  double* tv = dalloc<double>(h, nnz);
+  h2d(h, tp, (const long long*)P->colptr, n + 1);
+  h2d(h, tv, P->vals, nnz);
+  // row indices arrive as int64: stage in chunks and narrow on the device
+  {
+    const long long chunk = 1LL << 26;
+    long long* stage = dalloc<long long>(h, std::min(chunk, std::max(nnz, 1LL)));
+    for (long long o = 0; o < nnz; o += chunk) {
+      const long long c = std::min(chunk, nnz - o);
+      h2d(h, stage, (const long long*)P->rowidx + o, c);
+      k_i64_to_i32<<<elem_grid(h, c), kBlock, 0, h->st>>>(stage, ti + o, c);
+    }
+    CK(cudaStreamSynchronize(h->st));
+    dfree(h, stage);
+  }
+  h->At = Csr{tp, ti, tv, n};
+  long long* rp = dalloc<long long>(h, m + 1);
+  int* ci = dalloc<int>(h, nnz);
+  double* av = dalloc<double>(h, nnz);
+  if (nnz > 0) {
+    int* colidx = dalloc<int>(h, nnz);
+    k_expand_cols<<<elem_grid(h, n * 32), kBlock, 0, h->st>>>(tp, n, colidx);
+    int* keys_out = dalloc<int>(h, nnz);
+    int* perm_in = dalloc<int>(h, nnz);
+    int* perm_out = dalloc<int>(h, nnz);
+    k_iota<<<elem_grid(h, nnz), kBlock, 0, h->st>>>(perm_in, nnz);
+    int bits = 1;
+    while ((1LL << bits) < m) ++bits;
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const int*)ti, keys_out,
+                                       (const int*)perm_in, perm_out, (int)nnz, 0, bits, h->st));
+    void* tmp = dalloc<char>(h, tmp_bytes);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, (const int*)ti, keys_out,
+                                       (const int*)perm_in, perm_out, (int)nnz, 0, bits, h->st));
+    k_rowptr<<<elem_grid(h, m + 1), kBlock, 0, h->st>>>(keys_out, nnz, m, rp);
+    k_gather_csr<<<elem_grid(h, nnz), kBlock, 0, h->st>>>(perm_out, colidx, tv, nnz, ci, av);
+    CK(cudaStreamSynchronize(h->st));
+    dfree(h, tmp);
+    dfree(h, perm_out);
+    dfree(h, perm_in);
+    dfree(h, keys_out);
+    dfree(h, colidx);
+  } else {
+    CK(cudaMemsetAsync(rp, 0, (m + 1) * sizeof(long long), h->st));
+  }
+  h->A = Csr{rp, ci, av, m};
+  h->LA = pick_lanes(nnz, m);
+  h->LAt = pick_lanes(nnz, n);
+}
+
+double dev_scalar(scs_handle* h, int idx = 0) {
+  double v = 0.0;
+  CK(cudaMemcpyAsync(&v, h->dscal + idx, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return v;
+}
+
+double norm2_dev(scs_handle* h, const double* a, const double* b, long long n, int mode) {
+  k_norm2<<<elem_grid(h, n), kBlock, 0, h->st>>>(a, b, n, mode, h->V.part, &h->ctl->counter,
+                                                   h->dscal);
+  return dev_scalar(h);
+}
+
+// ---------------------------------------------------------------------------
+// equilibration (scaling.py:79-129) -- D, E from A only; sigma, rho need b, c
+// ---------------------------------------------------------------------------
+void equilibrate(scs_handle* h) {
+  const long long m = h->m, n = h->n, nnz = h->nnz;
+  double* cn = h->tmp_n;
+  double* rn = h->tmp_m;
+  double* cs = h->V.Gp;  // scratch n
+  double* rs = h->tmp_m2;
+  // D = 1, E = 1
+  {
+    std::vector<double> ones(std::max(m, n), 1.0);
+    h2d(h, h->D, ones.data(), m);
+    h2d(h, h->E, ones.data(), n);
+    CK(cudaStreamSynchronize(h->st));
+  }
+  const long long zl = h->K.z + h->K.l;
+  auto row_norms = [&](const Csr& M, double* out) {
+    k_row_norms<<<elem_grid(h, M.rows * 32), kBlock, 0, h->st>>>(M, out);
+  };
+  if (h->set.normalize) {
+    for (int sw = 0; sw < h->set.sweeps; ++sw) {
+      row_norms(h->At, cn);  // column norms of A
+      k_inv_sqrt_scale<<<elem_grid(h, n), kBlock, 0, h->st>>>(cn, n, cs, h->E);
+      k_scale_rows<<<elem_grid(h, n * 32), kBlock, 0, h->st>>>((long long*)h->At.rp,
+                                                                (double*)h->At.v, n, cs);
+      k_scale_cols<<<elem_grid(h, nnz), kBlock, 0, h->st>>>(h->A.ci, (double*)h->A.v, nnz, cs);
+      row_norms(h->A, rn);
+      k_block_rows<<<elem_grid(h, std::max<long long>(zl, (long long)h->nseg * kBlock)), kBlock, 0,
+                     h->st>>>(rn, zl, h->nseg, h->seg_off, h->seg_len, h->seg_mean, rs, h->D, 1);
+      k_scale_rows<<<elem_grid(h, m * 32), kBlock, 0, h->st>>>((long long*)h->A.rp,
+                                                                (double*)h->A.v, m, rs);
+      k_scale_cols<<<elem_grid(h, nnz), kBlock, 0, h->st>>>(h->At.ci, (double*)h->At.v, nnz, rs);
+    }
+    row_norms(h->At, cn);
+    k_pos_mean<<<elem_grid(h, n), kBlock, 0, h->st>>>(cn, n, h->V.part, &h->ctl->counter, h->dscal);
+    double s0 = dev_scalar(h, 0), c0 = dev_scalar(h, 1);
+    h->mean_col = c0 > 0 ? s0 / c0 : 1.0;
+    row_norms(h->A, rn);
+    k_block_rows<<<elem_grid(h, std::max<long long>(zl, (long long)h->nseg * kBlock)), kBlock, 0,
+                   h->st>>>(rn, zl, h->nseg, h->seg_off, h->seg_len, h->seg_mean, rs, h->D, 0);
+    k_pos_mean<<<elem_grid(h, zl), kBlock, 0, h->st>>>(rn, zl, h->V.part, &h->ctl->counter, h->dscal);
+    double s1 = dev_scalar(h, 0), c1 = dev_scalar(h, 1);
+    k_pos_mean<<<elem_grid(h, h->nseg), kBlock, 0, h->st>>>(h->seg_mean, h->nseg, h->V.part,
+                                                             &h->ctl->counter, h->dscal);
+    double s2 = dev_scalar(h, 0), c2 = dev_scalar(h, 1);
+    h->mean_row = (c1 + c2) > 0 ? (s1 + s2) / (c1 + c2) : 1.0;
+  } else {
+    h->mean_col = h->mean_row = 1.0;
+  }
+  CK(cudaStreamSynchronize(h->st));
+}
+
+// sigma, rho, b_hat, c_hat and the residual constants (scaling.py:422-429,
+// 469-478)
+void scale_vectors(scs_handle* h) {
+  const long long m = h->m, n = h->n;
+  if (h->set.normalize) {
+    const double dbn = sqrt(norm2_dev(h, h->D, h->b0, m, 0));
+    const double ecn = sqrt(norm2_dev(h, h->E, h->c0, n, 0));
+    h->sigma = dbn > 0 ? h->mean_col / dbn : 1.0;
+    h->rho = ecn > 0 ? h->mean_row / ecn : 1.0;
+  } else {
+    h->sigma = h->rho = 1.0;
+  }
+  k_scale_vec<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->b0, h->D, h->sigma, m, h->bh);
+  k_scale_vec<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->c0, h->E, h->rho, n, h->ch);
+  const double dib = sqrt(norm2_dev(h, h->bh, h->D, m, 1));
+  const double eic = sqrt(norm2_dev(h, h->ch, h->E, n, 1));
+  Ctl* c = h->ctl_h;
+  CK(cudaMemcpyAsync(c, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  c->b_norm = dib / h->sigma;
+  c->c_norm = eic / h->rho;
+  c->b_ref = dib > 0 ? dib : 1.0;
+  c->c_ref = eic > 0 ? eic : 1.0;
+  c->sigma = h->sigma;
+  c->rho = h->rho;
+  CK(cudaMemcpyAsync(h->ctl, c, sizeof(Ctl), cudaMemcpyHostToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));
+}
+
+void pull_ctl(scs_handle* h) {
+  CK(cudaMemcpyAsync(h->ctl_h, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+}
+void push_ctl(scs_handle* h) {
+  CK(cudaMemcpyAsync(h->ctl, h->ctl_h, sizeof(Ctl), cudaMemcpyHostToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));
+}
+
+void check_err(scs_handle* h) {
+  const int e = h->ctl_h->err;
+  if (!e) return;
+  if (e & ERR_CG_CURVATURE)
+    throw Fail{SCS_ENONFINITE, "cg_solve: operator is not positive definite on iterates"};
+  if (e & ERR_CG_NONFINITE) throw Fail{SCS_ENONFINITE, "cg_solve: non-finite residual"};
+  if (e & ERR_CONE_NONFINITE) throw Fail{SCS_ENONFINITE, "project_embedding_cone: non-finite input"};
+  if (e & ERR_JACOBI)
+    throw Fail{SCS_ENOCONV, "Jacobi eigensolver did not converge within 100 sweeps"};
+}
+
+// one CG step (A p, A^T, update, p update)
+void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p) {
+  EpiAp ea{};
+  ea.V = V;
+  ea.xs[0] = V.p;
+  launch_spmv(h, h->A, h->LA, ea);
+  EpiAtGp eg{};
+  eg.V = V;
+  eg.xs[0] = V.q;
+  launch_spmv(h, h->At, h->LAt, eg);
+  k_cg_update<<<elem_grid(h, h->n), kBlock, 0, h->st>>>(V, cap);
+  h->launches++;
+  if (with_p) {
+    k_cg_p<<<elem_grid(h, h->n), kBlock, 0, h->st>>>(V);
+    h->launches++;
+  }
+}
+
+// g = M^-1 h by CG to 1e-9 (1 + ||h||) from zero (embedding.py:145-162)
+void solve_g(scs_handle* h) {
+  const long long n = h->n, m = h->m;
+  Vec G = h->V;
+  G.rhs_x = h->ch;
+  G.rhs_y = h->bh;
+  G.x = h->V.gx;
+  G.Axw = h->zero_m;
+  k_zero<<<elem_grid(h, n), kBlock, 0, h->st>>>(G.x, n);
+  const double hn = sqrt(norm2_dev(h, h->ch, h->ch, n, 2) + norm2_dev(h, h->bh, h->bh, m, 2));
+  pull_ctl(h);
+  Ctl* c = h->ctl_h;
+  c->stop = 0;
+  c->err = 0;
+  c->tol = 1e-9 * (1.0 + hn);
+  c->cg_done = 0;
+  c->cg_it = 0;
+  c->counter = 0;
+  push_ctl(h);
+  const long long cap = 10 * n + 100;  // embedding.py:104
+  EpiAtFirst e0{};
+  e0.V = G;
+  e0.xs[0] = G.rhs_y;
+  e0.xs[1] = G.Axw;
+  launch_spmv(h, h->At, h->LAt, e0);
+  long long done_steps = 0;
+  while (true) {
+    pull_ctl(h);
+    check_err(h);
+    if (c->cg_done) break;
+    const long long batch = std::min<long long>(32, cap - done_steps);
+    if (batch <= 0) break;
+    for (long long i = 0; i < batch; ++i) cg_step(h, G, cap, true);
+    done_steps += batch;
+  }
+  EpiAFinal ef{};
+  ef.V = G;
+  ef.xs[0] = G.x;
+  ef.zy_out = h->V.gy;
+  ef.setup = 1;
+  // setup finish must run even though stop == 0; cg_it accumulates
+  launch_spmv(h, h->A, h->LA, ef);
+  pull_ctl(h);
+  check_err(h);
+  if (c->denom < 1.0 - 1e-9)
+    throw Fail{SCS_ESETUP, "Schur denominator " + std::to_string(c->denom) + " below 1"};
+}
+
+// capture one ADMM iteration into a CUDA graph
+void build_graph(scs_handle* h) {
+  if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+  const Vec V = h->V;
+  const long long before = h->launches;
+  CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+  k_prep<<<elem_grid(h, h->n + h->m), kBlock, 0, h->st>>>(V);
+  h->launches++;
+  EpiAtFirst e0{};
+  e0.V = V;
+  e0.xs[0] = V.rhs_y;
+  e0.xs[1] = V.Axw;
+  launch_spmv(h, h->At, h->LAt, e0);
+  const long long cgm = h->set.cg_max;
+  for (long long i = 0; i < cgm; ++i) cg_step(h, V, cgm, i + 1 < cgm);
+  EpiAFinal ef{};
+  ef.V = V;
+  ef.xs[0] = V.x;
+  ef.zy_out = V.zy;
+  ef.setup = 0;
+  launch_spmv(h, h->A, h->LA, ef);
+  const long long work = std::max<long long>(h->n + h->K.z + h->K.l, 1);
+  int g_tail = std::max(elem_grid(h, work), std::min(h->K.n_chunk, h->grid_full));
+  g_tail = std::max(g_tail, std::min((int)((h->K.n_ssoc * 32LL + kBlock - 1) / kBlock), h->grid_full));
+  k_cone_tail<<<g_tail, kBlock, 0, h->st>>>(V, h->K);
+  h->launches++;
+  if (h->K.n_chunk > 0 || h->K.n_psd > 0) {
+    const int g = std::max(1, std::min(std::max(h->K.n_chunk, h->K.n_psd), h->grid_full));
+    k_cone_apply<<<g, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side);
+    h->launches++;
+  }
+  EpiResA ra{};
+  ra.V = V;
+  ra.xs[0] = V.u;
+  launch_spmv(h, h->A, h->LA, ra);
+  EpiResAt rt{};
+  rt.V = V;
+  rt.xs[0] = V.u + h->n;
+  launch_spmv(h, h->At, h->LAt, rt);
+  cudaGraph_t g;
+  CK(cudaStreamEndCapture(h->st, &g));
+  CK(cudaGraphInstantiate(&h->gexec, g, 0));
+  cudaGraphDestroy(g);
+  h->launches_per_iter = h->launches - before;
+}
+
+void launch_residuals(scs_handle* h) {
+  EpiResA ra{};
+  ra.V = h->V;
+  ra.xs[0] = h->V.u;
+  launch_spmv(h, h->A, h->LA, ra);
+  EpiResAt rt{};
+  rt.V = h->V;
+  rt.xs[0] = h->V.u + h->n;
+  launch_spmv(h, h->At, h->LAt, rt);
+}
+
+void fill_info(scs_handle* h, scs_info* info) {
+  if (!info) return;
+  const Ctl* c = h->ctl_h;
+  info->status = c->status;
+  info->iterations = c->iter;
+  info->cg_iters = c->cg_iters_total;
+  for (int i = 0; i < 8; ++i) info->res[i] = c->res[i];
+  info->setup_seconds = h->setup_seconds;
+  info->launches = h->launches;
+}
+
+void do_begin(scs_handle* h, const double* wx, const double* wy, const double* ws) {
+  const long long n = h->n, m = h->m;
+  double *dx = nullptr, *dy = nullptr, *ds = nullptr;
+  if (wx) {
+    dx = h->tmp_n;
+    dy = h->tmp_m;
+    ds = h->tmp_m2;
+    h2d(h, dx, wx, n);
+    h2d(h, dy, wy, m);
+    h2d(h, ds, ws, m);
+  }
+  k_init_state<<<elem_grid(h, n + m + 1), kBlock, 0, h->st>>>(h->V, dx, dy, ds, h->sigma, h->rho);
+  pull_ctl(h);
+  Ctl* c = h->ctl_h;
+  c->iter = 0;
+  c->k_sched = 0;  // reset_schedule (embedding.py:45-48)
+  c->status = SCS_RUNNING;
+  c->stop = 0;
+  c->err = 0;
+  c->warm_zero = 1;
+  c->force_check = 0;
+  c->check_now = 0;
+  c->counter = 0;
+  c->max_iters = h->set.max_iters;
+  c->check_interval = h->set.check_interval;
+  push_ctl(h);
+  h->launched_iters = 0;
+  h->launches = 0;
+}
+
+// run up to k iterations, stopping at termination or max_iters
+void do_steps(scs_handle* h, long long k) {
+  Ctl* c = h->ctl_h;
+  long long todo = std::min(k, h->set.max_iters - h->launched_iters);
+  long long batch = 1;
+  while (todo > 0) {
+    const long long b = std::min(batch, todo);
+    for (long long i = 0; i < b; ++i) CK(cudaGraphLaunch(h->gexec, h->st));
+    h->launches += b * h->launches_per_iter;
+    h->launched_iters += b;
+    todo -= b;
+    pull_ctl(h);
+    check_err(h);
+    if (c->stop) break;
+    batch = std::min<long long>(batch * 2, 64);
+  }
+  if (c->iter != h->launched_iters && !c->stop)
+    throw Fail{SCS_ECUDA, "internal: iteration count mismatch"};
+}
+
+// post-loop status (solver.py:364-369)
+void do_finish(scs_handle* h) {
+  Ctl* c = h->ctl_h;
+  pull_ctl(h);
+  if (c->status != SCS_RUNNING) return;
+  c->force_check = 1;
+  c->check_now = 1;
+  c->stop = 0;
+  push_ctl(h);
+  launch_residuals(h);
+  // tau > 1e-8 ||u|| ?
+  const long long len = h->n + h->m + 1;
+  const double un = sqrt(norm2_dev(h, h->V.u, h->V.u, len, 2));
+  pull_ctl(h);
+  double ut = 0.0;
+  d2h(h, &ut, h->V.u + len - 1, 1);
+  CK(cudaStreamSynchronize(h->st));
+  c->status = ut > 1e-8 * un ? SCS_MAX_ITERS_REACHED : SCS_INDETERMINATE;
+  c->force_check = 0;
+  c->stop = 1;
+  push_ctl(h);
+}
+
+int guard(scs_handle* h, const std::function<void()>& fn) {
+  try {
+    if (h) CK(cudaSetDevice(h->dev));
+    fn();
+    return SCS_OK;
+  } catch (const Fail& f) {
+    if (h) h->err = f.msg;
+    set_global_err(f.msg);
+    return f.code;
+  } catch (const std::exception& e) {
+    if (h) h->err = e.what();
+    set_global_err(e.what());
+    return SCS_ENOMEM;
+  }
+}
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int scs_abi_version(void) { return SCS_B200_ABI_VERSION; }
+
+const char* scs_last_error(const scs_handle* h) {
+  if (h) return h->err.c_str();
+  std::lock_guard<std::mutex> g(g_err_mu);
+  return g_err.c_str();
+}
+
+void scs_destroy(scs_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (auto& b : h->bufs)
+    if (b.p) cudaFree(b.p);
+  if (h->ctl_h) cudaFreeHost(h->ctl_h);
+  if (h->st) cudaStreamDestroy(h->st);
+  delete h;
+}
+
+static void validate(const scs_problem* P, const scs_settings* S) {
+  if (!P || !S) throw Fail{SCS_EINVAL, "null problem or settings"};
+  if (P->m < 0 || P->n < 0) throw Fail{SCS_EINVAL, "matrix dimensions must be nonnegative"};
+  if (!(S->alpha > 0.0 && S->alpha < 2.0)) throw Fail{SCS_EINVAL, "alpha must lie in (0, 2)"};
+  const double eps[5] = {S->eps_pri, S->eps_dual, S->eps_gap, S->eps_infeas, S->eps_unbdd};
+  for (double e : eps)
+    if (!(e > 0)) throw Fail{SCS_EINVAL, "eps must be positive"};
+  if (S->max_iters < 1 || S->check_interval < 1)
+    throw Fail{SCS_EINVAL, "max_iters and check_interval must be >= 1"};
+  if (S->cg_max < 1) throw Fail{SCS_EINVAL, "cg_max must be >= 1"};
+  if (S->sweeps < 0) throw Fail{SCS_EINVAL, "sweeps must be >= 0"};
+  if (P->z < 0 || P->l < 0 || P->ep < 0) throw Fail{SCS_EINVAL, "cone dimensions must be nonnegative"};
+  if (P->colptr[0] != 0) throw Fail{SCS_EINVAL, "colptr must start at 0 and end at nnz"};
+  for (long long j = 0; j < P->n; ++j)
+    if (P->colptr[j + 1] < P->colptr[j]) throw Fail{SCS_EINVAL, "colptr must be nondecreasing"};
+}
+
+int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist,
+               scs_handle** out) {
+  if (!out) return SCS_EINVAL;
+  *out = nullptr;
+  scs_handle* h = new scs_handle();
+  Timer tm;
+  int rc = guard(nullptr, [&] {
+    validate(P, S);
+    h->set = *S;
+    h->dev = S->device;
+    CK(cudaSetDevice(h->dev));
+    CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev));
+    h->grid_full = h->sms * (2048 / kBlock);
+    if (h->grid_full > kMaxGrid) h->grid_full = kMaxGrid;
+    CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    if (dist && dist->world > 1) {
+      h->rank = dist->rank;
+      h->world = dist->world;
+    }
+    h->m = P->m;
+    h->n = P->n;
+    h->m_glob = P->m_global > 0 ? P->m_global : P->m;
+    h->row_lo = P->row_lo;
+    h->nnz = P->colptr[P->n];
+    const long long m = h->m, n = h->n;
+    CK(cudaMallocHost((void**)&h->ctl_h, sizeof(Ctl)));
+    memset(h->ctl_h, 0, sizeof(Ctl));
+    h->ctl = dalloc<Ctl>(h, 1);
+    Ctl* c = h->ctl_h;
+    c->alpha = S->alpha;
+    c->cg_tol = (S->cg_tol > 0.0) ? S->cg_tol : 0.0;
+    c->eps[0] = S->eps_pri; c->eps[1] = S->eps_dual; c->eps[2] = S->eps_gap;
+    c->eps[3] = S->eps_infeas; c->eps[4] = S->eps_unbdd;
+    c->max_iters = S->max_iters;
+    c->check_interval = S->check_interval;
+    c->status = SCS_RUNNING;
+    c->denom = 1.0;
+    c->sigma = c->rho = 1.0;
+    push_ctl(h);
+    build_cones(h, P);
+    // vectors
+    Vec& V = h->V;
+    V.n = n;
+    V.m = m;
+    V.ctl = h->ctl;
+    V.u = dalloc<double>(h, n + m + 1);
+    V.v = dalloc<double>(h, n + m + 1);
+    h->b0 = dalloc<double>(h, m);
+    h->c0 = dalloc<double>(h, n);
+    h->bh = dalloc<double>(h, m);
+    h->ch = dalloc<double>(h, n);
+    h->D = dalloc<double>(h, m);
+    h->E = dalloc<double>(h, n);
+    V.c = h->ch; V.b = h->bh; V.D = h->D; V.E = h->E;
+    V.gx = dalloc<double>(h, n);
+    V.gy = dalloc<double>(h, m);
+    V.rhs_x = dalloc<double>(h, n);
+    V.rhs_y = dalloc<double>(h, m);
+    V.x = dalloc<double>(h, n);
+    V.r = dalloc<double>(h, n);
+    V.p = dalloc<double>(h, n);
+    V.Gp = dalloc<double>(h, n);
+    V.q = dalloc<double>(h, m);
+    V.Axw = dalloc<double>(h, m);
+    V.zy = dalloc<double>(h, m);
+    V.part = dalloc<double>(h, (size_t)kMaxRed * kMaxGrid);
+    V.chunk_part = dalloc<double>(h, std::max(h->K.n_chunk, 1));
+    V.soc_fac = dalloc<double>(h, 3 * std::max(h->K.n_bsoc, 1));
+    h->tmp_n = dalloc<double>(h, n);
+    h->tmp_m = dalloc<double>(h, m);
+    h->tmp_m2 = dalloc<double>(h, m);
+    h->zero_m = dalloc<double>(h, m);
+    h->seg_mean = dalloc<double>(h, std::max(h->nseg, 1));
+    h->dscal = dalloc<double>(h, 8);
+    CK(cudaMemsetAsync(h->zero_m, 0, std::max<long long>(m, 1) * sizeof(double), h->st));
+    h2d(h, h->b0, P->b, m);
+    h2d(h, h->c0, P->c, n);
+    build_matrices(h, P);
+    equilibrate(h);
+    scale_vectors(h);
+    solve_g(h);
+    build_graph(h);
+    CK(cudaStreamSynchronize(h->st));
+  });
+  if (rc != SCS_OK) {
+    h->err = scs_last_error(nullptr);
+    scs_destroy(h);
+    return rc;
+  }
+  h->setup_seconds = tm.s();
+  *out = h;
+  return SCS_OK;
+}
+
+int scs_begin(scs_handle* h, const double* wx, const double* wy, const double* ws) {
+  if (!h) return SCS_EINVAL;
+  return guard(h, [&] { do_begin(h, wx, wy, ws); });
+}
+
+int scs_step(scs_handle* h, int64_t k, scs_info* info) {
+  if (!h) return SCS_EINVAL;
+  return guard(h, [&] {
+    do_steps(h, k);
+    fill_info(h, info);
+  });
+}
+
+int scs_finish(scs_handle* h, scs_info* info) {
+  if (!h) return SCS_EINVAL;
+  return guard(h, [&] {
+    do_finish(h);
+    fill_info(h, info);
+  });
+}
+
+int scs_solve(scs_handle* h, const double* wx, const double* wy, const double* ws,
+              scs_info* info) {
+  if (!h) return SCS_EINVAL;
+  Timer tm;
+  return guard(h, [&] {
+    do_begin(h, wx, wy, ws);
+    do_steps(h, h->set.max_iters);
+    do_finish(h);
+    fill_info(h, info);
+    if (info) info->solve_seconds = tm.s();
+  });
+}
+
+int scs_get_state(scs_handle* h, double* u, double* v) {
+  if (!h) return SCS_EINVAL;
+  return guard(h, [&] {
+    const long long len = h->n + h->m + 1;
+    if (u) d2h(h, u, h->V.u, len);
+    if (v) d2h(h, v, h->V.v, len);
+    CK(cudaStreamSynchronize(h->st));
+  });
+}
+
+int scs_get_scaling(scs_handle* h, double* D, double* E, double* sigma, double* rho) {
+  if (!h) return SCS_EINVAL;
+  return guard(h, [&] {
+    if (D) d2h(h, D, h->D, h->m);
+    if (E) d2h(h, E, h->E, h->n);
+    CK(cudaStreamSynchronize(h->st));
+    if (sigma) *sigma = h->sigma;
+    if (rho) *rho = h->rho;
+  });
+}
+
+int scs_update_vectors(scs_handle* h, const double* b, const double* c) {
+  if (!h) return SCS_EINVAL;
+  Timer tm;
+  return guard(h, [&] {
+    if (b) h2d(h, h->b0, b, h->m);
+    if (c) h2d(h, h->c0, c, h->n);
+    scale_vectors(h);
+    solve_g(h);
+    CK(cudaStreamSynchronize(h->st));
+    h->setup_seconds = tm.s();
+  });
+}
+
+int scs_apply_a(scs_handle* h, int which, const double* in, double* out) {
+  if (!h) return SCS_EINVAL;
+  return guard(h, [&] {
+    const long long nin = which == 0 ? h->n : h->m, nout = which == 0 ? h->m : h->n;
+    double* din = which == 0 ? h->tmp_n : h->tmp_m;
+    double* dout = which == 0 ? h->tmp_m2 : h->V.Gp;
+    h2d(h, din, in, nin);
+    EpiPlain e{};
+    e.V = h->V;
+    e.xs[0] = din;
+    e.out = dout;
+    if (which == 0) launch_spmv(h, h->A, h->LA, e);
+    else launch_spmv(h, h->At, h->LAt, e);
+    d2h(h, out, dout, nout);
+    CK(cudaStreamSynchronize(h->st));
+  });
+}
+
+int scs_point_residuals(scs_handle* h, const double* x, const double* y, const double* s,
+                        double* out3) {
+  if (!h) return SCS_EINVAL;
+  return guard(h, [&] {
+    const long long n = h->n, m = h->m;
+    // A x = D^-1 A_hat E^-1 x ; A^T y = E^-1 A_hat^T D^-1 y
+    h2d(h, h->tmp_n, x, n);
+    k_div<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->tmp_n, h->E, n, h->V.r);
+    EpiPlain e{};
+    e.V = h->V;
+    e.xs[0] = h->V.r;
+    e.out = h->tmp_m2;
+    launch_spmv(h, h->A, h->LA, e);
+    h2d(h, h->tmp_m, s, m);
+    k_point_pri<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->tmp_m2, h->D, h->tmp_m, h->b0, m, h->V.q);
+    const double pri = sqrt(norm2_dev(h, h->V.q, h->V.q, m, 2));
+    const double bn = sqrt(norm2_dev(h, h->b0, h->b0, m, 2));
+    h2d(h, h->tmp_m, y, m);
+    k_div<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->tmp_m, h->D, m, h->tmp_m2);
+    EpiPlain f{};
+    f.V = h->V;
+    f.xs[0] = h->tmp_m2;
+    f.out = h->V.Gp;
+    launch_spmv(h, h->At, h->LAt, f);
+    k_point_dual<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->V.Gp, h->E, h->c0, n, h->V.p);
+    const double dual = sqrt(norm2_dev(h, h->V.p, h->V.p, n, 2));
+    const double cn = sqrt(norm2_dev(h, h->c0, h->c0, n, 2));
+    const double ctx = norm2_dev(h, h->c0, h->tmp_n, n, 2);
+    const double bty = norm2_dev(h, h->b0, h->tmp_m, m, 2);
+    out3[0] = pri / (1.0 + bn);
+    out3[1] = dual / (1.0 + cn);
+    out3[2] = fabs(ctx + bty) / (1.0 + fabs(ctx) + fabs(bty));
+  });
+}
+
+int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t ns,
+                     const int64_t* s, int64_t ep, int kind, int64_t n, const double* x,
+                     double* out, int device) {
+  scs_handle* h = new scs_handle();
+  int rc = guard(nullptr, [&] {
+    if (kind < 0 || kind > 2) throw Fail{SCS_EINVAL, "kind must be 0, 1 or 2"};
+    h->dev = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
+    h->grid_full = std::min(h->sms * (2048 / kBlock), kMaxGrid);
+    long long m = z + l + 3 * ep;
+    for (int64_t i = 0; i < nq; ++i) m += q[i];
+    for (int64_t i = 0; i < ns; ++i) m += s[i] * (s[i] + 1) / 2;
+    if (kind != 2) n = 0;
+    h->m = h->m_glob = m;
+    h->n = n;
+    scs_problem P{};
+    P.m = m; P.n = n; P.z = z; P.l = l; P.nq = nq; P.q = q; P.ns = ns; P.s = s; P.ep = ep;
+    build_cones(h, &P);
+    CK(cudaMallocHost((void**)&h->ctl_h, sizeof(Ctl)));
+    memset(h->ctl_h, 0, sizeof(Ctl));
+    h->ctl = dalloc<Ctl>(h, 1);
+    Ctl* c = h->ctl_h;
+    c->alpha = 1.0;
+    c->corr = 0.0;
+    c->check_interval = 1;
+    c->status = SCS_RUNNING;
+    push_ctl(h);
+    const long long len = n + m + 1;
+    std::vector<double> xin(len, 0.0);
+    if (kind == 2) std::copy(x, x + len, xin.begin());
+    else for (long long i = 0; i < m; ++i) xin[i] = kind == 1 ? -x[i] : x[i];
+    Vec& V = h->V;
+    V.n = n; V.m = m; V.ctl = h->ctl;
+    V.u = dalloc<double>(h, len);
+    V.v = dalloc<double>(h, len);
+    V.x = dalloc<double>(h, n);
+    V.gx = dalloc<double>(h, n);
+    V.gy = dalloc<double>(h, m);
+    V.zy = dalloc<double>(h, m);
+    double* zc = dalloc<double>(h, std::max<long long>(n, m));
+    V.c = zc; V.b = zc;
+    V.part = dalloc<double>(h, (size_t)kMaxRed * kMaxGrid);
+    V.chunk_part = dalloc<double>(h, std::max(h->K.n_chunk, 1));
+    V.soc_fac = dalloc<double>(h, 3 * std::max(h->K.n_bsoc, 1));
+    CK(cudaMemsetAsync(zc, 0, std::max<long long>(n, m) * sizeof(double), h->st));
+    CK(cudaMemsetAsync(V.gx, 0, std::max<long long>(n, 1) * sizeof(double), h->st));
+    CK(cudaMemsetAsync(V.gy, 0, std::max<long long>(m, 1) * sizeof(double), h->st));
+    CK(cudaMemsetAsync(V.u, 0, len * sizeof(double), h->st));
+    CK(cudaMemsetAsync(V.v, 0, len * sizeof(double), h->st));
+    h2d(h, V.x, xin.data(), n);
+    h2d(h, V.zy, xin.data() + n, m);
+    h2d(h, V.u + n + m, xin.data() + n + m, 1);  // u_tau = x_tau, v_tau = 0
+    const long long work = std::max<long long>(n + h->K.z + h->K.l, 1);
+    int g = std::max(elem_grid(h, work), std::min(h->K.n_chunk, h->grid_full));
+    g = std::max(g, std::min((int)((h->K.n_ssoc * 32LL + kBlock - 1) / kBlock), h->grid_full));
+    k_cone_tail<<<g, kBlock, 0, h->st>>>(V, h->K);
+    if (h->K.n_chunk > 0 || h->K.n_psd > 0) {
+      const int ga = std::max(1, std::min(std::max(h->K.n_chunk, h->K.n_psd), h->grid_full));
+      k_cone_apply<<<ga, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side);
+    }
+    CK(cudaGetLastError());
+    std::vector<double> res(len);
+    d2h(h, res.data(), V.u, len);
+    pull_ctl(h);
+    check_err(h);
+    if (kind == 2) std::copy(res.begin(), res.end(), out);
+    else if (kind == 0) std::copy(res.begin(), res.begin() + m, out);
+    else for (long long i = 0; i < m; ++i) out[i] = x[i] + res[i];  // Pi_K(x) = x + Pi_K*(-x)
+  });
+  scs_destroy(h);
+  return rc;
+}
+
+int scs_bench_iters(scs_handle* h, int64_t k, double* ms) {
+  if (!h || !ms) return SCS_EINVAL;
+  return guard(h, [&] {
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, h->st));
+    for (int64_t i = 0; i < k; ++i) CK(cudaGraphLaunch(h->gexec, h->st));
+    CK(cudaEventRecord(e1, h->st));
+    CK(cudaEventSynchronize(e1));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, e0, e1));
+    *ms = f;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    h->launched_iters += k;
+    h->launches = k * h->launches_per_iter;
+    pull_ctl(h);
+    check_err(h);
+  });
+}
+
+int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms, double* bytes) {
+  if (!h || !ms || !bytes) return SCS_EINVAL;
+  return guard(h, [&] {
+    pull_ctl(h);
+    Ctl saved = *h->ctl_h;
+    h->ctl_h->stop = 0;
+    h->ctl_h->cg_done = 0;
+    h->ctl_h->rs = 1.0;
+    push_ctl(h);
+    const long long m = h->m, n = h->n, nnz = h->nnz;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    auto one = [&] {
+      if (kind == 0) {
+        EpiAp ea{};
+        ea.V = h->V;
+        ea.xs[0] = h->V.p;
+        launch_spmv(h, h->A, h->LA, ea);
+      } else {
+        EpiAtGp eg{};
+        eg.V = h->V;
+        eg.xs[0] = h->V.q;
+        launch_spmv(h, h->At, h->LAt, eg);
+      }
+    };
+    one();
+    CK(cudaEventRecord(e0, h->st));
+    for (int64_t i = 0; i < reps; ++i) one();
+    CK(cudaEventRecord(e1, h->st));
+    CK(cudaEventSynchronize(e1));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, e0, e1));
+    *ms = f / (double)std::max<int64_t>(reps, 1);
+    // algorithmic bytes: values + column indices, row pointers, the gathered
+    // vector once, the epilogue vectors
+    if (kind == 0) *bytes = 12.0 * nnz + 8.0 * (m + 1) + 8.0 * n + 8.0 * m;
+    else *bytes = 12.0 * nnz + 8.0 * (n + 1) + 8.0 * m + 16.0 * n;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *h->ctl_h = saved;
+    push_ctl(h);
+  });
+}
+
+int scs_nccl_unique_id(uint8_t* out128) {
+#ifdef SCS_WITH_NCCL
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return SCS_ENCCL;
+  memcpy(out128, id.internal, 128);
+  return SCS_OK;
+#else
+  (void)out128;
+  set_global_err("built without NCCL");
+  return SCS_ENCCL;
+#endif
+}
+
+}  // extern "C"
