@@ -84,9 +84,10 @@ constexpr int kChunk = 8192;     // big-SOC chunk (one CTA)
 // the L2 keeps the gather vectors resident.
 // ---------------------------------------------------------------------------
 template <int L, int NV>
-__device__ __forceinline__ void row_dot(const Csr& A, long long row, int gl,
+__device__ __forceinline__ void row_dot(const Csr& A, long long row, bool valid, int gl,
                                         const double* const (&xs)[NV], double (&s)[NV]) {
-  const long long k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
+  long long k0 = 0, k1 = 0;
+  if (valid) { k0 = __ldg(A.rp + row); k1 = __ldg(A.rp + row + 1); }
 #pragma unroll
   for (int t = 0; t < NV; ++t) s[t] = 0.0;
   long long k = k0 + gl;
@@ -107,25 +108,32 @@ __device__ __forceinline__ void row_dot(const Csr& A, long long row, int gl,
 #pragma unroll
     for (int t = 0; t < NV; ++t) s[t] = fma(a, __ldg(xs[t] + c), s[t]);
   }
+  // all 32 lanes reach the shuffles: the row loop below is warp-uniform
 #pragma unroll
   for (int t = 0; t < NV; ++t) s[t] = group_sum<L>(s[t]);
 }
 
 // Generic CSR SpMV with a per-row epilogue and an optional grid reduction
-// whose last block runs Epi::finish.  Grid-stride over rows by L-lane groups.
+// whose last block runs Epi::finish.  Each warp owns 32/L consecutive rows
+// per step (L lanes per row); the row loop is warp-uniform so the group
+// shuffles never see diverged lanes.
 template <int L, class Epi>
 __global__ void __launch_bounds__(kBlock) k_spmv(Csr A, Epi epi) {
   if (epi.skip()) return;
+  constexpr int kGroups = 32 / L;
   const int gl = threadIdx.x & (L - 1);
-  const long long group = ((long long)blockIdx.x * kBlock + threadIdx.x) / L;
-  const long long ngroups = ((long long)gridDim.x * kBlock) / L;
+  const int gi = (threadIdx.x & 31) / L;
+  const long long warp = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * kBlock) >> 5;
   double red[Epi::NR > 0 ? Epi::NR : 1];
 #pragma unroll
   for (int t = 0; t < (Epi::NR > 0 ? Epi::NR : 1); ++t) red[t] = 0.0;
-  for (long long row = group; row < A.rows; row += ngroups) {
+  for (long long base = warp * kGroups; base < A.rows; base += nwarps * kGroups) {
+    const long long row = base + gi;
+    const bool valid = row < A.rows;
     double s[Epi::NV];
-    row_dot<L, Epi::NV>(A, row, gl, epi.xs, s);
-    if (gl == 0) epi.row(row, s, red);
+    row_dot<L, Epi::NV>(A, row, valid, gl, epi.xs, s);
+    if (valid && gl == 0) epi.row(row, s, red);
   }
   epi.extra(red);
   if constexpr (Epi::NR > 0) {
