@@ -231,12 +231,26 @@ def proj_psd(blk, side):
 
 # --- exponential cone: NO reference -- parity unpinned ---------
 def _exp_in_primal(r, s, t):
-    return (s > 0 and s * math.exp(r / s) <= t) or (r <= 0 and s == 0 and t >= 0)
+    if s > 0:
+        return r / s < 700 and s * math.exp(r / s) <= t
+    return r <= 0 and s == 0 and t >= 0
 
 
 def _exp_in_dual(u, v, w):
-    return (u < 0 and -u * math.exp(v / u) <= math.e * w) or \
-        (u == 0 and v >= 0 and w >= 0)
+    if u < 0:
+        return v / u < 700 and -u * math.exp(v / u) <= math.e * w
+    return u == 0 and v >= 0 and w >= 0
+
+
+def _exp_sign(rho, r0, s0, t0):
+    """sign(F(rho)) without overflow: F q e^-rho (rho >= 0), F q e^rho (rho < 0)."""
+    q = rho * rho - rho + 1.0
+    a, b = (rho - 1.0) * r0 + s0, r0 - rho * s0
+    if rho >= 0:
+        e = math.exp(-rho)
+        return a - b * e * e - t0 * q * e
+    e = math.exp(rho)
+    return a * e * e - b - t0 * q * e
 
 
 def proj_exp_primal(v0):
@@ -244,8 +258,10 @@ def proj_exp_primal(v0):
 
     Hard case: the projection is s*(rho, 1, e^rho) with polar part
     -lam*(-1, rho-1, e^-rho); eliminating s, lam leaves the univariate root
-    ((rho-1) r0 + s0) e^rho - (r0 - rho s0) e^-rho - t0 (rho^2 - rho + 1) = 0
-    on the interval where s > 0 and lam > 0, solved by bisection here.
+    F(rho) = ((rho-1) r0 + s0) e^rho - (r0 - rho s0) e^-rho - t0 (rho^2 - rho + 1)
+    on the interval where s > 0 and lam > 0, found by bisection on an
+    overflow-free rescaling of F; t is recovered as t0 + lam e^-rho when
+    rho > 0 (s e^rho would amplify the rounding of s by e^rho).
     """
     r0, s0, t0 = (float(x) for x in v0)
     if _exp_in_primal(r0, s0, t0):
@@ -263,31 +279,28 @@ def proj_exp_primal(v0):
         hi = min(hi, r0 / s0)
     elif s0 < 0:
         lo = max(lo, r0 / s0)
-
-    def f(rho):
-        q = rho * rho - rho + 1.0
-        return ((rho - 1.0) * r0 + s0) * math.exp(rho) / q - \
-            (r0 - rho * s0) * math.exp(-rho) / q - t0
-
-    # finite bracket: expand the open side(s)
     if not math.isfinite(lo):
         lo = (hi if math.isfinite(hi) else 0.0) - 1.0
-        while f(lo) > 0:
-            lo = 2.0 * lo - 1.0 if lo < 0 else lo - 1.0
+        while _exp_sign(lo, r0, s0, t0) > 0:
+            lo = 2.0 * lo - 1.0
     if not math.isfinite(hi):
         hi = lo + 1.0
-        while f(hi) < 0:
-            hi = 2.0 * hi + 1.0 if hi > 0 else hi + 1.0
-    for _ in range(200):
+        while _exp_sign(hi, r0, s0, t0) < 0:
+            hi = 2.0 * abs(hi) + 1.0
+    for _ in range(400):
         mid = 0.5 * (lo + hi)
-        if f(mid) < 0:
+        if mid <= lo or mid >= hi:
+            break
+        if _exp_sign(mid, r0, s0, t0) < 0:
             lo = mid
         else:
             hi = mid
     rho = 0.5 * (lo + hi)
     q = rho * rho - rho + 1.0
     s = ((rho - 1.0) * r0 + s0) / q
-    return np.array([s * rho, s, s * math.exp(rho)])
+    lam = (r0 - rho * s0) / q
+    t = t0 + lam * math.exp(-rho) if rho > 0 else s * math.exp(rho)
+    return np.array([s * rho, s, t])
 
 
 def proj_exp_dual(v):

@@ -18,7 +18,7 @@ namespace scs {
 //   F(rho) = ((rho-1) r0 + s0) e^rho - (r0 - rho s0) e^-rho
 //            - t0 (rho^2 - rho + 1) = 0
 // on the interval where s > 0 and lam > 0 (F is increasing there).  Solved
-// by safeguarded Newton inside a bisection bracket.
+// by bisection on an overflow-free rescaling of F with the same sign.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ bool exp_in_primal(double r, double s, double t) {
   return (s > 0.0 && s * exp(r / s) <= t) || (r <= 0.0 && s == 0.0 && t >= 0.0);
@@ -28,16 +28,24 @@ __device__ __forceinline__ bool exp_in_dual(double u, double v, double w) {
          (u == 0.0 && v >= 0.0 && w >= 0.0);
 }
 
-__device__ __forceinline__ double exp_F(double rho, double r0, double s0, double t0) {
+// sign(F(rho)) without overflow: F * q * e^{-rho} for rho >= 0 and
+// F * q * e^{rho} for rho < 0 (q = rho^2 - rho + 1 > 0).
+__device__ __forceinline__ double exp_sign_fn(double rho, double r0, double s0, double t0) {
   const double q = rho * rho - rho + 1.0;
-  const double er = exp(fmin(rho, 700.0)), emr = exp(fmin(-rho, 700.0));
-  return ((rho - 1.0) * r0 + s0) * er / q - (r0 - rho * s0) * emr / q - t0;
+  const double a = (rho - 1.0) * r0 + s0, b = r0 - rho * s0;
+  if (rho >= 0.0) {
+    const double e = exp(-rho);
+    return a - b * e * e - t0 * q * e;
+  }
+  const double e = exp(rho);
+  return a * e * e - b - t0 * q * e;
 }
 
 __device__ void exp_proj_primal(double r0, double s0, double t0, double* out) {
   if (exp_in_primal(r0, s0, t0)) { out[0] = r0; out[1] = s0; out[2] = t0; return; }
   if (exp_in_dual(-r0, -s0, -t0)) { out[0] = 0.0; out[1] = 0.0; out[2] = 0.0; return; }
   if (r0 <= 0.0 && s0 <= 0.0) { out[0] = r0; out[1] = 0.0; out[2] = fmax(t0, 0.0); return; }
+  // root interval: s(rho) > 0 and lam(rho) > 0
   double lo = -INFINITY, hi = INFINITY;
   if (r0 > 0.0) lo = fmax(lo, 1.0 - s0 / r0);
   else if (r0 < 0.0) hi = fmin(hi, 1.0 - s0 / r0);
@@ -45,32 +53,25 @@ __device__ void exp_proj_primal(double r0, double s0, double t0, double* out) {
   else if (s0 < 0.0) lo = fmax(lo, r0 / s0);
   if (!isfinite(lo)) {
     lo = (isfinite(hi) ? hi : 0.0) - 1.0;
-    for (int i = 0; i < 64 && exp_F(lo, r0, s0, t0) > 0.0; ++i) lo = lo < 0.0 ? 2.0 * lo - 1.0 : lo - 1.0;
+    for (int i = 0; i < 80 && exp_sign_fn(lo, r0, s0, t0) > 0.0; ++i) lo = 2.0 * lo - 1.0;
   }
   if (!isfinite(hi)) {
     hi = lo + 1.0;
-    for (int i = 0; i < 64 && exp_F(hi, r0, s0, t0) < 0.0; ++i) hi = hi > 0.0 ? 2.0 * hi + 1.0 : hi + 1.0;
+    for (int i = 0; i < 80 && exp_sign_fn(hi, r0, s0, t0) < 0.0; ++i) hi = 2.0 * fabs(hi) + 1.0;
   }
-  double rho = 0.5 * (lo + hi);
-  for (int it = 0; it < 200; ++it) {
-    const double f = exp_F(rho, r0, s0, t0);
-    if (f < 0.0) lo = rho; else hi = rho;
-    if (f == 0.0 || hi - lo <= 1e-15 * fmax(1.0, fabs(rho))) break;
-    // Newton on F; derivative by the product rule
-    const double q = rho * rho - rho + 1.0, dq = 2.0 * rho - 1.0;
-    const double er = exp(fmin(rho, 700.0)), emr = exp(fmin(-rho, 700.0));
-    const double a = (rho - 1.0) * r0 + s0, bb = r0 - rho * s0;
-    const double df = (r0 * er + a * er) / q - a * er * dq / (q * q)
-                      - ((-s0) * emr - bb * emr) / q + bb * emr * dq / (q * q);
-    double nr = rho - f / df;
-    if (!(nr > lo && nr < hi) || !isfinite(nr)) nr = 0.5 * (lo + hi);
-    rho = nr;
+  for (int it = 0; it < 200 && hi - lo > 1e-15 * fmax(1.0, fabs(lo)); ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    if (exp_sign_fn(mid, r0, s0, t0) < 0.0) lo = mid; else hi = mid;
   }
+  const double rho = 0.5 * (lo + hi);
   const double q = rho * rho - rho + 1.0;
   const double s = ((rho - 1.0) * r0 + s0) / q;
+  const double lam = (r0 - rho * s0) / q;
   out[0] = s * rho;
   out[1] = s;
-  out[2] = s * exp(rho);
+  // t = s e^rho = t0 + lam e^-rho at the root; use the form that cannot blow up
+  out[2] = rho > 0.0 ? t0 + lam * exp(-rho) : s * exp(rho);
 }
 
 // Pi_{K_exp*}(v) = v + Pi_{K_exp}(-v)  (Moreau)

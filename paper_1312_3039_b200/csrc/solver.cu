@@ -7,7 +7,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -612,6 +614,22 @@ struct scs_handle {
 
 namespace {
 
+bool dbg_on() {
+  static int on = -1;
+  if (on < 0) on = getenv("SCS_DEBUG") ? 1 : 0;
+  return on == 1;
+}
+void dbg(const char* fmt, ...) {
+  if (!dbg_on()) return;
+  va_list ap;
+  va_start(ap, fmt);
+  fprintf(stderr, "[scs] ");
+  vfprintf(stderr, fmt, ap);
+  fprintf(stderr, "\n");
+  fflush(stderr);
+  va_end(ap);
+}
+
 void set_global_err(const std::string& s) {
   std::lock_guard<std::mutex> g(g_err_mu);
   g_err = s;
@@ -1015,6 +1033,7 @@ void solve_g(scs_handle* h) {
   long long done_steps = 0;
   while (true) {
     pull_ctl(h);
+    dbg("g-solve: steps=%lld cg_it=%d done=%d err=%d", done_steps, c->cg_it, c->cg_done, c->err);
     check_err(h);
     if (c->cg_done) break;
     const long long batch = std::min<long long>(32, cap - done_steps);
@@ -1145,6 +1164,8 @@ void do_steps(scs_handle* h, long long k) {
     h->launched_iters += b;
     todo -= b;
     pull_ctl(h);
+    dbg("steps: launched=%lld iter=%lld status=%d stop=%d err=%d cg_it=%d", h->launched_iters,
+        c->iter, c->status, c->stop, c->err, c->cg_it);
     check_err(h);
     if (c->stop) break;
     batch = std::min<long long>(batch * 2, 64);
@@ -1241,7 +1262,9 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
   scs_handle* h = new scs_handle();
   Timer tm;
   int rc = guard(nullptr, [&] {
+    dbg("scs_create enter");
     validate(P, S);
+    dbg("validated");
     h->set = *S;
     h->dev = S->device;
     CK(cudaSetDevice(h->dev));
@@ -1273,7 +1296,9 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     c->denom = 1.0;
     c->sigma = c->rho = 1.0;
     push_ctl(h);
+    dbg("ctl pushed");
     build_cones(h, P);
+    dbg("cones built");
     // vectors
     Vec& V = h->V;
     V.n = n;
@@ -1311,11 +1336,18 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     CK(cudaMemsetAsync(h->zero_m, 0, std::max<long long>(m, 1) * sizeof(double), h->st));
     h2d(h, h->b0, P->b, m);
     h2d(h, h->c0, P->c, n);
+    dbg("create m=%lld n=%lld nnz=%lld", m, n, h->nnz);
     build_matrices(h, P);
+    CK(cudaStreamSynchronize(h->st));
+    dbg("matrices built LA=%d LAt=%d", h->LA, h->LAt);
     equilibrate(h);
+    dbg("equilibrated mean_col=%g mean_row=%g", h->mean_col, h->mean_row);
     scale_vectors(h);
+    dbg("scaled sigma=%g rho=%g", h->sigma, h->rho);
     solve_g(h);
+    dbg("g solved denom=%g cg=%lld", h->ctl_h->denom, h->ctl_h->cg_iters_total);
     build_graph(h);
+    dbg("graph built launches/iter=%lld", h->launches_per_iter);
     CK(cudaStreamSynchronize(h->st));
   });
   if (rc != SCS_OK) {
