@@ -478,13 +478,17 @@ class Workspace:
         else:
             self._call(self._lib.scs_begin(self._h, native.ptr(wx), native.ptr(wy),
                                            native.ptr(ws)))
+            # the termination check of iteration k runs inside step k+1 (it
+            # shares that step's first matrix passes); a step that ends in
+            # a status leaves the state -- and the iteration count -- at k
             while True:
+                prev = int(info.iterations)
                 self._call(self._lib.scs_step(self._h, 1, native.C.byref(info)))
-                if info.iterations == 0:
-                    break
-                u, v = self.state()
-                on_iteration(SolverState(u=u, v=v, iter=int(info.iterations)))
-                if info.status >= 0 or info.iterations >= st.max_iters:
+                if info.iterations > prev:
+                    u, v = self.state()
+                    on_iteration(SolverState(u=u, v=v, iter=int(info.iterations)))
+                if info.status >= 0 or info.iterations >= st.max_iters or \
+                        info.iterations == prev:
                     break
             self._call(self._lib.scs_finish(self._h, native.C.byref(info)))
         u, v = self.state()

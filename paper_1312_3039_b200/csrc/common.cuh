@@ -44,8 +44,9 @@ struct Ctl {
   int err;                  // ERR_* bits
   int warm_zero;            // cg_warm == 0 exactly (skip A cg_warm gather)
   int force_check;          // residual kernels run regardless of interval
-  int check_now;            // this iteration checks termination
-  int pad0, pad1;
+  int check_now;            // unused (kept for layout)
+  int check_pending;        // the last finished iteration is due a check
+  int pad1;
   // per-iteration scalars
   double tol;               // CG tolerance of this iteration
   double rs;                // CG r'r carried between CG steps

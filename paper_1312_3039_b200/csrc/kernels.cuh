@@ -7,18 +7,26 @@
 //
 //   k_prep         w = u+v, rhs = w[:-1] - w_tau h, ||rhs|| -> CG tol       embedding.py:177-185
 //   SpMV A^T  [EpiAtFirst]  cg_rhs = rhs_x - A^T rhs_y, r0 = cg_rhs - G x0   embedding.py:109, sparse_linalg.py:461-469
+//                           (+ A^T u_y of the previous iterate, see below)
 //   cg_max x { SpMV A [EpiAp]; SpMV A^T [EpiAtGp]; k_cg_update; k_cg_p }    sparse_linalg.py:470-485
+//                           (the first A pass also carries A u_x, below)
 //   SpMV A    [EpiAFinal]   z_y = rhs_y + A x, corr = h'p / denom          embedding.py:113, 192
 //   k_cone_tail    u~, relaxation, cone projection (elementwise / SOC / exp),
 //                  tau update                                               embedding.py:193-196, solver.py:163-165
 //   k_cone_apply   large SOC + PSD (Jacobi) blocks                          cones.py:172-191
-//   SpMV A    [EpiResA]  + SpMV A^T [EpiResAt]  residuals + termination     scaling.py:148-207, solver.py:210-234
 //
-// A x_{warm} is NOT recomputed at the head of CG: the previous iteration's
-// EpiAFinal already produced A x for the same x (cg_warm), bit-identical,
-// and stored it (Axw) -- the reference's A-pass for r0 is redundant work.
-// The reference's trailing exact-residual pass (sparse_linalg.py:486), whose
-// value its caller discards (embedding.py:110), is not performed.
+// Matrix passes per iteration: 2 + 2k (k = CG steps); the reference makes 6 + 2k
+// (k = CG steps, sparse_linalg.py:461,471,486 + embedding.py:109,113 +
+// scaling.py:466-467).  Removed, with bit-identical results:
+//  * A x_warm at the head of CG: the previous iteration's EpiAFinal already
+//    produced A x for the same x (cg_warm) and stored it (Y3 slot 1);
+//  * the trailing exact-residual pass (sparse_linalg.py:486), whose value
+//    its caller discards (embedding.py:110);
+//  * the two residual passes of the termination check (scaling.py:466-467):
+//    they gather the same interleaved sector as the next iteration's first
+//    A^T / A pass, so they ride along; the next iteration is speculative
+//    until the check of the previous one has passed (its state writes come
+//    after the check), exactly reproducing the reference's loop exit.
 #pragma once
 
 #include "common.cuh"
@@ -34,17 +42,22 @@ struct Csr {
 };
 
 // Device vectors of one handle.  x-part length n, y-part length m (local).
+// Gather vectors are interleaved so that one 32-byte sector request serves
+// every SpMV that shares a matrix pass:
+//   X2[2j + 0] = p_j (CG direction)      X2[2j + 1] = (u_x)_j
+//   Y3[4i + 0] = (rhs_y)_i               Y3[4i + 1] = (A cg_warm)_i
+//   Y3[4i + 2] = (u_y)_i                 Y3[4i + 3] = unused
 struct Vec {
   long long n, m;
-  double *u, *v;              // n + m + 1
+  double *u, *v;              // n + m + 1 (SolverState)
   const double *c, *b;        // scaled data
   const double *D, *E;        // scalings
   double *gx, *gy;            // g = M^-1 h
-  double *rhs_x, *rhs_y;      // rhs = w[:-1] - w_tau h
+  double *rhs_x;              // rhs = w[:-1] - w_tau h (x-part; y-part in Y3)
   double *x;                  // CG iterate == cg_warm (embedding.py:111)
-  double *r, *p, *Gp;         // CG vectors (n)
+  double *r, *Gp;             // CG vectors (n)
+  double *X2, *Y3;            // interleaved gather vectors
   double *q;                  // A p (m)
-  double *Axw;                // A cg_warm (m)
   double *zy;                 // z_y = rhs_y + A x (m)
   double *part;               // kMaxRed * kMaxGrid partials
   double *chunk_part;         // big-SOC chunk partial norms
@@ -81,11 +94,34 @@ constexpr int kChunk = 8192;     // big-SOC chunk (one CTA)
 // ---------------------------------------------------------------------------
 // CSR row dot products: L lanes per row, lane-strided, FMA, group shuffle.
 // The matrix streams (ci, v) are loaded with evict-first (ld.global.cs) so
-// the L2 keeps the gather vectors resident.
+// the L2 keeps the gather vectors resident.  NV values are gathered per
+// nonzero from an interleaved vector (STRIDE doubles per entry) with one
+// load instruction: 64-bit, 128-bit (double2) or 256-bit (v4.f64).
 // ---------------------------------------------------------------------------
-template <int L, int NV>
+template <int NV, int STRIDE>
+__device__ __forceinline__ void gather(const double* __restrict__ xb, int c, double (&g)[NV]) {
+  const double* p = xb + (size_t)c * STRIDE;
+  if constexpr (NV == 1) {
+    g[0] = __ldg(p);
+  } else if constexpr (NV == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    g[0] = t.x;
+    g[1] = t.y;
+  } else {
+    static_assert(STRIDE == 4 && NV <= 4, "256-bit gathers need a stride of 4");
+    double a, b, cc, d;
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(a), "=d"(b), "=d"(cc), "=d"(d) : "l"(p));
+    g[0] = a;
+    g[1] = b;
+    if constexpr (NV > 2) g[2] = cc;
+    if constexpr (NV > 3) g[3] = d;
+  }
+}
+
+template <int L, int NV, int STRIDE>
 __device__ __forceinline__ void row_dot(const Csr& A, long long row, bool valid, int gl,
-                                        const double* const (&xs)[NV], double (&s)[NV]) {
+                                        const double* __restrict__ xb, double (&s)[NV]) {
   long long k0 = 0, k1 = 0;
   if (valid) { k0 = __ldg(A.rp + row); k1 = __ldg(A.rp + row + 1); }
 #pragma unroll
@@ -98,15 +134,19 @@ __device__ __forceinline__ void row_dot(const Csr& A, long long row, bool valid,
     for (int u = 0; u < 4; ++u) { c[u] = __ldcs(A.ci + k + u * L); a[u] = __ldcs(A.v + k + u * L); }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
+      double g[NV];
+      gather<NV, STRIDE>(xb, c[u], g);
 #pragma unroll
-      for (int t = 0; t < NV; ++t) s[t] = fma(a[u], __ldg(xs[t] + c[u]), s[t]);
+      for (int t = 0; t < NV; ++t) s[t] = fma(a[u], g[t], s[t]);
     }
   }
   for (; k < k1; k += L) {
     const int c = __ldcs(A.ci + k);
     const double a = __ldcs(A.v + k);
+    double g[NV];
+    gather<NV, STRIDE>(xb, c, g);
 #pragma unroll
-    for (int t = 0; t < NV; ++t) s[t] = fma(a, __ldg(xs[t] + c), s[t]);
+    for (int t = 0; t < NV; ++t) s[t] = fma(a, g[t], s[t]);
   }
   // all 32 lanes reach the shuffles: the row loop below is warp-uniform
 #pragma unroll
@@ -116,23 +156,26 @@ __device__ __forceinline__ void row_dot(const Csr& A, long long row, bool valid,
 // Generic CSR SpMV with a per-row epilogue and an optional grid reduction
 // whose last block runs Epi::finish.  Each warp owns 32/L consecutive rows
 // per step (L lanes per row); the row loop is warp-uniform so the group
-// shuffles never see diverged lanes.
+// shuffles never see diverged lanes.  Epi::load() reads the Ctl flags once
+// and says whether the whole launch is a no-op.
 template <int L, class Epi>
-__global__ void __launch_bounds__(kBlock) k_spmv(Csr A, Epi epi) {
-  if (epi.skip()) return;
+__global__ void __launch_bounds__(kBlock) k_spmv(Csr A, Epi epi0) {
+  Epi epi = epi0;
+  if (!epi.load()) return;
   constexpr int kGroups = 32 / L;
+  constexpr int NR = Epi::NR > 0 ? Epi::NR : 1;
   const int gl = threadIdx.x & (L - 1);
   const int gi = (threadIdx.x & 31) / L;
   const long long warp = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * kBlock) >> 5;
-  double red[Epi::NR > 0 ? Epi::NR : 1];
+  double red[NR];
 #pragma unroll
-  for (int t = 0; t < (Epi::NR > 0 ? Epi::NR : 1); ++t) red[t] = 0.0;
+  for (int t = 0; t < NR; ++t) red[t] = 0.0;
   for (long long base = warp * kGroups; base < A.rows; base += nwarps * kGroups) {
     const long long row = base + gi;
     const bool valid = row < A.rows;
     double s[Epi::NV];
-    row_dot<L, Epi::NV>(A, row, valid, gl, epi.xs, s);
+    row_dot<L, Epi::NV, Epi::STRIDE>(A, row, valid, gl, epi.xb, s);
     if (valid && gl == 0) epi.row(row, s, red);
   }
   epi.extra(red);
@@ -141,28 +184,49 @@ __global__ void __launch_bounds__(kBlock) k_spmv(Csr A, Epi epi) {
   }
 }
 
+__device__ void finish_residuals(Ctl* c, double ut, double s_pri, double s_unb, double buy,
+                                 double s_dual, double s_inf, double cux);
+
 // ---- epilogues --------------------------------------------------------------
 struct EpiBase {
   Vec V;
+  const double* xb;  // gather base
+  int pend;          // residual check of the previous iteration rides along
   __device__ void extra(double*) const {}
+  __device__ __forceinline__ double utau() const { return V.u[V.n + V.m]; }
 };
 
-// r0 = (rhs_x - A^T rhs_y) - (x0 + A^T (A x0)); p = r (sparse_linalg.py:461-469)
+// First A^T pass of an iteration (sparse_linalg.py:461-469 + scaling.py:467):
+//   r0 = (rhs_x - A^T rhs_y) - (x0 + A^T (A x0)); p = r0
+// and, when the previous iteration is due a termination check, A^T u_y of
+// that iterate (dual residual / infeasibility, scaling.py:484-490).  One
+// 256-bit gather per nonzero serves all three products.
 struct EpiAtFirst : EpiBase {
-  static constexpr int NV = 2, NR = 1;
-  const double* xs[2];
-  __device__ bool skip() const { return V.ctl->stop; }
-  __device__ void row(long long j, const double (&s)[2], double* red) const {
+  static constexpr int NV = 3, STRIDE = 4, NR = 4;
+  __device__ bool load() {
+    pend = V.ctl->check_pending;
+    return !V.ctl->stop;
+  }
+  __device__ void row(long long j, const double (&s)[3], double* red) const {
     const double cg_rhs = V.rhs_x[j] - s[0];
     const double gx = V.x[j] + s[1];
     const double r = cg_rhs - gx;
     V.r[j] = r;
-    V.p[j] = r;
+    V.X2[2 * j] = r;
     red[0] += r * r;
+    if (pend) {
+      const double ei = 1.0 / V.E[j];
+      const double du = ei * (s[2] / utau() + V.c[j]);
+      const double inf = ei * s[2];
+      red[1] += du * du;
+      red[2] += inf * inf;
+      red[3] += V.c[j] * V.X2[2 * j + 1];
+    }
   }
   __device__ void finish(const double* tot) const {
     if (threadIdx.x) return;
     Ctl* c = V.ctl;
+    if (pend) { c->sums[3] = tot[1]; c->sums[4] = tot[2]; c->sums[5] = tot[3]; }
     const double res = sqrt(tot[0]);
     c->cg_it = 0;
     if (!isfinite(res)) { c->err |= ERR_CG_NONFINITE; c->stop = 1; c->cg_done = 1; return; }
@@ -172,22 +236,48 @@ struct EpiAtFirst : EpiBase {
   }
 };
 
-// q = A p
+// q = A p.  MERGED: the first CG pass also carries A u_x of the previous
+// iterate (primal residual / unboundedness, scaling.py:466-489) and closes
+// that iteration's termination check (solver.py:359-363).
+template <bool MERGED>
 struct EpiAp : EpiBase {
-  static constexpr int NV = 1, NR = 0;
-  const double* xs[1];
-  __device__ bool skip() const { return V.ctl->stop || V.ctl->cg_done; }
-  __device__ void row(long long i, const double (&s)[1], double*) const { V.q[i] = s[0]; }
-  __device__ void finish(const double*) const {}
+  static constexpr int NV = MERGED ? 2 : 1, STRIDE = 2, NR = MERGED ? 3 : 0;
+  __device__ bool load() {
+    const Ctl* c = V.ctl;
+    pend = MERGED ? c->check_pending : 0;
+    return !c->stop && (!c->cg_done || pend);
+  }
+  __device__ void row(long long i, const double (&s)[NV], double* red) const {
+    V.q[i] = s[0];
+    if constexpr (MERGED) {
+      if (pend) {
+        const double t = s[1] + V.v[V.n + i];
+        const double di = 1.0 / V.D[i];
+        const double pr = di * (t / utau() - V.b[i]);
+        const double ub = di * t;
+        red[0] += pr * pr;
+        red[1] += ub * ub;
+        red[2] += V.b[i] * V.Y3[4 * i + 2];
+      }
+    }
+  }
+  __device__ void finish(const double* tot) const {
+    if constexpr (MERGED) {
+      if (threadIdx.x || !pend) return;
+      Ctl* c = V.ctl;
+      finish_residuals(c, utau(), tot[0], tot[1], tot[2], c->sums[3], c->sums[4], c->sums[5]);
+      c->check_pending = 0;
+      if (c->stop) c->k_sched -= 1;  // the speculative iteration never happened
+    }
+  }
 };
 
 // Gp = p + A^T q, p'Gp -> alpha (sparse_linalg.py:471-475)
 struct EpiAtGp : EpiBase {
-  static constexpr int NV = 1, NR = 1;
-  const double* xs[1];
-  __device__ bool skip() const { return V.ctl->stop || V.ctl->cg_done; }
+  static constexpr int NV = 1, STRIDE = 1, NR = 1;
+  __device__ bool load() { return !V.ctl->stop && !V.ctl->cg_done; }
   __device__ void row(long long j, const double (&s)[1], double* red) const {
-    const double pj = V.p[j];
+    const double pj = V.X2[2 * j];
     const double g = pj + s[0];
     V.Gp[j] = g;
     red[0] += pj * g;
@@ -205,15 +295,14 @@ struct EpiAtGp : EpiBase {
 // (embedding.py:113, 192).  In setup mode (g = M^-1 h) writes g_y and the
 // Schur denominator instead (embedding.py:152-161).
 struct EpiAFinal : EpiBase {
-  static constexpr int NV = 1, NR = 2;
-  const double* xs[1];
+  static constexpr int NV = 1, STRIDE = 1, NR = 2;
   double* zy_out;
   int setup;
-  __device__ bool skip() const { return V.ctl->stop; }
+  __device__ bool load() { return !V.ctl->stop; }
   __device__ void row(long long i, const double (&s)[1], double* red) const {
-    const double z = V.rhs_y[i] + s[0];
+    const double z = V.Y3[4 * i] + s[0];
     zy_out[i] = z;
-    if (!setup) V.Axw[i] = s[0];
+    if (!setup) V.Y3[4 * i + 1] = s[0];
     red[1] += V.b[i] * z;
   }
   __device__ void extra(double* red) const {
@@ -235,16 +324,18 @@ struct EpiAFinal : EpiBase {
   }
 };
 
-// A u_x -> primal residual / unboundedness partial norms (scaling.py:466-489)
+// Stand-alone termination check (after the last iteration of a loop, or a
+// forced residual evaluation): A u_x ...
 struct EpiResA : EpiBase {
-  static constexpr int NV = 1, NR = 3;
-  const double* xs[1];
-  __device__ bool skip() const { return V.ctl->stop || !V.ctl->check_now; }
+  static constexpr int NV = 1, STRIDE = 1, NR = 3;
+  __device__ bool load() {
+    const Ctl* c = V.ctl;
+    return !c->stop && (c->check_pending || c->force_check);
+  }
   __device__ void row(long long i, const double (&s)[1], double* red) const {
-    const double ut = V.u[V.n + V.m];
     const double t = s[0] + V.v[V.n + i];
     const double di = 1.0 / V.D[i];
-    const double pr = di * (t / ut - V.b[i]);
+    const double pr = di * (t / utau() - V.b[i]);
     const double ub = di * t;
     red[0] += pr * pr;
     red[1] += ub * ub;
@@ -258,19 +349,16 @@ struct EpiResA : EpiBase {
   }
 };
 
-__device__ void finish_residuals(Ctl* c, double ut, double s_pri, double s_unb, double buy,
-                                 double s_dual, double s_inf, double cux);
-
-// A^T u_y -> dual residual / infeasibility norms, then termination
-// (scaling.py:467-507, solver.py:210-234)
+// ... and A^T u_y, then the status (scaling.py:467-507, solver.py:210-234)
 struct EpiResAt : EpiBase {
-  static constexpr int NV = 1, NR = 3;
-  const double* xs[1];
-  __device__ bool skip() const { return V.ctl->stop || !V.ctl->check_now; }
+  static constexpr int NV = 1, STRIDE = 1, NR = 3;
+  __device__ bool load() {
+    const Ctl* c = V.ctl;
+    return !c->stop && (c->check_pending || c->force_check);
+  }
   __device__ void row(long long j, const double (&s)[1], double* red) const {
-    const double ut = V.u[V.n + V.m];
     const double ei = 1.0 / V.E[j];
-    const double du = ei * (s[0] / ut + V.c[j]);
+    const double du = ei * (s[0] / utau() + V.c[j]);
     const double inf = ei * s[0];
     red[0] += du * du;
     red[1] += inf * inf;
@@ -279,16 +367,16 @@ struct EpiResAt : EpiBase {
   __device__ void finish(const double* tot) const {
     if (threadIdx.x) return;
     Ctl* c = V.ctl;
-    finish_residuals(c, V.u[V.n + V.m], c->sums[0], c->sums[1], c->sums[2], tot[0], tot[1], tot[2]);
+    finish_residuals(c, utau(), c->sums[0], c->sums[1], c->sums[2], tot[0], tot[1], tot[2]);
+    c->check_pending = 0;
   }
 };
 
 // Plain products for the C-ABI test hook (scs_apply_a).
 struct EpiPlain : EpiBase {
-  static constexpr int NV = 1, NR = 0;
-  const double* xs[1];
+  static constexpr int NV = 1, STRIDE = 1, NR = 0;
   double* out;
-  __device__ bool skip() const { return false; }
+  __device__ bool load() { return true; }
   __device__ void row(long long i, const double (&s)[1], double*) const { out[i] = s[0]; }
   __device__ void finish(const double*) const {}
 };

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(kBlock) k_prep(Vec V) {
     const double w = V.u[i] + V.v[i];
     double r;
     if (i < n) { r = w - wt * V.c[i]; V.rhs_x[i] = r; }
-    else { r = w - wt * V.b[i - n]; V.rhs_y[i - n] = r; }
+    else { r = w - wt * V.b[i - n]; V.Y3[4 * (i - n)] = r; }
     red[0] += r * r;
   }
   if (grid_sum_last<1>(red, V.part, &c->counter) && threadIdx.x == 0) {
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(Vec V, long long cap) {
   const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
   const long long nt = (long long)gridDim.x * kBlock;
   for (long long j = tid; j < V.n; j += nt) {
-    V.x[j] += a * V.p[j];
+    V.x[j] += a * V.X2[2 * j];
     const double r = V.r[j] - a * V.Gp[j];
     V.r[j] = r;
     red[0] += r * r;
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_p(Vec V) {
   const double be = c->cg_beta;
   const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
   const long long nt = (long long)gridDim.x * kBlock;
-  for (long long j = tid; j < V.n; j += nt) V.p[j] = V.r[j] + be * V.p[j];
+  for (long long j = tid; j < V.n; j += nt) V.X2[2 * j] = V.r[j] + be * V.X2[2 * j];
 }
 
 // relaxed point of element i of the (x, y) part:
@@ -106,6 +106,7 @@ __device__ __forceinline__ Relax relax_y(const Vec& V, long long i, double corr,
 __device__ __forceinline__ void store_y(const Vec& V, long long i, double ub, double up) {
   const double vi = V.v[V.n + i];
   V.u[V.n + i] = up;
+  V.Y3[4 * i + 2] = up;           // gather copy for the next residual pass
   V.v[V.n + i] = (vi - ub) + up;  // solver.py:165
 }
 
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K) {
     bad |= !isfinite(t);
     const double vj = V.v[j];
     V.u[j] = t;
+    V.X2[2 * j + 1] = t;
     V.v[j] = (vj - ub) + t;
   }
   // zero (free in K*) and nonnegative rows
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K) {
     V.u[n + m] = up;
     V.v[n + m] = (vt_ - ub) + up;
     c->iter += 1;
-    c->check_now = c->force_check || (c->iter % c->check_interval == 0);
+    c->check_pending = (c->iter % c->check_interval == 0);  // solver.py:359
   }
   // big SOC factors: one warp per cone over its chunk partials
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -518,8 +520,11 @@ __global__ void k_init_state(Vec V, const double* wx, const double* wy, const do
     }
     V.u[i] = u;
     V.v[i] = v;
-    if (i < n) V.x[i] = 0.0;
-    if (i >= n && i < n + m) V.Axw[i - n] = 0.0;
+    if (i < n) { V.x[i] = 0.0; V.X2[2 * i] = 0.0; V.X2[2 * i + 1] = u; }
+    if (i >= n && i < n + m) {
+      double* y = V.Y3 + 4 * (i - n);
+      y[0] = 0.0; y[1] = 0.0; y[2] = u; y[3] = 0.0;
+    }
   }
 }
 // x / E  and y / D helpers for point residuals
@@ -540,6 +545,14 @@ __global__ void k_point_dual(const double* aty, const double* E, const double* c
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long i = tid; i < n; i += nt) out[i] = aty[i] / E[i] + c[i];
+}
+// Y3 for the setup solve: slot 0 = b_hat (rhs_y), slots 1..3 = 0
+__global__ void k_fill_y3(double* Y3, const double* b, long long m) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < m; i += nt) {
+    Y3[4 * i] = b[i]; Y3[4 * i + 1] = 0.0; Y3[4 * i + 2] = 0.0; Y3[4 * i + 3] = 0.0;
+  }
 }
 __global__ void k_zero(double* x, long long n) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -987,15 +1000,23 @@ void check_err(scs_handle* h) {
     throw Fail{SCS_ENOCONV, "Jacobi eigensolver did not converge within 100 sweeps"};
 }
 
-// one CG step (A p, A^T, update, p update)
-void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p) {
-  EpiAp ea{};
-  ea.V = V;
-  ea.xs[0] = V.p;
-  launch_spmv(h, h->A, h->LA, ea);
+// one CG step (A p, A^T, update, p update); the first step of an ADMM
+// iteration also closes the previous iteration's termination check
+void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p, bool merged) {
+  if (merged) {
+    EpiAp<true> ea{};
+    ea.V = V;
+    ea.xb = V.X2;
+    launch_spmv(h, h->A, h->LA, ea);
+  } else {
+    EpiAp<false> ea{};
+    ea.V = V;
+    ea.xb = V.X2;
+    launch_spmv(h, h->A, h->LA, ea);
+  }
   EpiAtGp eg{};
   eg.V = V;
-  eg.xs[0] = V.q;
+  eg.xb = V.q;
   launch_spmv(h, h->At, h->LAt, eg);
   k_cg_update<<<elem_grid(h, h->n), kBlock, 0, h->st>>>(V, cap);
   h->launches++;
@@ -1010,10 +1031,9 @@ void solve_g(scs_handle* h) {
   const long long n = h->n, m = h->m;
   Vec G = h->V;
   G.rhs_x = h->ch;
-  G.rhs_y = h->bh;
   G.x = h->V.gx;
-  G.Axw = h->zero_m;
   k_zero<<<elem_grid(h, n), kBlock, 0, h->st>>>(G.x, n);
+  k_fill_y3<<<elem_grid(h, m), kBlock, 0, h->st>>>(G.Y3, h->bh, m);
   const double hn = sqrt(norm2_dev(h, h->ch, h->ch, n, 2) + norm2_dev(h, h->bh, h->bh, m, 2));
   pull_ctl(h);
   Ctl* c = h->ctl_h;
@@ -1023,12 +1043,13 @@ void solve_g(scs_handle* h) {
   c->cg_done = 0;
   c->cg_it = 0;
   c->counter = 0;
+  c->check_pending = 0;
+  c->force_check = 0;
   push_ctl(h);
   const long long cap = 10 * n + 100;  // embedding.py:104
   EpiAtFirst e0{};
   e0.V = G;
-  e0.xs[0] = G.rhs_y;
-  e0.xs[1] = G.Axw;
+  e0.xb = G.Y3;
   launch_spmv(h, h->At, h->LAt, e0);
   long long done_steps = 0;
   while (true) {
@@ -1038,15 +1059,14 @@ void solve_g(scs_handle* h) {
     if (c->cg_done) break;
     const long long batch = std::min<long long>(32, cap - done_steps);
     if (batch <= 0) break;
-    for (long long i = 0; i < batch; ++i) cg_step(h, G, cap, true);
+    for (long long i = 0; i < batch; ++i) cg_step(h, G, cap, true, false);
     done_steps += batch;
   }
   EpiAFinal ef{};
   ef.V = G;
-  ef.xs[0] = G.x;
+  ef.xb = G.x;
   ef.zy_out = h->V.gy;
   ef.setup = 1;
-  // setup finish must run even though stop == 0; cg_it accumulates
   launch_spmv(h, h->A, h->LA, ef);
   pull_ctl(h);
   check_err(h);
@@ -1064,14 +1084,13 @@ void build_graph(scs_handle* h) {
   h->launches++;
   EpiAtFirst e0{};
   e0.V = V;
-  e0.xs[0] = V.rhs_y;
-  e0.xs[1] = V.Axw;
+  e0.xb = V.Y3;
   launch_spmv(h, h->At, h->LAt, e0);
   const long long cgm = h->set.cg_max;
-  for (long long i = 0; i < cgm; ++i) cg_step(h, V, cgm, i + 1 < cgm);
+  for (long long i = 0; i < cgm; ++i) cg_step(h, V, cgm, i + 1 < cgm, i == 0);
   EpiAFinal ef{};
   ef.V = V;
-  ef.xs[0] = V.x;
+  ef.xb = V.x;
   ef.zy_out = V.zy;
   ef.setup = 0;
   launch_spmv(h, h->A, h->LA, ef);
@@ -1085,14 +1104,6 @@ void build_graph(scs_handle* h) {
     k_cone_apply<<<g, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side);
     h->launches++;
   }
-  EpiResA ra{};
-  ra.V = V;
-  ra.xs[0] = V.u;
-  launch_spmv(h, h->A, h->LA, ra);
-  EpiResAt rt{};
-  rt.V = V;
-  rt.xs[0] = V.u + h->n;
-  launch_spmv(h, h->At, h->LAt, rt);
   cudaGraph_t g;
   CK(cudaStreamEndCapture(h->st, &g));
   CK(cudaGraphInstantiate(&h->gexec, g, 0));
@@ -1100,14 +1111,15 @@ void build_graph(scs_handle* h) {
   h->launches_per_iter = h->launches - before;
 }
 
+// stand-alone termination check / residual evaluation of the current state
 void launch_residuals(scs_handle* h) {
   EpiResA ra{};
   ra.V = h->V;
-  ra.xs[0] = h->V.u;
+  ra.xb = h->V.u;
   launch_spmv(h, h->A, h->LA, ra);
   EpiResAt rt{};
   rt.V = h->V;
-  rt.xs[0] = h->V.u + h->n;
+  rt.xb = h->V.u + h->n;
   launch_spmv(h, h->At, h->LAt, rt);
 }
 
@@ -1143,7 +1155,7 @@ void do_begin(scs_handle* h, const double* wx, const double* wy, const double* w
   c->err = 0;
   c->warm_zero = 1;
   c->force_check = 0;
-  c->check_now = 0;
+  c->check_pending = 0;
   c->counter = 0;
   c->max_iters = h->set.max_iters;
   c->check_interval = h->set.check_interval;
@@ -1174,13 +1186,20 @@ void do_steps(scs_handle* h, long long k) {
     throw Fail{SCS_ECUDA, "internal: iteration count mismatch"};
 }
 
-// post-loop status (solver.py:364-369)
+// Loop exit (solver.py:359-369): the last iteration's termination check is
+// still pending (it normally rides on the next iteration's first passes);
+// run it stand-alone, then apply the post-loop status rule.
 void do_finish(scs_handle* h) {
   Ctl* c = h->ctl_h;
   pull_ctl(h);
   if (c->status != SCS_RUNNING) return;
+  if (c->check_pending && !c->stop) {
+    launch_residuals(h);
+    pull_ctl(h);
+    check_err(h);
+    if (c->status != SCS_RUNNING) return;
+  }
   c->force_check = 1;
-  c->check_now = 1;
   c->stop = 0;
   push_ctl(h);
   launch_residuals(h);
@@ -1316,13 +1335,12 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     V.gx = dalloc<double>(h, n);
     V.gy = dalloc<double>(h, m);
     V.rhs_x = dalloc<double>(h, n);
-    V.rhs_y = dalloc<double>(h, m);
     V.x = dalloc<double>(h, n);
     V.r = dalloc<double>(h, n);
-    V.p = dalloc<double>(h, n);
     V.Gp = dalloc<double>(h, n);
+    V.X2 = dalloc<double>(h, 2 * n);
+    V.Y3 = dalloc<double>(h, 4 * m);
     V.q = dalloc<double>(h, m);
-    V.Axw = dalloc<double>(h, m);
     V.zy = dalloc<double>(h, m);
     V.part = dalloc<double>(h, (size_t)kMaxRed * kMaxGrid);
     V.chunk_part = dalloc<double>(h, std::max(h->K.n_chunk, 1));
@@ -1437,7 +1455,7 @@ int scs_apply_a(scs_handle* h, int which, const double* in, double* out) {
     h2d(h, din, in, nin);
     EpiPlain e{};
     e.V = h->V;
-    e.xs[0] = din;
+    e.xb = din;
     e.out = dout;
     if (which == 0) launch_spmv(h, h->A, h->LA, e);
     else launch_spmv(h, h->At, h->LAt, e);
@@ -1456,7 +1474,7 @@ int scs_point_residuals(scs_handle* h, const double* x, const double* y, const d
     k_div<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->tmp_n, h->E, n, h->V.r);
     EpiPlain e{};
     e.V = h->V;
-    e.xs[0] = h->V.r;
+    e.xb = h->V.r;
     e.out = h->tmp_m2;
     launch_spmv(h, h->A, h->LA, e);
     h2d(h, h->tmp_m, s, m);
@@ -1467,11 +1485,11 @@ int scs_point_residuals(scs_handle* h, const double* x, const double* y, const d
     k_div<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->tmp_m, h->D, m, h->tmp_m2);
     EpiPlain f{};
     f.V = h->V;
-    f.xs[0] = h->tmp_m2;
+    f.xb = h->tmp_m2;
     f.out = h->V.Gp;
     launch_spmv(h, h->At, h->LAt, f);
-    k_point_dual<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->V.Gp, h->E, h->c0, n, h->V.p);
-    const double dual = sqrt(norm2_dev(h, h->V.p, h->V.p, n, 2));
+    k_point_dual<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->V.Gp, h->E, h->c0, n, h->V.r);
+    const double dual = sqrt(norm2_dev(h, h->V.r, h->V.r, n, 2));
     const double cn = sqrt(norm2_dev(h, h->c0, h->c0, n, 2));
     const double ctx = norm2_dev(h, h->c0, h->tmp_n, n, 2);
     const double bty = norm2_dev(h, h->b0, h->tmp_m, m, 2);
@@ -1522,6 +1540,8 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t
     V.gx = dalloc<double>(h, n);
     V.gy = dalloc<double>(h, m);
     V.zy = dalloc<double>(h, m);
+    V.X2 = dalloc<double>(h, 2 * n);
+    V.Y3 = dalloc<double>(h, 4 * m);
     double* zc = dalloc<double>(h, std::max<long long>(n, m));
     V.c = zc; V.b = zc;
     V.part = dalloc<double>(h, (size_t)kMaxRed * kMaxGrid);
@@ -1593,14 +1613,14 @@ int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms, double* 
     CK(cudaEventCreate(&e1));
     auto one = [&] {
       if (kind == 0) {
-        EpiAp ea{};
+        EpiAp<false> ea{};
         ea.V = h->V;
-        ea.xs[0] = h->V.p;
+        ea.xb = h->V.X2;
         launch_spmv(h, h->A, h->LA, ea);
       } else {
         EpiAtGp eg{};
         eg.V = h->V;
-        eg.xs[0] = h->V.q;
+        eg.xb = h->V.q;
         launch_spmv(h, h->At, h->LAt, eg);
       }
     };
@@ -1614,7 +1634,7 @@ int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms, double* 
     *ms = f / (double)std::max<int64_t>(reps, 1);
     // algorithmic bytes: values + column indices, row pointers, the gathered
     // vector once, the epilogue vectors
-    if (kind == 0) *bytes = 12.0 * nnz + 8.0 * (m + 1) + 8.0 * n + 8.0 * m;
+    if (kind == 0) *bytes = 12.0 * nnz + 8.0 * (m + 1) + 8.0 * n + 8.0 * m;  // p gathered once
     else *bytes = 12.0 * nnz + 8.0 * (n + 1) + 8.0 * m + 16.0 * n;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
