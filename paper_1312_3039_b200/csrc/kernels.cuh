@@ -174,9 +174,13 @@ __global__ void __launch_bounds__(kBlock) k_spmv(Csr A, Epi epi0) {
   for (long long base = warp * kGroups; base < A.rows; base += nwarps * kGroups) {
     const long long row = base + gi;
     const bool valid = row < A.rows;
+    // epilogue operands are loaded before the dot product so their latency
+    // overlaps the matrix stream instead of stalling the warp afterwards
+    typename Epi::Pre pre;
+    if (valid) epi.pre(row, pre);
     double s[Epi::NV];
     row_dot<L, Epi::NV, Epi::STRIDE>(A, row, valid, gl, epi.xb, s);
-    if (valid && gl == 0) epi.row(row, s, red);
+    if (valid && gl == 0) epi.row(row, s, pre, red);
   }
   epi.extra(red);
   if constexpr (Epi::NR > 0) {
@@ -192,6 +196,8 @@ struct EpiBase {
   Vec V;
   const double* xb;  // gather base
   int pend;          // residual check of the previous iteration rides along
+  struct Pre {};
+  __device__ void pre(long long, Pre&) const {}
   __device__ void extra(double*) const {}
   __device__ __forceinline__ double utau() const { return V.u[V.n + V.m]; }
 };
@@ -207,20 +213,26 @@ struct EpiAtFirst : EpiBase {
     pend = V.ctl->check_pending;
     return !V.ctl->stop;
   }
-  __device__ void row(long long j, const double (&s)[3], double* red) const {
-    const double cg_rhs = V.rhs_x[j] - s[0];
-    const double gx = V.x[j] + s[1];
+  struct Pre { double rx, x, e, c, ux, ut; };
+  __device__ void pre(long long j, Pre& p) const {
+    p.rx = V.rhs_x[j];
+    p.x = V.x[j];
+    if (pend) { p.e = V.E[j]; p.c = V.c[j]; p.ux = V.X2[2 * j + 1]; p.ut = utau(); }
+  }
+  __device__ void row(long long j, const double (&s)[3], const Pre& p, double* red) const {
+    const double cg_rhs = p.rx - s[0];
+    const double gx = p.x + s[1];
     const double r = cg_rhs - gx;
     V.r[j] = r;
     V.X2[2 * j] = r;
     red[0] += r * r;
     if (pend) {
-      const double ei = 1.0 / V.E[j];
-      const double du = ei * (s[2] / utau() + V.c[j]);
+      const double ei = 1.0 / p.e;
+      const double du = ei * (s[2] / p.ut + p.c);
       const double inf = ei * s[2];
       red[1] += du * du;
       red[2] += inf * inf;
-      red[3] += V.c[j] * V.X2[2 * j + 1];
+      red[3] += p.c * p.ux;
     }
   }
   __device__ void finish(const double* tot) const {
@@ -247,17 +259,25 @@ struct EpiAp : EpiBase {
     pend = MERGED ? c->check_pending : 0;
     return !c->stop && (!c->cg_done || pend);
   }
-  __device__ void row(long long i, const double (&s)[NV], double* red) const {
+  struct Pre { double vs, d, b, uy, ut; };
+  __device__ void pre(long long i, Pre& p) const {
+    if constexpr (MERGED) {
+      if (pend) {
+        p.vs = V.v[V.n + i]; p.d = V.D[i]; p.b = V.b[i]; p.uy = V.Y3[4 * i + 2]; p.ut = utau();
+      }
+    }
+  }
+  __device__ void row(long long i, const double (&s)[NV], const Pre& p, double* red) const {
     V.q[i] = s[0];
     if constexpr (MERGED) {
       if (pend) {
-        const double t = s[1] + V.v[V.n + i];
-        const double di = 1.0 / V.D[i];
-        const double pr = di * (t / utau() - V.b[i]);
+        const double t = s[1] + p.vs;
+        const double di = 1.0 / p.d;
+        const double pr = di * (t / p.ut - p.b);
         const double ub = di * t;
         red[0] += pr * pr;
         red[1] += ub * ub;
-        red[2] += V.b[i] * V.Y3[4 * i + 2];
+        red[2] += p.b * p.uy;
       }
     }
   }
@@ -276,8 +296,10 @@ struct EpiAp : EpiBase {
 struct EpiAtGp : EpiBase {
   static constexpr int NV = 1, STRIDE = 1, NR = 1;
   __device__ bool load() { return !V.ctl->stop && !V.ctl->cg_done; }
-  __device__ void row(long long j, const double (&s)[1], double* red) const {
-    const double pj = V.X2[2 * j];
+  struct Pre { double p; };
+  __device__ void pre(long long j, Pre& p) const { p.p = V.X2[2 * j]; }
+  __device__ void row(long long j, const double (&s)[1], const Pre& pf, double* red) const {
+    const double pj = pf.p;
     const double g = pj + s[0];
     V.Gp[j] = g;
     red[0] += pj * g;
@@ -299,11 +321,13 @@ struct EpiAFinal : EpiBase {
   double* zy_out;
   int setup;
   __device__ bool load() { return !V.ctl->stop; }
-  __device__ void row(long long i, const double (&s)[1], double* red) const {
-    const double z = V.Y3[4 * i] + s[0];
+  struct Pre { double ry, b; };
+  __device__ void pre(long long i, Pre& p) const { p.ry = V.Y3[4 * i]; p.b = V.b[i]; }
+  __device__ void row(long long i, const double (&s)[1], const Pre& p, double* red) const {
+    const double z = p.ry + s[0];
     zy_out[i] = z;
     if (!setup) V.Y3[4 * i + 1] = s[0];
-    red[1] += V.b[i] * z;
+    red[1] += p.b * z;
   }
   __device__ void extra(double* red) const {
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -332,14 +356,18 @@ struct EpiResA : EpiBase {
     const Ctl* c = V.ctl;
     return !c->stop && (c->check_pending || c->force_check);
   }
-  __device__ void row(long long i, const double (&s)[1], double* red) const {
-    const double t = s[0] + V.v[V.n + i];
-    const double di = 1.0 / V.D[i];
-    const double pr = di * (t / utau() - V.b[i]);
+  struct Pre { double vs, d, b, uy, ut; };
+  __device__ void pre(long long i, Pre& p) const {
+    p.vs = V.v[V.n + i]; p.d = V.D[i]; p.b = V.b[i]; p.uy = V.u[V.n + i]; p.ut = utau();
+  }
+  __device__ void row(long long i, const double (&s)[1], const Pre& p, double* red) const {
+    const double t = s[0] + p.vs;
+    const double di = 1.0 / p.d;
+    const double pr = di * (t / p.ut - p.b);
     const double ub = di * t;
     red[0] += pr * pr;
     red[1] += ub * ub;
-    red[2] += V.b[i] * V.u[V.n + i];
+    red[2] += p.b * p.uy;
   }
   __device__ void finish(const double* tot) const {
     if (threadIdx.x) return;
@@ -356,13 +384,17 @@ struct EpiResAt : EpiBase {
     const Ctl* c = V.ctl;
     return !c->stop && (c->check_pending || c->force_check);
   }
-  __device__ void row(long long j, const double (&s)[1], double* red) const {
-    const double ei = 1.0 / V.E[j];
-    const double du = ei * (s[0] / utau() + V.c[j]);
+  struct Pre { double e, c, ux, ut; };
+  __device__ void pre(long long j, Pre& p) const {
+    p.e = V.E[j]; p.c = V.c[j]; p.ux = V.u[j]; p.ut = utau();
+  }
+  __device__ void row(long long j, const double (&s)[1], const Pre& p, double* red) const {
+    const double ei = 1.0 / p.e;
+    const double du = ei * (s[0] / p.ut + p.c);
     const double inf = ei * s[0];
     red[0] += du * du;
     red[1] += inf * inf;
-    red[2] += V.c[j] * V.u[j];
+    red[2] += p.c * p.ux;
   }
   __device__ void finish(const double* tot) const {
     if (threadIdx.x) return;
@@ -377,7 +409,7 @@ struct EpiPlain : EpiBase {
   static constexpr int NV = 1, STRIDE = 1, NR = 0;
   double* out;
   __device__ bool load() { return true; }
-  __device__ void row(long long i, const double (&s)[1], double*) const { out[i] = s[0]; }
+  __device__ void row(long long i, const double (&s)[1], const Pre&, double*) const { out[i] = s[0]; }
   __device__ void finish(const double*) const {}
 };
 
