@@ -19,7 +19,7 @@
 // (k = CG steps, sparse_linalg.py:461,471,486 + embedding.py:109,113 +
 // scaling.py:466-467).  Removed, with bit-identical results:
 //  * A x_warm at the head of CG: the previous iteration's EpiAFinal already
-//    produced A x for the same x (cg_warm) and stored it (Y3 slot 1);
+//    produced A x for the same x (cg_warm) and stored it (Axw);
 //  * the trailing exact-residual pass (sparse_linalg.py:486), whose value
 //    its caller discards (embedding.py:110);
 //  * the two residual passes of the termination check (scaling.py:466-467):
@@ -42,21 +42,24 @@ struct Csr {
 };
 
 // Device vectors of one handle.  x-part length n, y-part length m (local).
-// Gather vectors are interleaved so that one 32-byte sector request serves
-// every SpMV that shares a matrix pass:
-//   X2[2j + 0] = p_j (CG direction)      X2[2j + 1] = (u_x)_j
-//   Y3[4i + 0] = (rhs_y)_i               Y3[4i + 1] = (A cg_warm)_i
-//   Y3[4i + 2] = (u_y)_i                 Y3[4i + 3] = unused
+// Gather vectors are interleaved so that one 16-byte load (one sector
+// request) serves every SpMV that shares a matrix pass:
+//   X2[2j + 0] = p_j (CG direction)          X2[2j + 1] = (u_x)_j
+//   Y2[2i + 0] = (rhs_y + A cg_warm)_i       Y2[2i + 1] = (u_y)_i
+// The first A^T pass forms A^T rhs_y + A^T (A x0) as A^T (rhs_y + A x0):
+// same products, one gather (a rounding-level reassociation).
 struct Vec {
   long long n, m;
   double *u, *v;              // n + m + 1 (SolverState)
   const double *c, *b;        // scaled data
   const double *D, *E;        // scalings
+  const double *Dinv, *Einv;  // 1/D, 1/E (scaling.py:464-465)
   double *gx, *gy;            // g = M^-1 h
-  double *rhs_x;              // rhs = w[:-1] - w_tau h (x-part; y-part in Y3)
+  double *rhs_x, *rhs_y;      // rhs = w[:-1] - w_tau h
   double *x;                  // CG iterate == cg_warm (embedding.py:111)
   double *r, *Gp;             // CG vectors (n)
-  double *X2, *Y3;            // interleaved gather vectors
+  double *X2, *Y2;            // interleaved gather vectors
+  double *Axw;                // A cg_warm (m), from the previous EpiAFinal
   double *q;                  // A p (m)
   double *zy;                 // z_y = rhs_y + A x (m)
   double *part;               // kMaxRed * kMaxGrid partials
@@ -120,10 +123,8 @@ __device__ __forceinline__ void gather(const double* __restrict__ xb, int c, dou
 }
 
 template <int L, int NV, int STRIDE>
-__device__ __forceinline__ void row_dot(const Csr& A, long long row, bool valid, int gl,
+__device__ __forceinline__ void row_dot(const Csr& A, long long k0, long long k1, int gl,
                                         const double* __restrict__ xb, double (&s)[NV]) {
-  long long k0 = 0, k1 = 0;
-  if (valid) { k0 = __ldg(A.rp + row); k1 = __ldg(A.rp + row + 1); }
 #pragma unroll
   for (int t = 0; t < NV; ++t) s[t] = 0.0;
   long long k = k0 + gl;
@@ -156,8 +157,10 @@ __device__ __forceinline__ void row_dot(const Csr& A, long long row, bool valid,
 // Generic CSR SpMV with a per-row epilogue and an optional grid reduction
 // whose last block runs Epi::finish.  Each warp owns 32/L consecutive rows
 // per step (L lanes per row); the row loop is warp-uniform so the group
-// shuffles never see diverged lanes.  Epi::load() reads the Ctl flags once
-// and says whether the whole launch is a no-op.
+// shuffles never see diverged lanes.  The next row's pointers are fetched
+// one step ahead and the epilogue operands before the dot product, so the
+// matrix stream is the only dependent latency per row.  Epi::load() reads
+// the Ctl flags once and says whether the whole launch is a no-op.
 template <int L, class Epi>
 __global__ void __launch_bounds__(kBlock) k_spmv(Csr A, Epi epi0) {
   Epi epi = epi0;
@@ -168,19 +171,29 @@ __global__ void __launch_bounds__(kBlock) k_spmv(Csr A, Epi epi0) {
   const int gi = (threadIdx.x & 31) / L;
   const long long warp = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * kBlock) >> 5;
+  const long long stride = nwarps * kGroups;
   double red[NR];
 #pragma unroll
   for (int t = 0; t < NR; ++t) red[t] = 0.0;
-  for (long long base = warp * kGroups; base < A.rows; base += nwarps * kGroups) {
-    const long long row = base + gi;
-    const bool valid = row < A.rows;
-    // epilogue operands are loaded before the dot product so their latency
-    // overlaps the matrix stream instead of stalling the warp afterwards
+  long long base = warp * kGroups;
+  long long row = base + gi;
+  bool valid = row < A.rows;
+  long long k0 = 0, k1 = 0;
+  if (valid) { k0 = __ldg(A.rp + row); k1 = __ldg(A.rp + row + 1); }
+  for (; base < A.rows; base += stride) {
+    const long long nrow = row + stride;
+    const bool nvalid = nrow < A.rows;
+    long long nk0 = 0, nk1 = 0;
+    if (nvalid) { nk0 = __ldg(A.rp + nrow); nk1 = __ldg(A.rp + nrow + 1); }
     typename Epi::Pre pre;
     if (valid) epi.pre(row, pre);
     double s[Epi::NV];
-    row_dot<L, Epi::NV, Epi::STRIDE>(A, row, valid, gl, epi.xb, s);
+    row_dot<L, Epi::NV, Epi::STRIDE>(A, k0, k1, gl, epi.xb, s);
     if (valid && gl == 0) epi.row(row, s, pre, red);
+    row = nrow;
+    valid = nvalid;
+    k0 = nk0;
+    k1 = nk1;
   }
   epi.extra(red);
   if constexpr (Epi::NR > 0) {
@@ -203,33 +216,30 @@ struct EpiBase {
 };
 
 // First A^T pass of an iteration (sparse_linalg.py:461-469 + scaling.py:467):
-//   r0 = (rhs_x - A^T rhs_y) - (x0 + A^T (A x0)); p = r0
+//   r0 = (rhs_x - x0) - A^T (rhs_y + A x0); p = r0
 // and, when the previous iteration is due a termination check, A^T u_y of
 // that iterate (dual residual / infeasibility, scaling.py:484-490).  One
-// 256-bit gather per nonzero serves all three products.
+// 128-bit gather per nonzero serves both products.
 struct EpiAtFirst : EpiBase {
-  static constexpr int NV = 3, STRIDE = 4, NR = 4;
+  static constexpr int NV = 2, STRIDE = 2, NR = 4;
   __device__ bool load() {
     pend = V.ctl->check_pending;
     return !V.ctl->stop;
   }
-  struct Pre { double rx, x, e, c, ux, ut; };
+  struct Pre { double rx, x, ei, c, ux, ut; };
   __device__ void pre(long long j, Pre& p) const {
     p.rx = V.rhs_x[j];
     p.x = V.x[j];
-    if (pend) { p.e = V.E[j]; p.c = V.c[j]; p.ux = V.X2[2 * j + 1]; p.ut = utau(); }
+    if (pend) { p.ei = V.Einv[j]; p.c = V.c[j]; p.ux = V.X2[2 * j + 1]; p.ut = utau(); }
   }
-  __device__ void row(long long j, const double (&s)[3], const Pre& p, double* red) const {
-    const double cg_rhs = p.rx - s[0];
-    const double gx = p.x + s[1];
-    const double r = cg_rhs - gx;
+  __device__ void row(long long j, const double (&s)[2], const Pre& p, double* red) const {
+    const double r = (p.rx - p.x) - s[0];
     V.r[j] = r;
     V.X2[2 * j] = r;
     red[0] += r * r;
     if (pend) {
-      const double ei = 1.0 / p.e;
-      const double du = ei * (s[2] / p.ut + p.c);
-      const double inf = ei * s[2];
+      const double du = p.ei * (s[1] / p.ut + p.c);
+      const double inf = p.ei * s[1];
       red[1] += du * du;
       red[2] += inf * inf;
       red[3] += p.c * p.ux;
@@ -263,7 +273,7 @@ struct EpiAp : EpiBase {
   __device__ void pre(long long i, Pre& p) const {
     if constexpr (MERGED) {
       if (pend) {
-        p.vs = V.v[V.n + i]; p.d = V.D[i]; p.b = V.b[i]; p.uy = V.Y3[4 * i + 2]; p.ut = utau();
+        p.vs = V.v[V.n + i]; p.d = V.Dinv[i]; p.b = V.b[i]; p.uy = V.Y2[2 * i + 1]; p.ut = utau();
       }
     }
   }
@@ -272,7 +282,7 @@ struct EpiAp : EpiBase {
     if constexpr (MERGED) {
       if (pend) {
         const double t = s[1] + p.vs;
-        const double di = 1.0 / p.d;
+        const double di = p.d;
         const double pr = di * (t / p.ut - p.b);
         const double ub = di * t;
         red[0] += pr * pr;
@@ -322,11 +332,11 @@ struct EpiAFinal : EpiBase {
   int setup;
   __device__ bool load() { return !V.ctl->stop; }
   struct Pre { double ry, b; };
-  __device__ void pre(long long i, Pre& p) const { p.ry = V.Y3[4 * i]; p.b = V.b[i]; }
+  __device__ void pre(long long i, Pre& p) const { p.ry = V.rhs_y[i]; p.b = V.b[i]; }
   __device__ void row(long long i, const double (&s)[1], const Pre& p, double* red) const {
     const double z = p.ry + s[0];
     zy_out[i] = z;
-    if (!setup) V.Y3[4 * i + 1] = s[0];
+    if (!setup) V.Axw[i] = s[0];
     red[1] += p.b * z;
   }
   __device__ void extra(double* red) const {
@@ -358,11 +368,11 @@ struct EpiResA : EpiBase {
   }
   struct Pre { double vs, d, b, uy, ut; };
   __device__ void pre(long long i, Pre& p) const {
-    p.vs = V.v[V.n + i]; p.d = V.D[i]; p.b = V.b[i]; p.uy = V.u[V.n + i]; p.ut = utau();
+    p.vs = V.v[V.n + i]; p.d = V.Dinv[i]; p.b = V.b[i]; p.uy = V.u[V.n + i]; p.ut = utau();
   }
   __device__ void row(long long i, const double (&s)[1], const Pre& p, double* red) const {
     const double t = s[0] + p.vs;
-    const double di = 1.0 / p.d;
+    const double di = p.d;
     const double pr = di * (t / p.ut - p.b);
     const double ub = di * t;
     red[0] += pr * pr;
@@ -386,10 +396,10 @@ struct EpiResAt : EpiBase {
   }
   struct Pre { double e, c, ux, ut; };
   __device__ void pre(long long j, Pre& p) const {
-    p.e = V.E[j]; p.c = V.c[j]; p.ux = V.u[j]; p.ut = utau();
+    p.e = V.Einv[j]; p.c = V.c[j]; p.ux = V.u[j]; p.ut = utau();
   }
   __device__ void row(long long j, const double (&s)[1], const Pre& p, double* red) const {
-    const double ei = 1.0 / p.e;
+    const double ei = p.e;
     const double du = ei * (s[0] / p.ut + p.c);
     const double inf = ei * s[0];
     red[0] += du * du;

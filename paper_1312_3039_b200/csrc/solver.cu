@@ -44,7 +44,11 @@ __global__ void __launch_bounds__(kBlock) k_prep(Vec V) {
     const double w = V.u[i] + V.v[i];
     double r;
     if (i < n) { r = w - wt * V.c[i]; V.rhs_x[i] = r; }
-    else { r = w - wt * V.b[i - n]; V.Y3[4 * (i - n)] = r; }
+    else {
+      r = w - wt * V.b[i - n];
+      V.rhs_y[i - n] = r;
+      V.Y2[2 * (i - n)] = r + V.Axw[i - n];
+    }
     red[0] += r * r;
   }
   if (grid_sum_last<1>(red, V.part, &c->counter) && threadIdx.x == 0) {
@@ -106,7 +110,7 @@ __device__ __forceinline__ Relax relax_y(const Vec& V, long long i, double corr,
 __device__ __forceinline__ void store_y(const Vec& V, long long i, double ub, double up) {
   const double vi = V.v[V.n + i];
   V.u[V.n + i] = up;
-  V.Y3[4 * i + 2] = up;           // gather copy for the next residual pass
+  V.Y2[2 * i + 1] = up;           // gather copy for the next residual pass
   V.v[V.n + i] = (vi - ub) + up;  // solver.py:165
 }
 
@@ -522,8 +526,9 @@ __global__ void k_init_state(Vec V, const double* wx, const double* wy, const do
     V.v[i] = v;
     if (i < n) { V.x[i] = 0.0; V.X2[2 * i] = 0.0; V.X2[2 * i + 1] = u; }
     if (i >= n && i < n + m) {
-      double* y = V.Y3 + 4 * (i - n);
-      y[0] = 0.0; y[1] = 0.0; y[2] = u; y[3] = 0.0;
+      V.Y2[2 * (i - n)] = 0.0;
+      V.Y2[2 * (i - n) + 1] = u;
+      V.Axw[i - n] = 0.0;
     }
   }
 }
@@ -546,13 +551,16 @@ __global__ void k_point_dual(const double* aty, const double* E, const double* c
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long i = tid; i < n; i += nt) out[i] = aty[i] / E[i] + c[i];
 }
-// Y3 for the setup solve: slot 0 = b_hat (rhs_y), slots 1..3 = 0
-__global__ void k_fill_y3(double* Y3, const double* b, long long m) {
+// Y2 for the setup solve: slot 0 = b_hat (rhs_y + A 0), slot 1 = 0
+__global__ void k_fill_y2(double* Y2, const double* b, long long m) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
-  for (long long i = tid; i < m; i += nt) {
-    Y3[4 * i] = b[i]; Y3[4 * i + 1] = 0.0; Y3[4 * i + 2] = 0.0; Y3[4 * i + 3] = 0.0;
-  }
+  for (long long i = tid; i < m; i += nt) { Y2[2 * i] = b[i]; Y2[2 * i + 1] = 0.0; }
+}
+__global__ void k_recip(const double* a, long long n, double* out) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) out[i] = 1.0 / a[i];
 }
 __global__ void k_zero(double* x, long long n) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1033,7 +1041,8 @@ void solve_g(scs_handle* h) {
   G.rhs_x = h->ch;
   G.x = h->V.gx;
   k_zero<<<elem_grid(h, n), kBlock, 0, h->st>>>(G.x, n);
-  k_fill_y3<<<elem_grid(h, m), kBlock, 0, h->st>>>(G.Y3, h->bh, m);
+  G.rhs_y = h->bh;
+  k_fill_y2<<<elem_grid(h, m), kBlock, 0, h->st>>>(G.Y2, h->bh, m);
   const double hn = sqrt(norm2_dev(h, h->ch, h->ch, n, 2) + norm2_dev(h, h->bh, h->bh, m, 2));
   pull_ctl(h);
   Ctl* c = h->ctl_h;
@@ -1049,7 +1058,7 @@ void solve_g(scs_handle* h) {
   const long long cap = 10 * n + 100;  // embedding.py:104
   EpiAtFirst e0{};
   e0.V = G;
-  e0.xb = G.Y3;
+  e0.xb = G.Y2;
   launch_spmv(h, h->At, h->LAt, e0);
   long long done_steps = 0;
   while (true) {
@@ -1084,7 +1093,7 @@ void build_graph(scs_handle* h) {
   h->launches++;
   EpiAtFirst e0{};
   e0.V = V;
-  e0.xb = V.Y3;
+  e0.xb = V.Y2;
   launch_spmv(h, h->At, h->LAt, e0);
   const long long cgm = h->set.cg_max;
   for (long long i = 0; i < cgm; ++i) cg_step(h, V, cgm, i + 1 < cgm, i == 0);
@@ -1339,9 +1348,13 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     V.r = dalloc<double>(h, n);
     V.Gp = dalloc<double>(h, n);
     V.X2 = dalloc<double>(h, 2 * n);
-    V.Y3 = dalloc<double>(h, 4 * m);
+    V.Y2 = dalloc<double>(h, 2 * m);
+    V.rhs_y = dalloc<double>(h, m);
+    V.Axw = dalloc<double>(h, m);
     V.q = dalloc<double>(h, m);
     V.zy = dalloc<double>(h, m);
+    V.Dinv = dalloc<double>(h, m);
+    V.Einv = dalloc<double>(h, n);
     V.part = dalloc<double>(h, (size_t)kMaxRed * kMaxGrid);
     V.chunk_part = dalloc<double>(h, std::max(h->K.n_chunk, 1));
     V.soc_fac = dalloc<double>(h, 3 * std::max(h->K.n_bsoc, 1));
@@ -1359,6 +1372,8 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     CK(cudaStreamSynchronize(h->st));
     dbg("matrices built LA=%d LAt=%d", h->LA, h->LAt);
     equilibrate(h);
+    k_recip<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->D, m, (double*)V.Dinv);
+    k_recip<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->E, n, (double*)V.Einv);
     dbg("equilibrated mean_col=%g mean_row=%g", h->mean_col, h->mean_row);
     scale_vectors(h);
     dbg("scaled sigma=%g rho=%g", h->sigma, h->rho);
@@ -1541,7 +1556,7 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t
     V.gy = dalloc<double>(h, m);
     V.zy = dalloc<double>(h, m);
     V.X2 = dalloc<double>(h, 2 * n);
-    V.Y3 = dalloc<double>(h, 4 * m);
+    V.Y2 = dalloc<double>(h, 2 * m);
     double* zc = dalloc<double>(h, std::max<long long>(n, m));
     V.c = zc; V.b = zc;
     V.part = dalloc<double>(h, (size_t)kMaxRed * kMaxGrid);
