@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SCS_B200_ABI_VERSION 1
+#define SCS_B200_ABI_VERSION 2
 
 /* error codes -> Python exception classes:
  *   SCS_EINVAL, SCS_ENONFINITE -> ValueError (problem.py:38-53,
@@ -97,10 +97,20 @@ typedef struct {
   int32_t fast;     /* 0: reference algorithm (parity); 1: opt-in fast mode */
 } scs_settings;
 
-/* Distributed launch (row sharding over NCCL); NULL -> single GPU. */
+/* Distributed launch (row sharding); NULL -> single GPU.  Rank k passes
+ * rows [bounds[k], bounds[k+1]) (scs_problem.row_lo / m / m_global).  Ranks
+ * are one process per GPU joined by NCCL (nccl_id), or -- to test the
+ * sharded kernels on one GPU -- one host thread per shard in one process
+ * joined by an emulated group (emu_group).  flags & 1 forces the sharded
+ * code path (all-reduce points included) even when world == 1. */
+typedef struct scs_emu_group scs_emu_group;
 typedef struct {
   int32_t rank, world;
-  const uint8_t* nccl_id; /* 128 bytes from scs_nccl_unique_id on rank 0 */
+  const uint8_t* nccl_id;  /* 128 bytes from scs_nccl_unique_id on rank 0 */
+  scs_emu_group* emu_group;
+  const int64_t* bounds;   /* world + 1 global row bounds */
+  int32_t flags;
+  int32_t pad_;
 } scs_dist;
 
 /* Residuals (scaling.py:37-55, same field order) and iteration info
@@ -189,6 +199,15 @@ int scs_abi_version(void);
 /* NCCL bootstrap for world > 1: rank 0 creates the id and the host
  * broadcasts it (torch.distributed store / gloo) to the other ranks. */
 int scs_nccl_unique_id(uint8_t* out128);
+
+/* Sum `n` host doubles over the shards of a row-sharded handle (in place);
+ * a no-op copy for a single shard.  Used by the host for the m-length dot
+ * products of extract_solution (b'y, certificate normalisation). */
+int scs_allreduce(scs_handle* h, double* vals, int64_t n);
+
+/* In-process emulated group of `world` shards on one GPU (tests). */
+scs_emu_group* scs_emu_group_create(int32_t world);
+void scs_emu_group_destroy(scs_emu_group* g);
 
 /* Row partition for sharding: splits [0, m) into `world` contiguous ranges
  * at cone-block boundaries (only a second-order cone may straddle),

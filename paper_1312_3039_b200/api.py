@@ -350,16 +350,21 @@ class Workspace:
     case ``data`` holds this rank's row slice (see parallel.shard_problem).
     """
 
-    def __init__(self, data, settings=None, dist=None, row_lo=0, m_global=None):
+    def __init__(self, data, settings=None, dist=None):
         self.settings = settings if settings is not None else Settings()
         if not isinstance(self.settings, Settings):
             self.settings = Settings.from_reference(self.settings)
-        self.data = as_problem(data) if m_global is None else data
+        self._dist = dist
+        if dist is None:
+            self.data = as_problem(data)
+        else:
+            from .parallel import ShardProblem
+            if not isinstance(data, ShardProblem):  # a whole problem as one shard
+                d = as_problem(data)
+                data = ShardProblem(d.A.colptr, d.A.rowidx, d.A.vals, d.b, d.c, d.spec, 0, d.m)
+            self.data = data
         self._lib = native.load()
         self._h = None
-        self._dist = dist
-        self._row_lo = row_lo
-        self._m_global = m_global
         t0 = time.perf_counter()
         self._create()
         self.setup_time = time.perf_counter() - t0
@@ -367,20 +372,31 @@ class Workspace:
         self.final_state = None
         self._scal = None
 
+    @property
+    def sharded(self):
+        return self._dist is not None
+
     # -- native plumbing ------------------------------------------------------
+    def _arrays(self):
+        d = self.data
+        if self._dist is None:
+            A = d.A
+            return (A.nrows, A.ncols, A.colptr, A.rowidx, A.vals, d.b, d.c, d.spec, 0, 0)
+        return (d.m, d.n, d.colptr, d.rowidx, d.vals, d.b, d.c, d.spec, d.row_lo, d.m_global)
+
     def _create(self):
-        d, st = self.data, self.settings
-        A, spec = d.A, d.spec
-        self._keep = [native.i64(A.colptr), native.i64(A.rowidx), native.f64(A.vals),
-                      native.f64(d.b), native.f64(d.c), native.i64(spec.soc_dims),
+        st = self.settings
+        m, n, colptr, rowidx, vals, b, c, spec, row_lo, m_global = self._arrays()
+        self._keep = [native.i64(colptr), native.i64(rowidx), native.f64(vals),
+                      native.f64(b), native.f64(c), native.i64(spec.soc_dims),
                       native.i64(spec.psd_sides)]
-        cp, ri, va, b, c, q, s = self._keep
+        cp, ri, va, bb, cc, q, s = self._keep
         P = native.Problem(
-            m=A.nrows, n=A.ncols, colptr=native.ptr(cp, native.i64p),
-            rowidx=native.ptr(ri, native.i64p), vals=native.ptr(va), b=native.ptr(b),
-            c=native.ptr(c), z=spec.zero_dim, l=spec.nonneg_dim, nq=q.size,
+            m=m, n=n, colptr=native.ptr(cp, native.i64p),
+            rowidx=native.ptr(ri, native.i64p), vals=native.ptr(va), b=native.ptr(bb),
+            c=native.ptr(cc), z=spec.zero_dim, l=spec.nonneg_dim, nq=q.size,
             q=native.ptr(q, native.i64p), ns=s.size, s=native.ptr(s, native.i64p),
-            ep=spec.exp_dim, m_global=self._m_global or 0, row_lo=self._row_lo)
+            ep=spec.exp_dim, m_global=m_global, row_lo=row_lo)
         S = native.SettingsC(
             alpha=st.alpha, max_iters=st.max_iters, eps_pri=st.eps_pri, eps_dual=st.eps_dual,
             eps_gap=st.eps_gap, eps_infeas=st.eps_infeas, eps_unbdd=st.eps_unbdd,
@@ -390,10 +406,17 @@ class Workspace:
             fast=int(bool(st.fast)))
         dist = None
         if self._dist is not None:
-            rank, world, nid = self._dist
-            self._nid = (native.C.c_uint8 * 128).from_buffer_copy(bytes(nid))
-            dist = native.Dist(rank=rank, world=world,
-                               nccl_id=native.C.cast(self._nid, native.C.POINTER(native.C.c_uint8)))
+            sp = self._dist
+            self._bounds = native.i64(sp.bounds)
+            self._nid = None
+            if sp.nccl_id is not None:
+                self._nid = (native.C.c_uint8 * 128).from_buffer_copy(bytes(sp.nccl_id))
+            dist = native.Dist(
+                rank=sp.rank, world=sp.world,
+                nccl_id=native.C.cast(self._nid, native.C.POINTER(native.C.c_uint8))
+                if self._nid is not None else None,
+                emu_group=sp.emu_group, bounds=native.ptr(self._bounds, native.i64p),
+                flags=1 if sp.force else 0)
         h = native.C.c_void_p()
         rc = self._lib.scs_create(native.C.byref(P), native.C.byref(S),
                                   native.C.byref(dist) if dist is not None else None,
@@ -405,6 +428,13 @@ class Workspace:
             except native.NativeError as exc:
                 _raise(exc, setup=True)
         self._h = h
+
+    def allreduce(self, *vals):
+        """Sum scalars over the shards (identity without sharding)."""
+        arr = np.array(vals, dtype=np.float64)
+        if self._dist is not None:
+            self._call(self._lib.scs_allreduce(self._h, native.ptr(arr), arr.size))
+        return arr
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -452,9 +482,14 @@ class Workspace:
         t0 = time.perf_counter()
         nb = None if b is None else native.f64(b)
         nc = None if c is None else native.f64(c)
-        self.data = ProblemData(self.data.A, self.data.b if nb is None else nb,
-                                self.data.c if nc is None else nc, self.data.spec) \
-            if self._m_global is None else self.data
+        if self._dist is None:
+            self.data = ProblemData(self.data.A, self.data.b if nb is None else nb,
+                                    self.data.c if nc is None else nc, self.data.spec)
+        else:
+            if nb is not None:
+                self.data.b = nb
+            if nc is not None:
+                self.data.c = nc
         self._scal = None
         self._call(self._lib.scs_update_vectors(self._h, native.ptr(nb), native.ptr(nc)))
         self.last_setup_time = time.perf_counter() - t0
@@ -522,13 +557,13 @@ class Workspace:
             x = sc.E * (ux / ut) / sc.sigma
             s = (vs / ut) / (sc.D * sc.sigma)
             y = sc.D * (uy / ut) / sc.rho
-            sol.x, sol.y, sol.s = x, y, s
+            sol.x, sol.y, sol.s = x, y, s  # y, s: this shard's rows when sharded
             sol.primal_obj = float(d.c @ x)
-            sol.dual_obj = float(-(d.b @ y))
+            sol.dual_obj = float(-self.allreduce(d.b @ y)[0])
             sol.info.pri_res, sol.info.dual_res, sol.info.gap = self.point_residuals(x, y, s)
         if status in (Status.INFEASIBLE, Status.INFEASIBLE_AND_UNBOUNDED):
             y_dir = sc.D * uy / sc.rho
-            sol.certificate = y_dir / (-(d.b @ y_dir))
+            sol.certificate = y_dir / (-self.allreduce(d.b @ y_dir)[0])
             sol.primal_obj = np.inf
             sol.dual_obj = np.inf
         if status in (Status.UNBOUNDED, Status.INFEASIBLE_AND_UNBOUNDED):

@@ -63,8 +63,12 @@ struct Vec {
   double *q;                  // A p (m)
   double *zy;                 // z_y = rhs_y + A x (m)
   double *part;               // kMaxRed * kMaxGrid partials
+  double *dred;               // deferred (to-be-all-reduced) totals, kMaxRed
+  double xw;                  // weight of replicated x-part terms in
+                              // all-reduced sums: 1 on rank 0, else 0
   double *chunk_part;         // big-SOC chunk partial norms
   double *soc_fac;            // 3 per big SOC: mode, head, scale
+  double *cone_red;           // [c'u~x, b'u~y, err, then (||z||^2, t0) per global big SOC]
   Ctl* ctl;
 };
 
@@ -82,6 +86,8 @@ struct Cones {
   const long long* chunk_off;     // chunk start (absolute y offset)
   const int* chunk_len;
   const int* chunk_cone;
+  const int* bsoc_gid;            // global id of each big SOC (all-reduce slot)
+  int n_big_global;               // big-path SOCs over all shards
   int n_psd;
   const long long* psd_off;
   const int* psd_side;
@@ -197,8 +203,66 @@ __global__ void __launch_bounds__(kBlock) k_spmv(Csr A, Epi epi0) {
   }
   epi.extra(red);
   if constexpr (Epi::NR > 0) {
+    if (grid_sum_last<Epi::NR>(red, epi.V.part, &epi.V.ctl->counter)) {
+      if (epi.defer) {  // row-sharded: totals are all-reduced, then k_finish
+        if (threadIdx.x == 0)
+          for (int t = 0; t < Epi::NR; ++t) epi.V.dred[t] = red[t];
+      } else {
+        epi.finish(red);
+      }
+    }
+  }
+}
+
+// Row-sharded A^T pass, part 1: raw partial products T[j*NV + t] of the
+// local rows of A (= local columns of A^T); all-reduced before part 2.
+template <class Inner>
+struct EpiRaw : Inner {
+  static constexpr int NR = 0;
+  double* T;
+  struct Pre {};
+  __device__ void pre(long long, Pre&) const {}
+  __device__ void row(long long j, const double (&s)[Inner::NV], const Pre&, double*) const {
+#pragma unroll
+    for (int t = 0; t < Inner::NV; ++t) T[j * Inner::NV + t] = s[t];
+  }
+  __device__ void extra(double*) const {}
+  __device__ void finish(const double*) const {}
+};
+
+// Row-sharded A^T pass, part 2: the epilogue over the all-reduced products.
+template <class Epi>
+__global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows, Epi epi0) {
+  Epi epi = epi0;
+  if (!epi.load()) return;
+  constexpr int NR = Epi::NR > 0 ? Epi::NR : 1;
+  double red[NR];
+#pragma unroll
+  for (int t = 0; t < NR; ++t) red[t] = 0.0;
+  const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long nt = (long long)gridDim.x * kBlock;
+  for (long long j = tid; j < rows; j += nt) {
+    typename Epi::Pre pre;
+    epi.pre(j, pre);
+    double s[Epi::NV];
+#pragma unroll
+    for (int t = 0; t < Epi::NV; ++t) s[t] = T[j * Epi::NV + t];
+    epi.row(j, s, pre, red);
+  }
+  epi.extra(red);
+  if constexpr (Epi::NR > 0) {
     if (grid_sum_last<Epi::NR>(red, epi.V.part, &epi.V.ctl->counter)) epi.finish(red);
   }
+}
+
+// Deferred finish after the all-reduce of V.dred (one block).
+template <class Epi>
+__global__ void k_finish(Epi epi0) {
+  Epi epi = epi0;
+  if (!epi.load()) return;
+  double tot[Epi::NR > 0 ? Epi::NR : 1];
+  for (int t = 0; t < Epi::NR; ++t) tot[t] = epi.V.dred[t];
+  epi.finish(tot);
 }
 
 __device__ void finish_residuals(Ctl* c, double ut, double s_pri, double s_unb, double buy,
@@ -209,6 +273,7 @@ struct EpiBase {
   Vec V;
   const double* xb;  // gather base
   int pend;          // residual check of the previous iteration rides along
+  int defer;         // row-sharded: totals go to V.dred for an all-reduce
   struct Pre {};
   __device__ void pre(long long, Pre&) const {}
   __device__ void extra(double*) const {}
@@ -342,7 +407,7 @@ struct EpiAFinal : EpiBase {
   __device__ void extra(double* red) const {
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nt = (long long)gridDim.x * blockDim.x;
-    for (long long j = tid; j < V.n; j += nt) red[0] += V.c[j] * V.x[j];
+    for (long long j = tid; j < V.n; j += nt) red[0] += V.xw * (V.c[j] * V.x[j]);
   }
   __device__ void finish(const double* tot) const {
     if (threadIdx.x) return;

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <functional>
 #include <mutex>
 #include <string>
@@ -31,8 +32,19 @@ namespace scs {
 // iteration kernels (non-SpMV)
 // ===========================================================================
 
-// w = u + v; rhs = w[:-1] - w_tau h; CG tolerance (embedding.py:177-185)
-__global__ void __launch_bounds__(kBlock) k_prep(Vec V) {
+// CG tolerance of this iteration from ||rhs||^2 (embedding.py:179-185)
+__device__ void prep_finish(Ctl* c, double rhs2) {
+  const long long k = ++c->k_sched;
+  c->tol = c->cg_tol > 0.0 ? c->cg_tol
+                           : 1e-3 * (1.0 + sqrt(rhs2)) / pow((double)(k < 1 ? 1 : k), 1.5);
+  c->cg_done = 0;
+  c->cg_it = 0;
+}
+
+// w = u + v; rhs = w[:-1] - w_tau h; ||rhs||^2 (embedding.py:177-185).
+// Row-sharded (defer): the x-part counts on rank 0 only (V.xw) and the
+// total is all-reduced before k_prep_finish.
+__global__ void __launch_bounds__(kBlock) k_prep(Vec V, int defer) {
   Ctl* c = V.ctl;
   if (c->stop) return;
   const long long n = V.n, m = V.m;
@@ -43,21 +55,25 @@ __global__ void __launch_bounds__(kBlock) k_prep(Vec V) {
   for (long long i = tid; i < n + m; i += nt) {
     const double w = V.u[i] + V.v[i];
     double r;
-    if (i < n) { r = w - wt * V.c[i]; V.rhs_x[i] = r; }
-    else {
+    if (i < n) {
+      r = w - wt * V.c[i];
+      V.rhs_x[i] = r;
+      red[0] += V.xw * (r * r);
+    } else {
       r = w - wt * V.b[i - n];
       V.rhs_y[i - n] = r;
       V.Y2[2 * (i - n)] = r + V.Axw[i - n];
+      red[0] += r * r;
     }
-    red[0] += r * r;
   }
   if (grid_sum_last<1>(red, V.part, &c->counter) && threadIdx.x == 0) {
-    const long long k = ++c->k_sched;
-    c->tol = c->cg_tol > 0.0 ? c->cg_tol
-                             : 1e-3 * (1.0 + sqrt(red[0])) / pow((double)(k < 1 ? 1 : k), 1.5);
-    c->cg_done = 0;
-    c->cg_it = 0;
+    if (defer) V.dred[0] = red[0];
+    else prep_finish(c, red[0]);
   }
+}
+__global__ void k_prep_finish(Vec V) {
+  if (V.ctl->stop || threadIdx.x) return;
+  prep_finish(V.ctl, V.dred[0]);
 }
 
 // x += alpha p; r -= alpha Gp; r'r -> stop test / beta (sparse_linalg.py:476-485)
@@ -129,7 +145,42 @@ __device__ __forceinline__ void soc_factor(double nz, double t, double* mode, do
 // or thread can finish alone (x-part free, zero, nonneg, small SOC, exp),
 // plus big-SOC chunk norms; the last block sets the tau entries, the big
 // SOC factors and the iteration counter.
-__global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K) {
+// tau entry (embedding.py:196, cones.py:248), iteration counter, and the
+// big-SOC factors (cones.py:172-184) from the (all-reduced) cone_red totals.
+// Runs in the last block of k_cone_tail, or as k_cone_finish after the
+// all-reduce when rows are sharded.
+__device__ void cone_finish(Vec V, Cones K) {
+  Ctl* c = V.ctl;
+  const double* cr = V.cone_red;
+  const long long n = V.n, m = V.m;
+  const double al = c->alpha;
+  if (threadIdx.x == 0) {
+    if (cr[2] != 0.0) { c->err |= ERR_CONE_NONFINITE; c->stop = 1; }
+    const double ut_ = V.u[n + m], vt_ = V.v[n + m];
+    const double wt = ut_ + vt_;
+    const double utau = (wt + cr[0]) + cr[1];
+    const double ub = al * utau + (1.0 - al) * ut_;
+    const double t = ub - vt_;
+    if (!isfinite(t)) { c->err |= ERR_CONE_NONFINITE; c->stop = 1; }
+    const double up = fmax(t, 0.0);
+    V.u[n + m] = up;
+    V.v[n + m] = (vt_ - ub) + up;
+    c->iter += 1;
+    c->check_pending = (c->iter % c->check_interval == 0);  // solver.py:359
+  }
+  for (int q = threadIdx.x; q < K.n_bsoc; q += blockDim.x) {
+    const int g = K.bsoc_gid[q];
+    soc_factor(sqrt(cr[3 + 2 * g]), cr[4 + 2 * g], V.soc_fac + 3 * q, V.soc_fac + 3 * q + 1,
+               V.soc_fac + 3 * q + 2);
+  }
+}
+
+__global__ void k_cone_finish(Vec V, Cones K) {
+  if (V.ctl->stop) return;
+  cone_finish(V, K);
+}
+
+__global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K, int defer) {
   Ctl* c = V.ctl;
   if (c->stop) return;
   const long long n = V.n, m = V.m;
@@ -141,7 +192,7 @@ __global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K) {
   // x-part: free cone (cones.py:246); v_x becomes exactly 0
   for (long long j = tid; j < n; j += nt) {
     const double ut = V.x[j] - corr * V.gx[j];
-    red[0] += V.c[j] * ut;
+    red[0] += V.xw * (V.c[j] * ut);
     const double ub = al * ut + (1.0 - al) * V.u[j];
     const double t = ub - V.v[j];
     bad |= !isfinite(t);
@@ -225,22 +276,19 @@ __global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K) {
   // would skip the reduction and strand its counter
   if (bad) atomicOr(&c->err, ERR_CONE_NONFINITE);
   if (!grid_sum_last<2>(red, V.part, &c->counter)) return;
-  // ---- last block: tau entry (embedding.py:196, cones.py:248) -------------
+  // ---- last block: local totals into cone_red ------------------------------
+  double* cr = V.cone_red;
   if (threadIdx.x == 0) {
-    if (c->err) c->stop = 1;
-    const double ut_ = V.u[n + m], vt_ = V.v[n + m];
-    const double wt = ut_ + vt_;
-    const double utau = (wt + red[0]) + red[1];
-    const double ub = al * utau + (1.0 - al) * ut_;
-    const double t = ub - vt_;
-    if (!isfinite(t)) { c->err |= ERR_CONE_NONFINITE; c->stop = 1; }
-    const double up = fmax(t, 0.0);
-    V.u[n + m] = up;
-    V.v[n + m] = (vt_ - ub) + up;
-    c->iter += 1;
-    c->check_pending = (c->iter % c->check_interval == 0);  // solver.py:359
+    cr[0] = red[0];
+    cr[1] = red[1];
+    cr[2] = (double)c->err;
   }
-  // big SOC factors: one warp per cone over its chunk partials
+  for (int g = threadIdx.x; g < K.n_big_global; g += kBlock) {
+    cr[3 + 2 * g] = 0.0;
+    cr[4 + 2 * g] = 0.0;
+  }
+  __syncthreads();
+  // big SOC partial norms: one warp per local cone over its chunk partials
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int q = warp; q < K.n_bsoc; q += kWarps) {
     double zz = 0.0;
@@ -248,10 +296,13 @@ __global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K) {
       zz += __ldcg(V.chunk_part + ch);
     zz = warp_sum(zz);
     if (lane == 0) {
-      const Relax r = relax_y(V, K.bsoc_off[q], corr, al);
-      soc_factor(sqrt(zz), r.t, V.soc_fac + 3 * q, V.soc_fac + 3 * q + 1, V.soc_fac + 3 * q + 2);
+      const int g = K.bsoc_gid[q];
+      cr[3 + 2 * g] = zz;
+      if (K.bsoc_off[q] >= 0) cr[4 + 2 * g] = relax_y(V, K.bsoc_off[q], corr, al).t;  // head is local
     }
   }
+  __syncthreads();
+  if (!defer) cone_finish(V, K);
 }
 
 // Big SOC apply (block per chunk) and PSD blocks (block per PSD, Jacobi in
@@ -413,12 +464,27 @@ __global__ void k_row_norms(Csr A, double* out) {
     if (lane == 0) out[r] = sqrt(s);
   }
 }
-// scale = where(nrm > 0, 1/sqrt(nrm), 1); acc *= scale (scaling.py:405-407)
-__global__ void k_inv_sqrt_scale(const double* nrm, long long n, double* scale, double* acc) {
+// per-row sum of squares (column norms of A come from CSR(A^T) rows; when
+// rows are sharded these partial sums are all-reduced before the sqrt)
+__global__ void k_row_sumsq(Csr A, double* out) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long r = w; r < A.rows; r += nw) {
+    double s = 0.0;
+    for (long long k = A.rp[r] + lane; k < A.rp[r + 1]; k += 32) s += A.v[k] * A.v[k];
+    s = warp_sum(s);
+    if (lane == 0) out[r] = s;
+  }
+}
+// nrm = sqrt(sumsq); scale = where(nrm > 0, 1/sqrt(nrm), 1); acc *= scale
+// (scaling.py:398, 405-407)
+__global__ void k_inv_sqrt_scale(double* sumsq, long long n, double* scale, double* acc) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long i = tid; i < n; i += nt) {
-    const double v = nrm[i];
+    const double v = sqrt(sumsq[i]);
+    sumsq[i] = v;
     const double s = v > 0.0 ? 1.0 / sqrt(v) : 1.0;
     scale[i] = s;
     acc[i] *= s;
@@ -440,35 +506,43 @@ __global__ void k_scale_cols(const int* ci, double* v, long long nnz, const doub
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long k = tid; k < nnz; k += nt) v[k] *= s[ci[k]];
 }
-// Row-block means (scaling.py:375-377, 409-413): singleton rows [0, zl)
-// keep their own norm; each cone block (segment) shares the mean of its
-// rows.  apply=1 also writes the row scale and multiplies D.
-__global__ void k_block_rows(const double* rn, long long zl, int nseg, const long long* seg_off,
-                             const long long* seg_len, double* seg_mean, double* rscale,
-                             double* D, int apply) {
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nt = (long long)gridDim.x * blockDim.x;
-  if (apply) {
-    for (long long i = tid; i < zl; i += nt) {
-      const double t = rn[i];
-      const double s = t > 0.0 ? 1.0 / sqrt(t) : 1.0;
-      rscale[i] = s;
-      D[i] *= s;
-    }
-  }
+// Row-block means (scaling.py:375-377, 409-413).  Every non-singleton
+// cone block is a segment with a global id; each shard sums the row norms
+// of its part into seg_sum[gid] (all-reduced when sharded), the mean is
+// seg_sum / global length.  Singleton (zero/nonneg) rows keep their norm.
+__global__ void k_seg_partial(const double* rn, int nseg, const long long* seg_off,
+                              const long long* seg_len, const int* seg_gid, double* seg_sum) {
   for (int q = blockIdx.x; q < nseg; q += gridDim.x) {
     const long long o = seg_off[q], d = seg_len[q];
     double s[1] = {0.0};
     for (long long e = threadIdx.x; e < d; e += blockDim.x) s[0] += rn[o + e];
     block_sum<1>(s);
-    const double mean = s[0] / (double)d;
-    if (threadIdx.x == 0) seg_mean[q] = mean;
-    if (apply) {
-      const double f = mean > 0.0 ? 1.0 / sqrt(mean) : 1.0;
-      for (long long e = threadIdx.x; e < d; e += blockDim.x) {
-        rscale[o + e] = f;
-        D[o + e] *= f;
-      }
+    if (threadIdx.x == 0) seg_sum[seg_gid[q]] = s[0];
+  }
+}
+__global__ void k_seg_means(const double* seg_sum, const long long* glen, int nseg_g,
+                            double* mean) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int g = tid; g < nseg_g; g += gridDim.x * blockDim.x) mean[g] = seg_sum[g] / (double)glen[g];
+}
+__global__ void k_block_rows(const double* rn, long long zl, int nseg, const long long* seg_off,
+                             const long long* seg_len, const int* seg_gid, const double* mean,
+                             double* rscale, double* D) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < zl; i += nt) {
+    const double t = rn[i];
+    const double s = t > 0.0 ? 1.0 / sqrt(t) : 1.0;
+    rscale[i] = s;
+    D[i] *= s;
+  }
+  for (int q = blockIdx.x; q < nseg; q += gridDim.x) {
+    const long long o = seg_off[q], d = seg_len[q];
+    const double mm = mean[seg_gid[q]];
+    const double f = mm > 0.0 ? 1.0 / sqrt(mm) : 1.0;
+    for (long long e = threadIdx.x; e < d; e += blockDim.x) {
+      rscale[o + e] = f;
+      D[o + e] *= f;
     }
   }
 }
@@ -562,6 +636,16 @@ __global__ void k_recip(const double* a, long long n, double* out) {
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long i = tid; i < n; i += nt) out[i] = 1.0 / a[i];
 }
+__global__ void k_sqrt(double* x, long long n) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) x[i] = sqrt(x[i]);
+}
+__global__ void k_add(double* a, const double* b, long long n) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) a[i] += b[i];
+}
 __global__ void k_zero(double* x, long long n) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
@@ -592,6 +676,104 @@ struct DevBuf {
   size_t bytes = 0;
 };
 
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw Fail{SCS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};        \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// communicators for row sharding: NCCL (one process per GPU) or an
+// in-process emulated group (several shards on one GPU, one host thread per
+// shard) used to test the sharded kernels without a second GPU.  The
+// emulated all-reduce synchronises on the host between kernels -- no kernel
+// ever waits on another shard's kernel.
+// ---------------------------------------------------------------------------
+struct ScsComm {
+  virtual ~ScsComm() {}
+  virtual void allreduce(cudaStream_t st, double* d, size_t n) = 0;
+  virtual bool capturable() const = 0;
+};
+
+}  // namespace
+
+struct scs_emu_group {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  bool broken = false;
+  std::vector<double*> ptr;
+  std::vector<size_t> cnt;
+};
+
+namespace {
+
+void emu_barrier(scs_emu_group* g) {
+  std::unique_lock<std::mutex> lk(g->mu);
+  if (g->broken) throw Fail{SCS_ENCCL, "emulated group broken by another shard"};
+  const long long my = g->gen;
+  if (++g->arrived == g->world) {
+    g->arrived = 0;
+    g->gen++;
+    g->cv.notify_all();
+    return;
+  }
+  if (!g->cv.wait_for(lk, std::chrono::seconds(120), [&] { return g->gen != my || g->broken; })) {
+    g->broken = true;
+    g->cv.notify_all();
+    throw Fail{SCS_ENCCL, "emulated all-reduce timed out"};
+  }
+  if (g->broken) throw Fail{SCS_ENCCL, "emulated group broken by another shard"};
+}
+
+struct EmuComm : ScsComm {
+  scs_emu_group* g;
+  int rank;
+  EmuComm(scs_emu_group* g_, int r) : g(g_), rank(r) {}
+  void allreduce(cudaStream_t st, double* d, size_t n) override {
+    CK(cudaStreamSynchronize(st));
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      g->ptr[rank] = d;
+      g->cnt[rank] = n;
+    }
+    emu_barrier(g);
+    if (rank == 0) {
+      for (int r = 1; r < g->world; ++r)
+        if (g->cnt[r] != n) throw Fail{SCS_ENCCL, "emulated all-reduce: count mismatch"};
+      const int grid = (int)std::min<size_t>(1184, (n + 255) / 256 + 1);
+      for (int r = 1; r < g->world; ++r) k_add<<<grid, 256, 0, st>>>(d, g->ptr[r], (long long)n);
+      for (int r = 1; r < g->world; ++r)
+        CK(cudaMemcpyAsync(g->ptr[r], d, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    emu_barrier(g);
+  }
+  bool capturable() const override { return false; }
+};
+
+#ifdef SCS_WITH_NCCL
+struct NcclComm : ScsComm {
+  ncclComm_t c = nullptr;
+  ~NcclComm() override {
+    if (c) ncclCommDestroy(c);
+  }
+  void allreduce(cudaStream_t st, double* d, size_t n) override {
+    ncclResult_t r = ncclAllReduce(d, d, n, ncclDouble, ncclSum, c, st);
+    if (r != ncclSuccess) throw Fail{SCS_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r)};
+  }
+  bool capturable() const override { return true; }
+};
+#endif
+
 }  // namespace
 
 struct scs_handle {
@@ -603,25 +785,33 @@ struct scs_handle {
   // sizes
   long long m = 0, n = 0, nnz = 0, m_glob = 0, row_lo = 0;
   int rank = 0, world = 1;
+  bool sharded = false;   // reductions over rows are all-reduced
+  bool use_graph = true;  // iteration captured as a CUDA graph
+  ScsComm* comm = nullptr;
+  std::vector<long long> bounds;
   scs_settings set{};
   // matrices
   Csr A{}, At{};
   int LA = 32, LAt = 32;
   // cones
   Cones K{};
-  std::vector<long long> seg_off_h, seg_len_h;
+  int nseg = 0, nseg_g = 0;
   long long* seg_off = nullptr;
   long long* seg_len = nullptr;
-  int nseg = 0;
+  int* seg_gid = nullptr;
+  long long* seg_glen = nullptr;
+  double* seg_sum = nullptr;
+  double* seg_mean = nullptr;
   double* psd_scratch = nullptr;
   int smem_side = 0;
   size_t cone_smem = 0;
+  int cone_red_len = 3;
   // vectors
   Vec V{};
   double *b0 = nullptr, *c0 = nullptr;  // original b, c (device)
   double *bh = nullptr, *ch = nullptr, *D = nullptr, *E = nullptr;
   double *tmp_n = nullptr, *tmp_m = nullptr, *tmp_m2 = nullptr, *zero_m = nullptr;
-  double *seg_mean = nullptr;
+  double* Traw = nullptr;   // raw A^T partial products (sharded)
   double* dscal = nullptr;  // device scratch scalars
   Ctl* ctl = nullptr;
   Ctl* ctl_h = nullptr;     // pinned mirror
@@ -655,18 +845,6 @@ void set_global_err(const std::string& s) {
   std::lock_guard<std::mutex> g(g_err_mu);
   g_err = s;
 }
-
-struct Fail {
-  int code;
-  std::string msg;
-};
-
-#define CK(call)                                                                        \
-  do {                                                                                  \
-    cudaError_t e_ = (call);                                                            \
-    if (e_ != cudaSuccess)                                                              \
-      throw Fail{SCS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};        \
-  } while (0)
 
 template <class T>
 T* dalloc(scs_handle* h, size_t count) {
@@ -706,6 +884,10 @@ int pick_lanes(long long nnz, long long rows) {
   return 32;
 }
 
+void allreduce(scs_handle* h, double* d, size_t n) {
+  if (h->sharded && n) h->comm->allreduce(h->st, d, n);
+}
+
 template <class Epi>
 void launch_spmv(scs_handle* h, const Csr& M, int L, const Epi& epi) {
   const long long work = M.rows * (long long)L;
@@ -720,80 +902,156 @@ void launch_spmv(scs_handle* h, const Csr& M, int L, const Epi& epi) {
   h->launches++;
 }
 
+// A pass over the local rows.  Row-sharded: its (y-part) totals are
+// all-reduced and finished by k_finish.
+template <class Epi>
+void a_pass(scs_handle* h, Epi epi) {
+  epi.defer = (h->sharded && Epi::NR > 0) ? 1 : 0;
+  launch_spmv(h, h->A, h->LA, epi);
+  if (epi.defer) {
+    allreduce(h, h->V.dred, Epi::NR);
+    k_finish<Epi><<<1, 32, 0, h->st>>>(epi);
+    h->launches++;
+  }
+}
+
+// A^T pass.  Row-sharded: raw partial products of the local rows, one
+// all-reduce of NV n-vectors, then the epilogue on the reduced products
+// (its reductions are over replicated x-space data: no further all-reduce).
+template <class Epi>
+void at_pass(scs_handle* h, Epi epi) {
+  epi.defer = 0;
+  if (!h->sharded) {
+    launch_spmv(h, h->At, h->LAt, epi);
+    return;
+  }
+  EpiRaw<Epi> raw{};
+  static_cast<Epi&>(raw) = epi;
+  raw.T = h->Traw;
+  launch_spmv(h, h->At, h->LAt, raw);
+  allreduce(h, h->Traw, (size_t)h->n * Epi::NV);
+  k_rows<Epi><<<elem_grid(h, h->n), kBlock, 0, h->st>>>(h->Traw, h->n, epi);
+  h->launches++;
+}
+
 // ---------------------------------------------------------------------------
-// cone layout
+// cone layout of this shard: rows [row_lo, row_lo + m) of the global cone
 // ---------------------------------------------------------------------------
 void build_cones(scs_handle* h, const scs_problem* P) {
-  // block list in the reference order (cones.py:121-139), local row offsets
   const long long lo = h->row_lo, hi = h->row_lo + h->m;
+  const std::vector<long long>& B = h->bounds;
+  auto cut = [&](long long a, long long b) {  // block [a, b) split by a shard bound
+    for (size_t k = 1; k + 1 < B.size(); ++k)
+      if (B[k] > a && B[k] < b) return true;
+    return false;
+  };
   std::vector<long long> ssoc_off;
   std::vector<int> ssoc_len;
   std::vector<long long> bsoc_off, bsoc_len;
-  std::vector<int> bsoc_chunk_lo;
+  std::vector<int> bsoc_chunk_lo, bsoc_gid;
   std::vector<long long> chunk_off;
   std::vector<int> chunk_len, chunk_cone;
   std::vector<long long> psd_off;
   std::vector<int> psd_side;
-  if (h->world > 1) throw Fail{SCS_EINVAL, "row sharding is not enabled in this build"};
-  (void)hi;
-  const long long zg = P->z, lg = P->l;
-  h->K.z = zg;
-  h->K.l = lg;
-  long long off = zg + lg;
+  std::vector<long long> seg_off, seg_len, seg_glen;
+  std::vector<int> seg_gid;
+  // zero and nonneg rows: the shard's share of [0, z) and [z, z + l)
+  const long long z = P->z, l = P->l;
+  h->K.z = std::max(0LL, std::min(z, hi) - lo);
+  h->K.l = std::max(0LL, std::min(z + l, hi) - std::max(z, lo));
+  if (h->K.z < 0 || h->K.l < 0) throw Fail{SCS_EINVAL, "internal: bad zero/nonneg share"};
+  long long off = z + l;
+  int ng = 0, sg = 0;
   for (long long i = 0; i < P->nq; ++i) {  // cones.py:134-136
     const long long d = P->q[i];
     if (d < 1) throw Fail{SCS_EINVAL, "second-order cone dims must be >= 1"};
-    if (d <= kSmallSoc) {
-      ssoc_off.push_back(off - lo);
-      ssoc_len.push_back((int)d);
-    } else {
-      bsoc_off.push_back(off - lo);
-      bsoc_len.push_back(d);
-      bsoc_chunk_lo.push_back((int)chunk_off.size());
-      for (long long e = 0; e < d; e += kChunk) {
-        chunk_off.push_back(off + e - lo);
-        chunk_len.push_back((int)std::min<long long>(kChunk, d - e));
-        chunk_cone.push_back((int)bsoc_off.size() - 1);
+    const bool big = d > kSmallSoc || cut(off, off + d);
+    const long long a = std::max(off, lo), b = std::min(off + d, hi);
+    if (b > a) {
+      seg_off.push_back(a - lo);
+      seg_len.push_back(b - a);
+      seg_gid.push_back(sg);
+      if (!big) {
+        ssoc_off.push_back(off - lo);
+        ssoc_len.push_back((int)d);
+      } else {
+        bsoc_off.push_back(off - lo);  // negative when the head lives on another shard
+        bsoc_len.push_back(d);
+        bsoc_gid.push_back(ng);
+        bsoc_chunk_lo.push_back((int)chunk_off.size());
+        for (long long e = a; e < b; e += kChunk) {
+          chunk_off.push_back(e - lo);
+          chunk_len.push_back((int)std::min<long long>(kChunk, b - e));
+          chunk_cone.push_back((int)bsoc_off.size() - 1);
+        }
       }
     }
+    seg_glen.push_back(d);
+    ++sg;
+    if (big) ++ng;
     off += d;
   }
   bsoc_chunk_lo.push_back((int)chunk_off.size());
-  const long long psd_lo = off;
+  h->K.n_big_global = ng;
+  long long psd_lo = -1, psd_hi = -1;
   int max_side = 0;
   for (long long i = 0; i < P->ns; ++i) {  // cones.py:137-139
     const long long k = P->s[i];
     if (k < 1) throw Fail{SCS_EINVAL, "PSD side lengths must be >= 1"};
-    psd_off.push_back(off - lo);
-    psd_side.push_back((int)k);
-    max_side = std::max<int>(max_side, (int)k);
-    off += k * (k + 1) / 2;
+    const long long d = k * (k + 1) / 2;
+    if (cut(off, off + d)) throw Fail{SCS_EINVAL, "a shard bound cuts a PSD block"};
+    if (off >= lo && off + d <= hi) {
+      psd_off.push_back(off - lo);
+      psd_side.push_back((int)k);
+      max_side = std::max<int>(max_side, (int)k);
+      if (psd_lo < 0) psd_lo = off - lo;
+      psd_hi = off + d - lo;
+      seg_off.push_back(off - lo);
+      seg_len.push_back(d);
+      seg_gid.push_back(sg);
+    }
+    seg_glen.push_back(d);
+    ++sg;
+    off += d;
   }
-  const long long psd_hi = off;
-  h->K.psd_lo = psd_lo - lo;
-  h->K.psd_hi = psd_hi - lo;
-  h->K.exp_lo = off - lo;
-  h->K.n_exp = P->ep;
-  off += 3 * P->ep;
+  h->K.psd_lo = psd_lo < 0 ? 0 : psd_lo;
+  h->K.psd_hi = psd_hi < 0 ? 0 : psd_hi;
+  long long n_exp = 0, exp_lo = -1;
+  for (long long i = 0; i < P->ep; ++i) {
+    if (cut(off, off + 3)) throw Fail{SCS_EINVAL, "a shard bound cuts an exponential cone"};
+    if (off >= lo && off + 3 <= hi) {
+      if (exp_lo < 0) exp_lo = off - lo;
+      ++n_exp;
+      seg_off.push_back(off - lo);
+      seg_len.push_back(3);
+      seg_gid.push_back(sg);
+    }
+    seg_glen.push_back(3);
+    ++sg;
+    off += 3;
+  }
+  h->K.exp_lo = exp_lo < 0 ? 0 : exp_lo;
+  h->K.n_exp = n_exp;
   if (off != h->m_glob)
-    throw Fail{SCS_EINVAL, "cone dimension " + std::to_string(off) +
-                               " does not match row count " + std::to_string(h->m_glob)};
+    throw Fail{SCS_EINVAL, "cone dimension " + std::to_string(off) + " does not match row count " +
+                               std::to_string(h->m_glob)};
   auto up_ll = [&](const std::vector<long long>& v) {
     long long* d = dalloc<long long>(h, v.size());
     h2d(h, d, v.data(), v.size());
-    return (const long long*)d;
+    return d;
   };
   auto up_i = [&](const std::vector<int>& v) {
     int* d = dalloc<int>(h, v.size());
     h2d(h, d, v.data(), v.size());
-    return (const int*)d;
+    return d;
   };
   h->K.n_ssoc = (int)ssoc_off.size();
-  h->K.ssoc_len = up_i(ssoc_len);
   h->K.ssoc_off = up_ll(ssoc_off);
+  h->K.ssoc_len = up_i(ssoc_len);
   h->K.n_bsoc = (int)bsoc_off.size();
   h->K.bsoc_off = up_ll(bsoc_off);
   h->K.bsoc_len = up_ll(bsoc_len);
+  h->K.bsoc_gid = up_i(bsoc_gid);
   h->K.bsoc_chunk_lo = up_i(bsoc_chunk_lo);
   h->K.n_chunk = (int)chunk_off.size();
   h->K.chunk_off = up_ll(chunk_off);
@@ -803,19 +1061,16 @@ void build_cones(scs_handle* h, const scs_problem* P) {
   h->K.psd_off = up_ll(psd_off);
   h->K.psd_side = up_i(psd_side);
   h->K.max_side = max_side;
+  h->cone_red_len = 3 + 2 * ng;
   // equilibration segments: every non-singleton block (scaling.py:62-71)
-  {
-    long long o = zg + lg;
-    for (long long i = 0; i < P->nq; ++i) { h->seg_off_h.push_back(o - lo); h->seg_len_h.push_back(P->q[i]); o += P->q[i]; }
-    for (long long i = 0; i < P->ns; ++i) {
-      const long long d = P->s[i] * (P->s[i] + 1) / 2;
-      h->seg_off_h.push_back(o - lo); h->seg_len_h.push_back(d); o += d;
-    }
-    for (long long i = 0; i < P->ep; ++i) { h->seg_off_h.push_back(o - lo); h->seg_len_h.push_back(3); o += 3; }
-  }
-  h->nseg = (int)h->seg_off_h.size();
-  h->seg_off = (long long*)up_ll(h->seg_off_h);
-  h->seg_len = (long long*)up_ll(h->seg_len_h);
+  h->nseg = (int)seg_off.size();
+  h->nseg_g = sg;
+  h->seg_off = up_ll(seg_off);
+  h->seg_len = up_ll(seg_len);
+  h->seg_gid = up_i(seg_gid);
+  h->seg_glen = up_ll(seg_glen);
+  h->seg_sum = dalloc<double>(h, std::max(sg, 1));
+  h->seg_mean = dalloc<double>(h, std::max(sg, 1));
   // PSD workspace: shared memory up to ~200 KB, else global scratch
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
@@ -900,9 +1155,13 @@ double dev_scalar(scs_handle* h, int idx = 0) {
   return v;
 }
 
-double norm2_dev(scs_handle* h, const double* a, const double* b, long long n, int mode) {
+// sum over a vector (mode 0: (a b)^2, 1: (a/b)^2, 2: a b); `ysum` = the
+// vector is row-sharded, so the shard totals are all-reduced
+double norm2_dev(scs_handle* h, const double* a, const double* b, long long n, int mode,
+                 bool ysum = false) {
   k_norm2<<<elem_grid(h, n), kBlock, 0, h->st>>>(a, b, n, mode, h->V.part, &h->ctl->counter,
                                                    h->dscal);
+  if (ysum) allreduce(h, h->dscal, 1);
   return dev_scalar(h);
 }
 
@@ -915,7 +1174,6 @@ void equilibrate(scs_handle* h) {
   double* rn = h->tmp_m;
   double* cs = h->V.Gp;  // scratch n
   double* rs = h->tmp_m2;
-  // D = 1, E = 1
   {
     std::vector<double> ones(std::max(m, n), 1.0);
     h2d(h, h->D, ones.data(), m);
@@ -923,68 +1181,55 @@ void equilibrate(scs_handle* h) {
     CK(cudaStreamSynchronize(h->st));
   }
   const long long zl = h->K.z + h->K.l;
-  auto row_norms = [&](const Csr& M, double* out) {
-    k_row_norms<<<elem_grid(h, M.rows * 32), kBlock, 0, h->st>>>(M, out);
+  auto col_norms = [&]() {  // sqrt of all-reduced column sums of squares
+    k_row_sumsq<<<elem_grid(h, n * 32), kBlock, 0, h->st>>>(h->At, cn);
+    allreduce(h, cn, n);
+  };
+  auto row_norms = [&]() {
+    k_row_sumsq<<<elem_grid(h, m * 32), kBlock, 0, h->st>>>(h->A, rn);
+    k_sqrt<<<elem_grid(h, m), kBlock, 0, h->st>>>(rn, m);
+  };
+  auto seg_means = [&]() {
+    CK(cudaMemsetAsync(h->seg_sum, 0, std::max(h->nseg_g, 1) * sizeof(double), h->st));
+    k_seg_partial<<<std::max(1, std::min(h->nseg, h->grid_full)), kBlock, 0, h->st>>>(
+        rn, h->nseg, h->seg_off, h->seg_len, h->seg_gid, h->seg_sum);
+    allreduce(h, h->seg_sum, h->nseg_g);
+    k_seg_means<<<elem_grid(h, h->nseg_g), kBlock, 0, h->st>>>(h->seg_sum, h->seg_glen, h->nseg_g,
+                                                                 h->seg_mean);
   };
   if (h->set.normalize) {
     for (int sw = 0; sw < h->set.sweeps; ++sw) {
-      row_norms(h->At, cn);  // column norms of A
+      col_norms();
       k_inv_sqrt_scale<<<elem_grid(h, n), kBlock, 0, h->st>>>(cn, n, cs, h->E);
       k_scale_rows<<<elem_grid(h, n * 32), kBlock, 0, h->st>>>((long long*)h->At.rp,
                                                                 (double*)h->At.v, n, cs);
       k_scale_cols<<<elem_grid(h, nnz), kBlock, 0, h->st>>>(h->A.ci, (double*)h->A.v, nnz, cs);
-      row_norms(h->A, rn);
+      row_norms();
+      seg_means();
       k_block_rows<<<elem_grid(h, std::max<long long>(zl, (long long)h->nseg * kBlock)), kBlock, 0,
-                     h->st>>>(rn, zl, h->nseg, h->seg_off, h->seg_len, h->seg_mean, rs, h->D, 1);
+                     h->st>>>(rn, zl, h->nseg, h->seg_off, h->seg_len, h->seg_gid, h->seg_mean,
+                              rs, h->D);
       k_scale_rows<<<elem_grid(h, m * 32), kBlock, 0, h->st>>>((long long*)h->A.rp,
                                                                 (double*)h->A.v, m, rs);
       k_scale_cols<<<elem_grid(h, nnz), kBlock, 0, h->st>>>(h->At.ci, (double*)h->At.v, nnz, rs);
     }
-    row_norms(h->At, cn);
+    col_norms();
+    k_sqrt<<<elem_grid(h, n), kBlock, 0, h->st>>>(cn, n);  // replicated on every shard
     k_pos_mean<<<elem_grid(h, n), kBlock, 0, h->st>>>(cn, n, h->V.part, &h->ctl->counter, h->dscal);
     double s0 = dev_scalar(h, 0), c0 = dev_scalar(h, 1);
     h->mean_col = c0 > 0 ? s0 / c0 : 1.0;
-    row_norms(h->A, rn);
-    k_block_rows<<<elem_grid(h, std::max<long long>(zl, (long long)h->nseg * kBlock)), kBlock, 0,
-                   h->st>>>(rn, zl, h->nseg, h->seg_off, h->seg_len, h->seg_mean, rs, h->D, 0);
+    row_norms();
+    seg_means();
     k_pos_mean<<<elem_grid(h, zl), kBlock, 0, h->st>>>(rn, zl, h->V.part, &h->ctl->counter, h->dscal);
+    allreduce(h, h->dscal, 2);
     double s1 = dev_scalar(h, 0), c1 = dev_scalar(h, 1);
-    k_pos_mean<<<elem_grid(h, h->nseg), kBlock, 0, h->st>>>(h->seg_mean, h->nseg, h->V.part,
-                                                             &h->ctl->counter, h->dscal);
+    k_pos_mean<<<elem_grid(h, h->nseg_g), kBlock, 0, h->st>>>(h->seg_mean, h->nseg_g, h->V.part,
+                                                               &h->ctl->counter, h->dscal);
     double s2 = dev_scalar(h, 0), c2 = dev_scalar(h, 1);
     h->mean_row = (c1 + c2) > 0 ? (s1 + s2) / (c1 + c2) : 1.0;
   } else {
     h->mean_col = h->mean_row = 1.0;
   }
-  CK(cudaStreamSynchronize(h->st));
-}
-
-// sigma, rho, b_hat, c_hat and the residual constants (scaling.py:422-429,
-// 469-478)
-void scale_vectors(scs_handle* h) {
-  const long long m = h->m, n = h->n;
-  if (h->set.normalize) {
-    const double dbn = sqrt(norm2_dev(h, h->D, h->b0, m, 0));
-    const double ecn = sqrt(norm2_dev(h, h->E, h->c0, n, 0));
-    h->sigma = dbn > 0 ? h->mean_col / dbn : 1.0;
-    h->rho = ecn > 0 ? h->mean_row / ecn : 1.0;
-  } else {
-    h->sigma = h->rho = 1.0;
-  }
-  k_scale_vec<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->b0, h->D, h->sigma, m, h->bh);
-  k_scale_vec<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->c0, h->E, h->rho, n, h->ch);
-  const double dib = sqrt(norm2_dev(h, h->bh, h->D, m, 1));
-  const double eic = sqrt(norm2_dev(h, h->ch, h->E, n, 1));
-  Ctl* c = h->ctl_h;
-  CK(cudaMemcpyAsync(c, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->st));
-  CK(cudaStreamSynchronize(h->st));
-  c->b_norm = dib / h->sigma;
-  c->c_norm = eic / h->rho;
-  c->b_ref = dib > 0 ? dib : 1.0;
-  c->c_ref = eic > 0 ? eic : 1.0;
-  c->sigma = h->sigma;
-  c->rho = h->rho;
-  CK(cudaMemcpyAsync(h->ctl, c, sizeof(Ctl), cudaMemcpyHostToDevice, h->st));
   CK(cudaStreamSynchronize(h->st));
 }
 
@@ -995,6 +1240,33 @@ void pull_ctl(scs_handle* h) {
 void push_ctl(scs_handle* h) {
   CK(cudaMemcpyAsync(h->ctl, h->ctl_h, sizeof(Ctl), cudaMemcpyHostToDevice, h->st));
   CK(cudaStreamSynchronize(h->st));
+}
+
+// sigma, rho, b_hat, c_hat and the residual constants (scaling.py:422-429,
+// 469-478)
+void scale_vectors(scs_handle* h) {
+  const long long m = h->m, n = h->n;
+  if (h->set.normalize) {
+    const double dbn = sqrt(norm2_dev(h, h->D, h->b0, m, 0, true));
+    const double ecn = sqrt(norm2_dev(h, h->E, h->c0, n, 0));
+    h->sigma = dbn > 0 ? h->mean_col / dbn : 1.0;
+    h->rho = ecn > 0 ? h->mean_row / ecn : 1.0;
+  } else {
+    h->sigma = h->rho = 1.0;
+  }
+  k_scale_vec<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->b0, h->D, h->sigma, m, h->bh);
+  k_scale_vec<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->c0, h->E, h->rho, n, h->ch);
+  const double dib = sqrt(norm2_dev(h, h->bh, h->D, m, 1, true));
+  const double eic = sqrt(norm2_dev(h, h->ch, h->E, n, 1));
+  pull_ctl(h);
+  Ctl* c = h->ctl_h;
+  c->b_norm = dib / h->sigma;
+  c->c_norm = eic / h->rho;
+  c->b_ref = dib > 0 ? dib : 1.0;
+  c->c_ref = eic > 0 ? eic : 1.0;
+  c->sigma = h->sigma;
+  c->rho = h->rho;
+  push_ctl(h);
 }
 
 void check_err(scs_handle* h) {
@@ -1015,17 +1287,17 @@ void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p, bool merge
     EpiAp<true> ea{};
     ea.V = V;
     ea.xb = V.X2;
-    launch_spmv(h, h->A, h->LA, ea);
+    a_pass(h, ea);
   } else {
     EpiAp<false> ea{};
     ea.V = V;
     ea.xb = V.X2;
-    launch_spmv(h, h->A, h->LA, ea);
+    a_pass(h, ea);
   }
   EpiAtGp eg{};
   eg.V = V;
   eg.xb = V.q;
-  launch_spmv(h, h->At, h->LAt, eg);
+  at_pass(h, eg);
   k_cg_update<<<elem_grid(h, h->n), kBlock, 0, h->st>>>(V, cap);
   h->launches++;
   if (with_p) {
@@ -1040,10 +1312,10 @@ void solve_g(scs_handle* h) {
   Vec G = h->V;
   G.rhs_x = h->ch;
   G.x = h->V.gx;
-  k_zero<<<elem_grid(h, n), kBlock, 0, h->st>>>(G.x, n);
   G.rhs_y = h->bh;
+  k_zero<<<elem_grid(h, n), kBlock, 0, h->st>>>(G.x, n);
   k_fill_y2<<<elem_grid(h, m), kBlock, 0, h->st>>>(G.Y2, h->bh, m);
-  const double hn = sqrt(norm2_dev(h, h->ch, h->ch, n, 2) + norm2_dev(h, h->bh, h->bh, m, 2));
+  const double hn = sqrt(norm2_dev(h, h->ch, h->ch, n, 2) + norm2_dev(h, h->bh, h->bh, m, 2, true));
   pull_ctl(h);
   Ctl* c = h->ctl_h;
   c->stop = 0;
@@ -1059,7 +1331,7 @@ void solve_g(scs_handle* h) {
   EpiAtFirst e0{};
   e0.V = G;
   e0.xb = G.Y2;
-  launch_spmv(h, h->At, h->LAt, e0);
+  at_pass(h, e0);
   long long done_steps = 0;
   while (true) {
     pull_ctl(h);
@@ -1076,25 +1348,28 @@ void solve_g(scs_handle* h) {
   ef.xb = G.x;
   ef.zy_out = h->V.gy;
   ef.setup = 1;
-  launch_spmv(h, h->A, h->LA, ef);
+  a_pass(h, ef);
   pull_ctl(h);
   check_err(h);
   if (c->denom < 1.0 - 1e-9)
     throw Fail{SCS_ESETUP, "Schur denominator " + std::to_string(c->denom) + " below 1"};
 }
 
-// capture one ADMM iteration into a CUDA graph
-void build_graph(scs_handle* h) {
-  if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+// one ADMM iteration: the kernel sequence of kernels.cuh (with all-reduces
+// between kernels when rows are sharded)
+void enqueue_iteration(scs_handle* h) {
   const Vec V = h->V;
-  const long long before = h->launches;
-  CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
-  k_prep<<<elem_grid(h, h->n + h->m), kBlock, 0, h->st>>>(V);
+  k_prep<<<elem_grid(h, h->n + h->m), kBlock, 0, h->st>>>(V, h->sharded ? 1 : 0);
   h->launches++;
+  if (h->sharded) {
+    allreduce(h, V.dred, 1);
+    k_prep_finish<<<1, 32, 0, h->st>>>(V);
+    h->launches++;
+  }
   EpiAtFirst e0{};
   e0.V = V;
   e0.xb = V.Y2;
-  launch_spmv(h, h->At, h->LAt, e0);
+  at_pass(h, e0);
   const long long cgm = h->set.cg_max;
   for (long long i = 0; i < cgm; ++i) cg_step(h, V, cgm, i + 1 < cgm, i == 0);
   EpiAFinal ef{};
@@ -1102,17 +1377,36 @@ void build_graph(scs_handle* h) {
   ef.xb = V.x;
   ef.zy_out = V.zy;
   ef.setup = 0;
-  launch_spmv(h, h->A, h->LA, ef);
+  a_pass(h, ef);
   const long long work = std::max<long long>(h->n + h->K.z + h->K.l, 1);
   int g_tail = std::max(elem_grid(h, work), std::min(h->K.n_chunk, h->grid_full));
   g_tail = std::max(g_tail, std::min((int)((h->K.n_ssoc * 32LL + kBlock - 1) / kBlock), h->grid_full));
-  k_cone_tail<<<g_tail, kBlock, 0, h->st>>>(V, h->K);
+  k_cone_tail<<<g_tail, kBlock, 0, h->st>>>(V, h->K, h->sharded ? 1 : 0);
   h->launches++;
+  if (h->sharded) {
+    allreduce(h, V.cone_red, h->cone_red_len);
+    k_cone_finish<<<1, kBlock, 0, h->st>>>(V, h->K);
+    h->launches++;
+  }
   if (h->K.n_chunk > 0 || h->K.n_psd > 0) {
     const int g = std::max(1, std::min(std::max(h->K.n_chunk, h->K.n_psd), h->grid_full));
     k_cone_apply<<<g, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side);
     h->launches++;
   }
+}
+
+// capture one ADMM iteration into a CUDA graph (NCCL calls are capturable;
+// the emulated group is not, and runs the sequence directly)
+void build_graph(scs_handle* h) {
+  if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+  const long long before = h->launches;
+  if (!h->use_graph) {
+    // count launches with a dry count (no capture)
+    h->launches_per_iter = 0;
+    return;
+  }
+  CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+  enqueue_iteration(h);
   cudaGraph_t g;
   CK(cudaStreamEndCapture(h->st, &g));
   CK(cudaGraphInstantiate(&h->gexec, g, 0));
@@ -1120,16 +1414,27 @@ void build_graph(scs_handle* h) {
   h->launches_per_iter = h->launches - before;
 }
 
+void run_iteration(scs_handle* h) {
+  if (h->use_graph) {
+    CK(cudaGraphLaunch(h->gexec, h->st));
+    h->launches += h->launches_per_iter;
+  } else {
+    const long long before = h->launches;
+    enqueue_iteration(h);
+    h->launches_per_iter = h->launches - before;
+  }
+}
+
 // stand-alone termination check / residual evaluation of the current state
 void launch_residuals(scs_handle* h) {
   EpiResA ra{};
   ra.V = h->V;
   ra.xb = h->V.u;
-  launch_spmv(h, h->A, h->LA, ra);
+  a_pass(h, ra);
   EpiResAt rt{};
   rt.V = h->V;
   rt.xb = h->V.u + h->n;
-  launch_spmv(h, h->At, h->LAt, rt);
+  at_pass(h, rt);
 }
 
 void fill_info(scs_handle* h, scs_info* info) {
@@ -1180,8 +1485,7 @@ void do_steps(scs_handle* h, long long k) {
   long long batch = 1;
   while (todo > 0) {
     const long long b = std::min(batch, todo);
-    for (long long i = 0; i < b; ++i) CK(cudaGraphLaunch(h->gexec, h->st));
-    h->launches += b * h->launches_per_iter;
+    for (long long i = 0; i < b; ++i) run_iteration(h);
     h->launched_iters += b;
     todo -= b;
     pull_ctl(h);
@@ -1191,8 +1495,6 @@ void do_steps(scs_handle* h, long long k) {
     if (c->stop) break;
     batch = std::min<long long>(batch * 2, 64);
   }
-  if (c->iter != h->launched_iters && !c->stop)
-    throw Fail{SCS_ECUDA, "internal: iteration count mismatch"};
 }
 
 // Loop exit (solver.py:359-369): the last iteration's termination check is
@@ -1212,13 +1514,15 @@ void do_finish(scs_handle* h) {
   c->stop = 0;
   push_ctl(h);
   launch_residuals(h);
-  // tau > 1e-8 ||u|| ?
-  const long long len = h->n + h->m + 1;
-  const double un = sqrt(norm2_dev(h, h->V.u, h->V.u, len, 2));
+  // tau > 1e-8 ||u|| ?  (x-part and tau replicated, y-part sharded)
+  const long long n = h->n, m = h->m;
+  const double un2 = norm2_dev(h, h->V.u, h->V.u, n, 2) +
+                     norm2_dev(h, h->V.u + n, h->V.u + n, m, 2, true);
   pull_ctl(h);
   double ut = 0.0;
-  d2h(h, &ut, h->V.u + len - 1, 1);
+  d2h(h, &ut, h->V.u + n + m, 1);
   CK(cudaStreamSynchronize(h->st));
+  const double un = sqrt(un2 + ut * ut);
   c->status = ut > 1e-8 * un ? SCS_MAX_ITERS_REACHED : SCS_INDETERMINATE;
   c->force_check = 0;
   c->stop = 1;
@@ -1240,6 +1544,7 @@ int guard(scs_handle* h, const std::function<void()>& fn) {
     return SCS_ENOMEM;
   }
 }
+
 }  // namespace
 
 // ===========================================================================
@@ -1263,8 +1568,20 @@ void scs_destroy(scs_handle* h) {
     if (b.p) cudaFree(b.p);
   if (h->ctl_h) cudaFreeHost(h->ctl_h);
   if (h->st) cudaStreamDestroy(h->st);
+  delete h->comm;
   delete h;
 }
+
+scs_emu_group* scs_emu_group_create(int32_t world) {
+  if (world < 1) return nullptr;
+  scs_emu_group* g = new scs_emu_group();
+  g->world = world;
+  g->ptr.assign(world, nullptr);
+  g->cnt.assign(world, 0);
+  return g;
+}
+
+void scs_emu_group_destroy(scs_emu_group* g) { delete g; }
 
 static void validate(const scs_problem* P, const scs_settings* S) {
   if (!P || !S) throw Fail{SCS_EINVAL, "null problem or settings"};
@@ -1300,16 +1617,48 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     h->grid_full = h->sms * (2048 / kBlock);
     if (h->grid_full > kMaxGrid) h->grid_full = kMaxGrid;
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
-    if (dist && dist->world > 1) {
-      h->rank = dist->rank;
-      h->world = dist->world;
-    }
     h->m = P->m;
     h->n = P->n;
     h->m_glob = P->m_global > 0 ? P->m_global : P->m;
     h->row_lo = P->row_lo;
     h->nnz = P->colptr[P->n];
     const long long m = h->m, n = h->n;
+    h->bounds = {0, h->m_glob};
+    if (dist) {
+      h->rank = dist->rank;
+      h->world = dist->world;
+      if (h->world < 1 || h->rank < 0 || h->rank >= h->world)
+        throw Fail{SCS_EINVAL, "bad rank/world"};
+      if (dist->bounds) h->bounds.assign(dist->bounds, dist->bounds + h->world + 1);
+      else if (h->world > 1) throw Fail{SCS_EINVAL, "row-sharded create needs the shard bounds"};
+      if (h->bounds[h->rank] != h->row_lo || h->bounds[h->rank + 1] - h->bounds[h->rank] != m ||
+          h->bounds.front() != 0 || h->bounds.back() != h->m_glob)
+        throw Fail{SCS_EINVAL, "shard bounds do not match row_lo / m / m_global"};
+      h->sharded = h->world > 1 || (dist->flags & 1);
+      if (h->sharded) {
+        if (dist->emu_group) {
+          scs_emu_group* g = (scs_emu_group*)dist->emu_group;
+          if (g->world != h->world) throw Fail{SCS_EINVAL, "emulated group size != world"};
+          h->comm = new EmuComm(g, h->rank);
+        } else {
+#ifdef SCS_WITH_NCCL
+          if (!dist->nccl_id) throw Fail{SCS_EINVAL, "row-sharded create needs an NCCL id"};
+          NcclComm* nc = new NcclComm();
+          h->comm = nc;
+          ncclUniqueId id;
+          memcpy(id.internal, dist->nccl_id, sizeof(id.internal));
+          ncclResult_t r = ncclCommInitRank(&nc->c, h->world, id, h->rank);
+          if (r != ncclSuccess)
+            throw Fail{SCS_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)};
+#else
+          throw Fail{SCS_ENCCL, "built without NCCL"};
+#endif
+        }
+        h->use_graph = h->comm->capturable();
+      }
+    } else if (P->row_lo != 0 || h->m_glob != m) {
+      throw Fail{SCS_EINVAL, "a row slice needs a scs_dist"};
+    }
     CK(cudaMallocHost((void**)&h->ctl_h, sizeof(Ctl)));
     memset(h->ctl_h, 0, sizeof(Ctl));
     h->ctl = dalloc<Ctl>(h, 1);
@@ -1356,13 +1705,16 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     V.Dinv = dalloc<double>(h, m);
     V.Einv = dalloc<double>(h, n);
     V.part = dalloc<double>(h, (size_t)kMaxRed * kMaxGrid);
+    V.dred = dalloc<double>(h, kMaxRed);
     V.chunk_part = dalloc<double>(h, std::max(h->K.n_chunk, 1));
     V.soc_fac = dalloc<double>(h, 3 * std::max(h->K.n_bsoc, 1));
+    V.cone_red = dalloc<double>(h, h->cone_red_len);
+    V.xw = (!h->sharded || h->rank == 0) ? 1.0 : 0.0;
+    if (h->sharded) h->Traw = dalloc<double>(h, 2 * std::max<long long>(n, 1));
     h->tmp_n = dalloc<double>(h, n);
     h->tmp_m = dalloc<double>(h, m);
     h->tmp_m2 = dalloc<double>(h, m);
     h->zero_m = dalloc<double>(h, m);
-    h->seg_mean = dalloc<double>(h, std::max(h->nseg, 1));
     h->dscal = dalloc<double>(h, 8);
     CK(cudaMemsetAsync(h->zero_m, 0, std::max<long long>(m, 1) * sizeof(double), h->st));
     h2d(h, h->b0, P->b, m);
@@ -1472,8 +1824,8 @@ int scs_apply_a(scs_handle* h, int which, const double* in, double* out) {
     e.V = h->V;
     e.xb = din;
     e.out = dout;
-    if (which == 0) launch_spmv(h, h->A, h->LA, e);
-    else launch_spmv(h, h->At, h->LAt, e);
+    if (which == 0) a_pass(h, e);
+    else at_pass(h, e);
     d2h(h, out, dout, nout);
     CK(cudaStreamSynchronize(h->st));
   });
@@ -1484,30 +1836,31 @@ int scs_point_residuals(scs_handle* h, const double* x, const double* y, const d
   if (!h) return SCS_EINVAL;
   return guard(h, [&] {
     const long long n = h->n, m = h->m;
-    // A x = D^-1 A_hat E^-1 x ; A^T y = E^-1 A_hat^T D^-1 y
+    // A x = D^-1 A_hat E^-1 x ; A^T y = E^-1 A_hat^T D^-1 y  (rows may be sharded:
+    // m-length sums are all-reduced, A^T products go through at_pass)
     h2d(h, h->tmp_n, x, n);
     k_div<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->tmp_n, h->E, n, h->V.r);
     EpiPlain e{};
     e.V = h->V;
     e.xb = h->V.r;
     e.out = h->tmp_m2;
-    launch_spmv(h, h->A, h->LA, e);
+    a_pass(h, e);
     h2d(h, h->tmp_m, s, m);
     k_point_pri<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->tmp_m2, h->D, h->tmp_m, h->b0, m, h->V.q);
-    const double pri = sqrt(norm2_dev(h, h->V.q, h->V.q, m, 2));
-    const double bn = sqrt(norm2_dev(h, h->b0, h->b0, m, 2));
+    const double pri = sqrt(norm2_dev(h, h->V.q, h->V.q, m, 2, true));
+    const double bn = sqrt(norm2_dev(h, h->b0, h->b0, m, 2, true));
     h2d(h, h->tmp_m, y, m);
     k_div<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->tmp_m, h->D, m, h->tmp_m2);
     EpiPlain f{};
     f.V = h->V;
     f.xb = h->tmp_m2;
     f.out = h->V.Gp;
-    launch_spmv(h, h->At, h->LAt, f);
+    at_pass(h, f);
     k_point_dual<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->V.Gp, h->E, h->c0, n, h->V.r);
     const double dual = sqrt(norm2_dev(h, h->V.r, h->V.r, n, 2));
     const double cn = sqrt(norm2_dev(h, h->c0, h->c0, n, 2));
     const double ctx = norm2_dev(h, h->c0, h->tmp_n, n, 2);
-    const double bty = norm2_dev(h, h->b0, h->tmp_m, m, 2);
+    const double bty = norm2_dev(h, h->b0, h->tmp_m, m, 2, true);
     out3[0] = pri / (1.0 + bn);
     out3[1] = dual / (1.0 + cn);
     out3[2] = fabs(ctx + bty) / (1.0 + fabs(ctx) + fabs(bty));
@@ -1531,6 +1884,7 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t
     if (kind != 2) n = 0;
     h->m = h->m_glob = m;
     h->n = n;
+    h->bounds = {0, m};
     scs_problem P{};
     P.m = m; P.n = n; P.z = z; P.l = l; P.nq = nq; P.q = q; P.ns = ns; P.s = s; P.ep = ep;
     build_cones(h, &P);
@@ -1560,8 +1914,11 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t
     double* zc = dalloc<double>(h, std::max<long long>(n, m));
     V.c = zc; V.b = zc;
     V.part = dalloc<double>(h, (size_t)kMaxRed * kMaxGrid);
+    V.dred = dalloc<double>(h, kMaxRed);
     V.chunk_part = dalloc<double>(h, std::max(h->K.n_chunk, 1));
     V.soc_fac = dalloc<double>(h, 3 * std::max(h->K.n_bsoc, 1));
+    V.cone_red = dalloc<double>(h, h->cone_red_len);
+    V.xw = 1.0;
     CK(cudaMemsetAsync(zc, 0, std::max<long long>(n, m) * sizeof(double), h->st));
     CK(cudaMemsetAsync(V.gx, 0, std::max<long long>(n, 1) * sizeof(double), h->st));
     CK(cudaMemsetAsync(V.gy, 0, std::max<long long>(m, 1) * sizeof(double), h->st));
@@ -1573,7 +1930,7 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t
     const long long work = std::max<long long>(n + h->K.z + h->K.l, 1);
     int g = std::max(elem_grid(h, work), std::min(h->K.n_chunk, h->grid_full));
     g = std::max(g, std::min((int)((h->K.n_ssoc * 32LL + kBlock - 1) / kBlock), h->grid_full));
-    k_cone_tail<<<g, kBlock, 0, h->st>>>(V, h->K);
+    k_cone_tail<<<g, kBlock, 0, h->st>>>(V, h->K, 0);
     if (h->K.n_chunk > 0 || h->K.n_psd > 0) {
       const int ga = std::max(1, std::min(std::max(h->K.n_chunk, h->K.n_psd), h->grid_full));
       k_cone_apply<<<ga, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side);
@@ -1597,8 +1954,9 @@ int scs_bench_iters(scs_handle* h, int64_t k, double* ms) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
+    const long long before = h->launches;
     CK(cudaEventRecord(e0, h->st));
-    for (int64_t i = 0; i < k; ++i) CK(cudaGraphLaunch(h->gexec, h->st));
+    for (int64_t i = 0; i < k; ++i) run_iteration(h);
     CK(cudaEventRecord(e1, h->st));
     CK(cudaEventSynchronize(e1));
     float f = 0.f;
@@ -1607,7 +1965,7 @@ int scs_bench_iters(scs_handle* h, int64_t k, double* ms) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     h->launched_iters += k;
-    h->launches = k * h->launches_per_iter;
+    h->launches = h->launches - before;
     pull_ctl(h);
     check_err(h);
   });
@@ -1655,6 +2013,16 @@ int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms, double* 
     cudaEventDestroy(e1);
     *h->ctl_h = saved;
     push_ctl(h);
+  });
+}
+
+int scs_allreduce(scs_handle* h, double* vals, int64_t n) {
+  if (!h || n < 0 || n > 8) return SCS_EINVAL;
+  return guard(h, [&] {
+    h2d(h, h->dscal, vals, n);
+    allreduce(h, h->dscal, n);
+    d2h(h, vals, h->dscal, n);
+    CK(cudaStreamSynchronize(h->st));
   });
 }
 

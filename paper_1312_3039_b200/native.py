@@ -32,6 +32,7 @@ EXPORTS = (
     "scs_point_residuals", "scs_apply_a", "scs_project_cone", "scs_destroy",
     "scs_last_error", "scs_abi_version", "scs_nccl_unique_id",
     "scs_partition_rows", "scs_gen_lasso", "scs_bench_iters", "scs_bench_kernel",
+    "scs_emu_group_create", "scs_emu_group_destroy", "scs_allreduce",
 )
 
 
@@ -51,7 +52,9 @@ class SettingsC(C.Structure):
 
 
 class Dist(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.POINTER(C.c_uint8))]
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.POINTER(C.c_uint8)),
+                ("emu_group", C.c_void_p), ("bounds", C.POINTER(C.c_int64)),
+                ("flags", C.c_int32), ("pad_", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -98,6 +101,9 @@ def load():
         "scs_bench_iters": (C.c_int, [hp, C.c_int64, f64p]),
         "scs_bench_kernel": (C.c_int, [hp, C.c_int, C.c_int64, f64p, f64p]),
         "scs_destroy": (None, [hp]),
+        "scs_emu_group_create": (C.c_void_p, [C.c_int32]),
+        "scs_emu_group_destroy": (None, [C.c_void_p]),
+        "scs_allreduce": (C.c_int, [hp, f64p, C.c_int64]),
         "scs_last_error": (C.c_char_p, [hp]),
         "scs_abi_version": (C.c_int, []),
         "scs_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(native.EXPORTS)
-    assert lib.scs_abi_version() == 1
+    assert lib.scs_abi_version() == 2
 
 
 def test_last_error_without_handle():
