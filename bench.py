@@ -200,8 +200,8 @@ def run_ours(args, cfg):
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
-        raise SystemExit("row-sharded multi-GPU bench is not enabled in this build")
+    if world > 1 or os.environ.get("SCS_BENCH_FORCE_SHARDED"):
+        return run_sharded(args, cfg, rank, world)
     lib = native.load()
     t0 = time.perf_counter()
     colptr, rowidx, vals, b, c, cone = load_problem(cfg)
@@ -283,6 +283,101 @@ def run_ours(args, cfg):
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_sample(3, 1, nnz)
     print(json.dumps(line), flush=True)
+
+
+def lasso_bounds(cfg, world):
+    """Shard bounds for the LASSO encoding (nonzeros per row known
+    analytically: 2 for the +-z <= t rows, 1 for the two SOC head rows,
+    nnz_f/q for the F rows), cut by scs_partition_rows."""
+    from paper_1312_3039_b200 import native
+    p, q = cfg["p"], cfg["q"]
+    m, n, nnzf = lasso_dims(cfg)
+    w = np.empty(m, np.int64)
+    w[:2 * p] = 2
+    w[2 * p:2 * p + 2] = 1
+    w[2 * p + 2:] = max(1, nnzf // q)
+    return native.partition_rows({"z": 0, "l": 2 * p, "q": [q + 2], "s": [], "ep": 0}, w, world)
+
+
+def run_sharded(args, cfg, rank, world):
+    """N GPUs, one process each: A row-sharded, NCCL all-reduce of the A^T
+    partial products and y-part scalars (strong scaling: total work fixed)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1312_3039_b200 as P
+    from paper_1312_3039_b200 import native, parallel
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dist.init_process_group("gloo", init_method="env://", rank=rank, world_size=world)
+    lib = native.load()
+    m, n, nnzf = lasso_dims(cfg)
+    bounds = lasso_bounds(cfg, world)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    t0 = time.perf_counter()
+    colptr, rowidx, vals, b, c, cone = native.gen_lasso(cfg["p"], cfg["q"], nnzf, seed=cfg["seed"],
+                                                        row_lo=lo, row_hi=hi)
+    gen_s = time.perf_counter() - t0
+    nid = parallel.nccl_bootstrap(rank, world)
+    shard = parallel.ShardProblem(colptr, rowidx, vals, b, c, cone, lo, m)
+    st = P.Settings(max_iters=args.steps, device=local)
+    t0 = time.perf_counter()
+    ws = P.Workspace(shard, st, dist=parallel.ShardSpec(rank, world, bounds, nccl_id=nid,
+                                                        force=True))
+    setup_s = time.perf_counter() - t0
+    h = ws._h
+    native.check(lib.scs_begin(h, None, None, None), h)
+    ms = native.C.c_double()
+    native.check(lib.scs_bench_iters(h, args.warmup, native.C.byref(ms)), h)
+    dist.barrier()
+    with Clocks(local) as clk:
+        native.check(lib.scs_bench_iters(h, args.steps, native.C.byref(ms)), h)
+    info = native.Info()
+    native.check(lib.scs_step(h, 0, native.C.byref(info)), h)
+    t = torch.tensor([ms.value], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_iter = t.item() / args.steps
+    ips = 1000.0 / ms_iter
+    peak, peak_kind = peaks()
+    kern = {}
+    for kind, name in ((0, "spmv_A(q=A p)"), (1, "spmv_At_cg(Gp=p+A^T q; p'Gp)")):
+        kms, kb = native.C.c_double(), native.C.c_double()
+        native.check(lib.scs_bench_kernel(h, kind, 10, native.C.byref(kms), native.C.byref(kb)), h)
+        kern[name] = {"ms": kms.value, "bytes": kb.value, "gbs": kb.value / (kms.value * 1e-3) / 1e9}
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    nnz = cfg["nnz"]
+    x0, y0, s0 = np.zeros(n), np.zeros(hi - lo), np.zeros(hi - lo)
+    dist.barrier()
+    t0 = time.perf_counter()
+    sol = ws.solve(warm_start=(x0, y0, s0))
+    e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        line = {
+            "metric": "ADMM iterations/s (indirect SCS, LASSO-as-SOCP)", "value": ips,
+            "unit": "iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_iter, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(config_dict(args.config, cfg, m, n, nnz),
+                           parallelism=f"row-sharded x{world} (NCCL all-reduce)",
+                           bounds=[int(x) for x in bounds]),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": kern[dom]["gbs"] / peak, "traffic": None,
+                         "note": "rank 0's shard, kernel timed alone", "kernels": kern,
+                         "iteration": {"bytes_formula": b_iter(m, n, nnz),
+                                       "achieved": b_iter(m, n, nnz) * ips / 1e9,
+                                       "frac": b_iter(m, n, nnz) * ips / 1e9 / (peak * world)}},
+            "e2e": {"value": sol.info.iterations / e2e.item(), "unit": "iters/s",
+                    "h2d_bytes_per_step": 8 * (n + 2 * (hi - lo)) / max(sol.info.iterations, 1),
+                    "d2h_bytes_per_step": 8 * 3 * (n + hi - lo) / max(sol.info.iterations, 1),
+                    "iterations": sol.info.iterations, "seconds": e2e.item()},
+            "gpu_launches": int(info.launches), "clocks": clk.summary(),
+            "setup_s": setup_s, "generate_s": gen_s, "status_after_timed": int(info.status),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():
