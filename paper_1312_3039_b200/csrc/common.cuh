@@ -79,11 +79,13 @@ __device__ __forceinline__ double group_sum(double v) {
   return v;
 }
 
-// Deterministic block reduction of K values; result valid in every thread.
+// Deterministic block reduction of K values (any block size up to 1024);
+// result valid in every thread.
 template <int K>
 __device__ __forceinline__ void block_sum(double (&v)[K]) {
-  __shared__ double sh[K][kWarps];
+  __shared__ double sh[K][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
 #pragma unroll
   for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
   __syncthreads();
@@ -95,8 +97,7 @@ __device__ __forceinline__ void block_sum(double (&v)[K]) {
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) t += sh[k][w];
+    for (int w = 0; w < nw; ++w) t += sh[k][w];
     v[k] = t;
   }
   __syncthreads();

@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "cones.cuh"
 #include "kernels.cuh"
+#include "tiled.cuh"
 
 #ifdef SCS_WITH_NCCL
 #include <nccl.h>
@@ -793,6 +794,11 @@ struct scs_handle {
   // matrices
   Csr A{}, At{};
   int LA = 32, LAt = 32;
+  // slab-tiled copies (tiled.cuh) and their launch shapes per NV
+  bool tiled = false;
+  Tiled tA{}, tAt{};
+  int tsub[2][3] = {}, tsplit[2][3] = {};  // [matrix][NV]
+  double* Ptile = nullptr;
   // cones
   Cones K{};
   int nseg = 0, nseg_g = 0;
@@ -902,12 +908,142 @@ void launch_spmv(scs_handle* h, const Csr& M, int L, const Epi& epi) {
   h->launches++;
 }
 
+template <int NV, int STRIDE, class Epi>
+void set_tiled_smem(size_t bytes) {
+  static size_t done = 0;
+  if (bytes > 48 * 1024 && bytes > done) {
+    CK(cudaFuncSetAttribute(k_tiled<NV, STRIDE, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)bytes));
+    done = bytes;
+  }
+}
+
+// SpMV with the matrix A (mat = 0) or A^T (mat = 1): slab-tiled kernel when
+// the problem is large, CSR kernel otherwise.
+template <class Epi>
+void launch_mat(scs_handle* h, int mat, const Epi& epi) {
+  if (!h->tiled) {
+    if (mat == 0) launch_spmv(h, h->A, h->LA, epi);
+    else launch_spmv(h, h->At, h->LAt, epi);
+    return;
+  }
+  constexpr int NV = Epi::NV, STRIDE = Epi::STRIDE;
+  const Tiled& T = mat == 0 ? h->tA : h->tAt;
+  const int sub = h->tsub[mat][NV], splits = h->tsplit[mat][NV];
+  const size_t smem = (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8;
+  set_tiled_smem<NV, STRIDE, Epi>(smem);
+  const int ctas = T.NB * sub * splits;
+  k_tiled<NV, STRIDE, Epi><<<ctas, kTileThreads, smem, h->st>>>(T, epi, sub, splits, h->Ptile);
+  h->launches++;
+  if (splits > 1) {
+    k_tiled_combine<Epi><<<elem_grid(h, T.rows), kBlock, 0, h->st>>>(h->Ptile, splits, T.rows, epi);
+    h->launches++;
+  }
+}
+
+// Pick (row sub-blocks per CTA, slab splits) for a tiled matrix and NV:
+// smem budget, then a two-level bandwidth model (DRAM: matrix stream and
+// split partials; L2: + slab staging) with wave quantisation on the SMs.
+void tile_shapes(scs_handle* h, int mat, const Tiled& T, long long nnz) {
+  for (int NV = 1; NV <= 2; ++NV) {
+    double best = 1e300;
+    for (int sub = 1; sub <= kTileNsub; sub *= 2) {
+      const size_t smem = (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8;
+      if (smem > 200 * 1024) continue;
+      for (int splits = 1; splits <= 64 && splits <= T.S; splits *= 2) {
+        const double ctas = (double)T.NB * sub * splits;
+        const double stream = 12.0 * nnz + 8.0 * NV * T.rows;
+        const double slabs = (double)T.NB * sub * T.cols * NV * 8.0;
+        const double part = splits > 1 ? 16.0 * splits * T.rows * NV : 0.0;
+        const double waves = std::ceil(ctas / h->sms);
+        const double eff = ctas / (h->sms * waves);
+        const double t = std::max((stream + part) / 5.5e12, (stream + slabs + part) / 12e12) / eff;
+        if (t < best * 0.97) {
+          best = t;
+          h->tsub[mat][NV] = sub;
+          h->tsplit[mat][NV] = splits;
+        }
+      }
+    }
+  }
+}
+
+// Re-lay a CSR matrix out as slab tiles (stable device radix sort on the
+// tile key keeps the row-major order inside each tile).
+void build_tiled(scs_handle* h, const Csr& M, long long cols, Tiled& T) {
+  const long long rows = M.rows, nnz = M.rp ? 0 : 0;
+  (void)nnz;
+  long long nz = 0;
+  CK(cudaMemcpyAsync(&nz, M.rp + rows, sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  T.rows = rows;
+  T.cols = cols;
+  T.RB = 16384;
+  T.W = 8192;
+  T.S = (int)((cols + T.W - 1) / T.W);
+  T.NB = (int)((rows + T.RB - 1) / T.RB);
+  const long long ntile = (long long)T.NB * T.S * kTileNsub;
+  if (ntile >= (1LL << 31) - 1) throw Fail{SCS_EINVAL, "too many tiles"};
+  int* rowid = dalloc<int>(h, nz);
+  int* key = dalloc<int>(h, nz);
+  int* skey = dalloc<int>(h, nz);
+  int* perm_in = dalloc<int>(h, nz);
+  int* perm = dalloc<int>(h, nz);
+  k_expand_rows<<<elem_grid(h, rows * 32), kBlock, 0, h->st>>>(M.rp, rows, rowid);
+  k_tile_keys<<<elem_grid(h, nz), kBlock, 0, h->st>>>(rowid, M.ci, nz, T.RB, T.W, T.S, key);
+  k_iota<<<elem_grid(h, nz), kBlock, 0, h->st>>>(perm_in, nz);
+  int bits = 1;
+  while ((1LL << bits) < ntile) ++bits;
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const int*)key, skey,
+                                     (const int*)perm_in, perm, (int)nz, 0, bits, h->st));
+  void* tmp = dalloc<char>(h, tmp_bytes);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, (const int*)key, skey, (const int*)perm_in,
+                                     perm, (int)nz, 0, bits, h->st));
+  unsigned* pk = dalloc<unsigned>(h, nz);
+  double* tv = dalloc<double>(h, nz);
+  long long* ts = dalloc<long long>(h, ntile + 1);
+  k_tile_pack<<<elem_grid(h, nz), kBlock, 0, h->st>>>(perm, rowid, M.ci, M.v, nz, T.RB, T.W, pk, tv);
+  k_rowptr<<<elem_grid(h, ntile + 1), kBlock, 0, h->st>>>(skey, nz, ntile, ts);
+  CK(cudaStreamSynchronize(h->st));
+  dfree(h, tmp);
+  dfree(h, perm);
+  dfree(h, perm_in);
+  dfree(h, skey);
+  dfree(h, key);
+  dfree(h, rowid);
+  T.ts = ts;
+  T.pk = pk;
+  T.v = tv;
+}
+
+void setup_tiled(scs_handle* h) {
+  const char* env = getenv("SCS_TILED");
+  const bool want = env ? atoi(env) != 0 : h->nnz >= 4000000LL;
+  if (!want || h->nnz == 0) return;
+  build_tiled(h, h->A, h->n, h->tA);
+  build_tiled(h, h->At, h->m, h->tAt);
+  tile_shapes(h, 0, h->tA, h->nnz);
+  tile_shapes(h, 1, h->tAt, h->nnz);
+  size_t need = 0;
+  for (int mat = 0; mat < 2; ++mat)
+    for (int NV = 1; NV <= 2; ++NV) {
+      const Tiled& T = mat == 0 ? h->tA : h->tAt;
+      if (h->tsplit[mat][NV] > 1) need = std::max<size_t>(need, (size_t)h->tsplit[mat][NV] * (size_t)T.rows * NV);
+    }
+  if (need) h->Ptile = dalloc<double>(h, need);
+  h->tiled = true;
+  dbg("tiled: A NB=%d S=%d (sub,split) nv1=(%d,%d) nv2=(%d,%d); At NB=%d S=%d nv1=(%d,%d) nv2=(%d,%d)",
+      h->tA.NB, h->tA.S, h->tsub[0][1], h->tsplit[0][1], h->tsub[0][2], h->tsplit[0][2], h->tAt.NB,
+      h->tAt.S, h->tsub[1][1], h->tsplit[1][1], h->tsub[1][2], h->tsplit[1][2]);
+}
+
 // A pass over the local rows.  Row-sharded: its (y-part) totals are
 // all-reduced and finished by k_finish.
 template <class Epi>
 void a_pass(scs_handle* h, Epi epi) {
   epi.defer = (h->sharded && Epi::NR > 0) ? 1 : 0;
-  launch_spmv(h, h->A, h->LA, epi);
+  launch_mat(h, 0, epi);
   if (epi.defer) {
     allreduce(h, h->V.dred, Epi::NR);
     k_finish<Epi><<<1, 32, 0, h->st>>>(epi);
@@ -922,13 +1058,13 @@ template <class Epi>
 void at_pass(scs_handle* h, Epi epi) {
   epi.defer = 0;
   if (!h->sharded) {
-    launch_spmv(h, h->At, h->LAt, epi);
+    launch_mat(h, 1, epi);
     return;
   }
   EpiRaw<Epi> raw{};
   static_cast<Epi&>(raw) = epi;
   raw.T = h->Traw;
-  launch_spmv(h, h->At, h->LAt, raw);
+  launch_mat(h, 1, raw);
   allreduce(h, h->Traw, (size_t)h->n * Epi::NV);
   k_rows<Epi><<<elem_grid(h, h->n), kBlock, 0, h->st>>>(h->Traw, h->n, epi);
   h->launches++;
@@ -1727,6 +1863,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     k_recip<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->D, m, (double*)V.Dinv);
     k_recip<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->E, n, (double*)V.Einv);
     dbg("equilibrated mean_col=%g mean_row=%g", h->mean_col, h->mean_row);
+    setup_tiled(h);
     scale_vectors(h);
     dbg("scaled sigma=%g rho=%g", h->sigma, h->rho);
     solve_g(h);
@@ -1989,12 +2126,12 @@ int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms, double* 
         EpiAp<false> ea{};
         ea.V = h->V;
         ea.xb = h->V.X2;
-        launch_spmv(h, h->A, h->LA, ea);
+        launch_mat(h, 0, ea);
       } else {
         EpiAtGp eg{};
         eg.V = h->V;
         eg.xb = h->V.q;
-        launch_spmv(h, h->At, h->LAt, eg);
+        launch_mat(h, 1, eg);
       }
     };
     one();
