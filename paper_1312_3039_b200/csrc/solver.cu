@@ -930,7 +930,7 @@ void launch_mat(scs_handle* h, int mat, const Epi& epi) {
   constexpr int NV = Epi::NV, STRIDE = Epi::STRIDE;
   const Tiled& T = mat == 0 ? h->tA : h->tAt;
   const int sub = h->tsub[mat][NV], splits = h->tsplit[mat][NV];
-  const size_t smem = (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8;
+  const size_t smem = 2 * (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8;
   set_tiled_smem<NV, STRIDE, Epi>(smem);
   const int ctas = T.NB * sub * splits;
   k_tiled<NV, STRIDE, Epi><<<ctas, kTileThreads, smem, h->st>>>(T, epi, sub, splits, h->Ptile);
@@ -948,7 +948,7 @@ void tile_shapes(scs_handle* h, int mat, const Tiled& T, long long nnz) {
   for (int NV = 1; NV <= 2; ++NV) {
     double best = 1e300;
     for (int sub = 1; sub <= kTileNsub; sub *= 2) {
-      const size_t smem = (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8;
+      const size_t smem = 2 * (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8;
       if (smem > 200 * 1024) continue;
       for (int splits = 1; splits <= 64 && splits <= T.S; splits *= 2) {
         const double ctas = (double)T.NB * sub * splits;
@@ -979,7 +979,7 @@ void build_tiled(scs_handle* h, const Csr& M, long long cols, Tiled& T) {
   T.rows = rows;
   T.cols = cols;
   T.RB = 16384;
-  T.W = 8192;
+  T.W = 4096;
   T.S = (int)((cols + T.W - 1) / T.W);
   T.NB = (int)((rows + T.RB - 1) / T.RB);
   const long long ntile = (long long)T.NB * T.S * kTileNsub;

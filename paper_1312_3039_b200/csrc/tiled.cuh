@@ -57,19 +57,44 @@ __device__ __forceinline__ long long row_align(const unsigned* __restrict__ pk, 
   return e1;
 }
 
+// async copy of one gather-vector slab (NV values per column) into smem
+template <int NV, int STRIDE>
+__device__ __forceinline__ void slab_issue(const double* __restrict__ xb, long long c0, int wc,
+                                           double* dst) {
+  for (int i = threadIdx.x; i < wc; i += blockDim.x) {
+    const double* src = xb + (size_t)(c0 + i) * STRIDE;
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst + (size_t)i * NV);
+    if constexpr (NV == 1) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src));
+    } else {
+      static_assert(NV == 2, "tiled NV");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src));
+    }
+  }
+  asm volatile("cp.async.commit_group;");
+}
+
+__device__ __forceinline__ int next_tile(const Tiled& T, long long tb0, int fsb, int s, int s_hi) {
+  for (; s < s_hi; ++s) {
+    const long long tb = tb0 + (long long)s * kTileNsub;
+    if (__ldg(T.ts + tb) != __ldg(T.ts + tb + fsb)) return s;
+  }
+  return s_hi;
+}
+
 template <int NV, int STRIDE, class Epi>
 __global__ void __launch_bounds__(kTileThreads, 1)
     k_tiled(Tiled T, Epi epi0, int sub, int splits, double* P) {
   Epi epi = epi0;
   if (!epi.load()) return;
   extern __shared__ double sm[];
-  double* slab = sm;                    // W * NV
-  double* acc = sm + (size_t)T.W * NV;  // rows of this CTA * NV
+  double* slabs = sm;                       // 2 x W * NV (double buffer)
+  double* acc = sm + 2 * (size_t)T.W * NV;  // rows of this CTA * NV
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int sp = blockIdx.x % splits;
   const int rest = blockIdx.x / splits;
   const int sbc = rest % sub, b = rest / sub;
-  const int fsb = kTileNsub / sub;      // format sub-blocks per CTA
+  const int fsb = kTileNsub / sub;          // format sub-blocks per CTA
   const int rsub = T.RB / kTileNsub;
   const int rel0 = sbc * fsb * rsub;
   const long long r0 = (long long)b * T.RB + rel0;
@@ -77,50 +102,71 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   const int R = left <= 0 ? 0 : (int)(left < (long long)fsb * rsub ? left : (long long)fsb * rsub);
   for (int i = tid; i < R * NV; i += blockDim.x) acc[i] = 0.0;
   const int s_lo = (int)((long long)T.S * sp / splits), s_hi = (int)((long long)T.S * (sp + 1) / splits);
-  for (int s = s_lo; s < s_hi; ++s) {
-    const long long tb = ((long long)b * T.S + s) * kTileNsub + (long long)sbc * fsb;
-    const long long e0 = __ldg(T.ts + tb), e1 = __ldg(T.ts + tb + fsb);
-    if (e0 == e1) continue;  // empty tile: no slab load
-    __syncthreads();         // previous tile is done with the slab
+  const long long tb0 = (long long)b * T.S * kTileNsub + (long long)sbc * fsb;
+  auto slab_of = [&](int s, double* dst) {
     const long long c0 = (long long)s * T.W;
     const int wc = (int)((T.cols - c0) < T.W ? (T.cols - c0) : T.W);
-    for (int i = tid; i < wc; i += blockDim.x) {
-      double g[NV];
-      gather<NV, STRIDE>(epi.xb, (int)(c0 + i), g);
-#pragma unroll
-      for (int t = 0; t < NV; ++t) slab[i * NV + t] = g[t];
+    slab_issue<NV, STRIDE>(epi.xb, c0, wc, dst);
+  };
+  int s = next_tile(T, tb0, fsb, s_lo, s_hi);
+  if (s < s_hi) slab_of(s, slabs);
+  int cur = 0;
+  while (s < s_hi) {
+    const int sn = next_tile(T, tb0, fsb, s + 1, s_hi);
+    if (sn < s_hi) {
+      slab_of(sn, slabs + (size_t)(cur ^ 1) * T.W * NV);
+      asm volatile("cp.async.wait_group 1;");
+    } else {
+      asm volatile("cp.async.wait_group 0;");
     }
-    __syncthreads();
+    __syncthreads();  // slab s visible to the whole CTA
+    const double* slab = slabs + (size_t)cur * T.W * NV;
+    const long long tb = tb0 + (long long)s * kTileNsub;
+    const long long e0 = __ldg(T.ts + tb), e1 = __ldg(T.ts + tb + fsb);
     const long long len = e1 - e0;
     const long long ws = row_align(T.pk, e0 + len * warp / nw, e0, e1);
     const long long we = row_align(T.pk, e0 + len * (warp + 1) / nw, e0, e1);
-    for (long long e = ws; e < we; e += 32) {
-      const long long k = e + lane;
-      const bool ok = k < we;
-      const unsigned p = ok ? __ldcs(T.pk + k) : 0u;
-      const double a = ok ? __ldcs(T.v + k) : 0.0;
-      const int r = ok ? (int)(p >> 16) - rel0 : -1 - lane;
-      const int c = (int)(p & 0xffffu);
-      double x[NV];
+    for (long long e = ws; e < we; e += 128) {
+      // four chunks of the stream in flight before any use
+      unsigned p[4];
+      double a[4];
 #pragma unroll
-      for (int t = 0; t < NV; ++t) x[t] = ok ? a * slab[c * NV + t] : 0.0;
-      // segmented inclusive scan over lanes of equal row (runs are contiguous)
+      for (int u = 0; u < 4; ++u) {
+        const long long k = e + u * 32 + lane;
+        const bool ok = k < we;
+        p[u] = ok ? __ldcs(T.pk + k) : 0u;
+        a[u] = ok ? __ldcs(T.v + k) : 0.0;
+      }
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int rp = __shfl_up_sync(0xffffffffu, r, o);
+      for (int u = 0; u < 4; ++u) {
+        if (e + u * 32 >= we) break;  // warp-uniform
+        const bool ok = e + u * 32 + lane < we;
+        const int r = ok ? (int)(p[u] >> 16) - rel0 : -1 - lane;
+        const int c = (int)(p[u] & 0xffffu);
+        double x[NV];
 #pragma unroll
-        for (int t = 0; t < NV; ++t) {
-          const double xp = __shfl_up_sync(0xffffffffu, x[t], o);
-          if (lane >= o && rp == r) x[t] += xp;
+        for (int t = 0; t < NV; ++t) x[t] = ok ? a[u] * slab[c * NV + t] : 0.0;
+        // segmented inclusive scan over lanes of equal row (runs are contiguous)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int rp = __shfl_up_sync(0xffffffffu, r, o);
+#pragma unroll
+          for (int t = 0; t < NV; ++t) {
+            const double xp = __shfl_up_sync(0xffffffffu, x[t], o);
+            if (lane >= o && rp == r) x[t] += xp;
+          }
         }
-      }
-      const int rn = __shfl_down_sync(0xffffffffu, r, 1);
-      if (ok && (lane == 31 || rn != r)) {
+        const int rn = __shfl_down_sync(0xffffffffu, r, 1);
+        if (ok && (lane == 31 || rn != r)) {
 #pragma unroll
-        for (int t = 0; t < NV; ++t) acc[r * NV + t] += x[t];
+          for (int t = 0; t < NV; ++t) acc[r * NV + t] += x[t];
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
+    __syncthreads();  // everyone is done with slab `cur` before it is refilled
+    cur ^= 1;
+    s = sn;
   }
   __syncthreads();
   constexpr int NR = Epi::NR > 0 ? Epi::NR : 1;
