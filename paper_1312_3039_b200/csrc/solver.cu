@@ -3,6 +3,7 @@
 // Ruiz equilibration, g = M^-1 h), the graph-captured iteration loop, and
 // the C-ABI declared in include/scs_b200.h.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1000,18 +1001,30 @@ void build_tiled(scs_handle* h, const Csr& M, long long cols, Tiled& T) {
   void* tmp = dalloc<char>(h, tmp_bytes);
   CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, (const int*)key, skey, (const int*)perm_in,
                                      perm, (int)nz, 0, bits, h->st));
-  unsigned* pk = dalloc<unsigned>(h, nz);
-  double* tv = dalloc<double>(h, nz);
+  // sub-tile starts, each sub-tile padded to a multiple of 4 entries so a
+  // lane's 4 entries are one 16-B index load and one 32-B value load
+  long long* ts_raw = dalloc<long long>(h, ntile + 1);
+  long long* cnt = dalloc<long long>(h, ntile + 1);
   long long* ts = dalloc<long long>(h, ntile + 1);
-  k_tile_pack<<<elem_grid(h, nz), kBlock, 0, h->st>>>(perm, rowid, M.ci, M.v, nz, T.RB, T.W, pk, tv);
-  k_rowptr<<<elem_grid(h, ntile + 1), kBlock, 0, h->st>>>(skey, nz, ntile, ts);
+  k_rowptr<<<elem_grid(h, ntile + 1), kBlock, 0, h->st>>>(skey, nz, ntile, ts_raw);
+  k_pad4<<<elem_grid(h, ntile), kBlock, 0, h->st>>>(ts_raw, ntile, cnt);
+  CK(cudaMemsetAsync(cnt + ntile, 0, sizeof(long long), h->st));
+  size_t scan_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt, ts, (int)(ntile + 1), h->st));
+  void* scan_tmp = dalloc<char>(h, scan_bytes);
+  CK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, cnt, ts, (int)(ntile + 1), h->st));
+  long long npad = 0;
+  CK(cudaMemcpyAsync(&npad, ts + ntile, sizeof(long long), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
-  dfree(h, tmp);
-  dfree(h, perm);
-  dfree(h, perm_in);
-  dfree(h, skey);
-  dfree(h, key);
-  dfree(h, rowid);
+  unsigned* pk = dalloc<unsigned>(h, npad);
+  double* tv = dalloc<double>(h, npad);
+  k_fill_pad<<<elem_grid(h, npad), kBlock, 0, h->st>>>(pk, tv, npad);
+  k_tile_pack<<<elem_grid(h, nz), kBlock, 0, h->st>>>(perm, skey, ts_raw, ts, rowid, M.ci, M.v, nz,
+                                                       T.RB, T.W, pk, tv);
+  CK(cudaStreamSynchronize(h->st));
+  dfree(h, scan_tmp);
+  dfree(h, cnt);
+  dfree(h, ts_raw);
   T.ts = ts;
   T.pk = pk;
   T.v = tv;

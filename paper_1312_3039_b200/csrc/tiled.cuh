@@ -40,23 +40,6 @@ struct Tiled {
   const double* v;
 };
 
-// First entry >= pos (within [e0, e1)) that starts a new row, so that warps
-// own whole rows of the tile.
-__device__ __forceinline__ long long row_align(const unsigned* __restrict__ pk, long long pos,
-                                               long long e0, long long e1) {
-  if (pos <= e0) return e0;
-  if (pos >= e1) return e1;
-  const unsigned rprev = __ldg(pk + pos - 1) >> 16;
-  const int lane = threadIdx.x & 31;
-  for (long long q = pos; q < e1; q += 32) {
-    const long long k = q + lane;
-    const bool start = k < e1 && (__ldg(pk + k) >> 16) != rprev;
-    const unsigned mask = __ballot_sync(0xffffffffu, start);
-    if (mask) return q + __ffs(mask) - 1;
-  }
-  return e1;
-}
-
 // async copy of one gather-vector slab (NV values per column) into smem
 template <int NV, int STRIDE>
 __device__ __forceinline__ void slab_issue(const double* __restrict__ xb, long long c0, int wc,
@@ -90,6 +73,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   extern __shared__ double sm[];
   double* slabs = sm;                       // 2 x W * NV (double buffer)
   double* acc = sm + 2 * (size_t)T.W * NV;  // rows of this CTA * NV
+  __shared__ int bndr[2 * (kTileThreads / 32)];
+  __shared__ double bndv[2 * (kTileThreads / 32) * NV];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int sp = blockIdx.x % splits;
   const int rest = blockIdx.x / splits;
@@ -123,48 +108,135 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const double* slab = slabs + (size_t)cur * T.W * NV;
     const long long tb = tb0 + (long long)s * kTileNsub;
     const long long e0 = __ldg(T.ts + tb), e1 = __ldg(T.ts + tb + fsb);
-    const long long len = e1 - e0;
-    const long long ws = row_align(T.pk, e0 + len * warp / nw, e0, e1);
-    const long long we = row_align(T.pk, e0 + len * (warp + 1) / nw, e0, e1);
+    // warp w owns the 4-aligned entry run [ws, we) of the (4-padded) tile;
+    // rows it shares with neighbouring warps go to its boundary slots
+    const long long q4 = (e1 - e0) >> 2;
+    const long long ws = e0 + 4 * (q4 * warp / nw), we = e0 + 4 * (q4 * (warp + 1) / nw);
+    int fr = -2, lr = -3;
+    if (we > ws) {
+      const unsigned pf = __ldg(T.pk + ws) >> 16, pl = __ldg(T.pk + we - 1) >> 16;
+      fr = pf == 0xffffu ? -2 : (int)pf - rel0;
+      lr = pl == 0xffffu ? -3 : (int)pl - rel0;
+    }
+    if (lane == 0) {
+      bndr[warp * 2] = fr;
+      bndr[warp * 2 + 1] = lr;
+#pragma unroll
+      for (int t = 0; t < NV; ++t) { bndv[(warp * 2) * NV + t] = 0.0; bndv[(warp * 2 + 1) * NV + t] = 0.0; }
+    }
+    __syncwarp();
+    auto emit = [&](int r, const double* v) {
+      if (r < 0) return;
+      double* dst = r == fr ? bndv + (warp * 2) * NV : (r == lr ? bndv + (warp * 2 + 1) * NV
+                                                                 : acc + (size_t)r * NV);
+#pragma unroll
+      for (int t = 0; t < NV; ++t) dst[t] += v[t];
+    };
     for (long long e = ws; e < we; e += 128) {
-      // four chunks of the stream in flight before any use
+      const long long kb = e + 4 * lane;  // this lane's 4 contiguous entries
       unsigned p[4];
       double a[4];
+      if (kb + 3 < we) {
+        const uint4 pv = __ldcs(reinterpret_cast<const uint4*>(T.pk + kb));
+        p[0] = pv.x; p[1] = pv.y; p[2] = pv.z; p[3] = pv.w;
+        double d0, d1, d2, d3;
+        asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
+                     : "=d"(d0), "=d"(d1), "=d"(d2), "=d"(d3) : "l"(T.v + kb));
+        a[0] = d0; a[1] = d1; a[2] = d2; a[3] = d3;
+      } else {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const long long k = e + u * 32 + lane;
-        const bool ok = k < we;
-        p[u] = ok ? __ldcs(T.pk + k) : 0u;
-        a[u] = ok ? __ldcs(T.v + k) : 0.0;
+        for (int k = 0; k < 4; ++k) { p[k] = 0xffff0000u; a[k] = 0.0; }
       }
+      int r[4];
+      double x[4][NV];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (e + u * 32 >= we) break;  // warp-uniform
-        const bool ok = e + u * 32 + lane < we;
-        const int r = ok ? (int)(p[u] >> 16) - rel0 : -1 - lane;
-        const int c = (int)(p[u] & 0xffffu);
-        double x[NV];
+      for (int k = 0; k < 4; ++k) {
+        const unsigned rr = p[k] >> 16;
+        const bool ok = rr != 0xffffu;
+        r[k] = ok ? (int)rr - rel0 : -1 - (lane * 4 + k);  // padding: unique, never matches
+        const int c = (int)(p[k] & 0xffffu);
 #pragma unroll
-        for (int t = 0; t < NV; ++t) x[t] = ok ? a[u] * slab[c * NV + t] : 0.0;
-        // segmented inclusive scan over lanes of equal row (runs are contiguous)
+        for (int t = 0; t < NV; ++t) x[k][t] = ok ? a[k] * slab[c * NV + t] : 0.0;
+      }
+      // lane-local folding: head run, closed middle runs (emitted), tail run
+      double hs[NV], ts[NV];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int rp = __shfl_up_sync(0xffffffffu, r, o);
+      for (int t = 0; t < NV; ++t) hs[t] = x[0][t];
+      const int hr = r[0];
+      int k = 1;
 #pragma unroll
-          for (int t = 0; t < NV; ++t) {
-            const double xp = __shfl_up_sync(0xffffffffu, x[t], o);
-            if (lane >= o && rp == r) x[t] += xp;
+      for (int kk = 1; kk < 4; ++kk)
+        if (k == kk && r[kk] == hr) {
+#pragma unroll
+          for (int t = 0; t < NV; ++t) hs[t] += x[kk][t];
+          ++k;
+        }
+      const bool single = k == 4;
+      int tr = hr;
+#pragma unroll
+      for (int t = 0; t < NV; ++t) ts[t] = hs[t];
+      if (!single) {
+        tr = r[k];
+#pragma unroll
+        for (int t = 0; t < NV; ++t) ts[t] = 0.0;
+#pragma unroll
+        for (int kk = 1; kk < 4; ++kk) {
+          if (kk < k) continue;
+          if (r[kk] != tr) {  // run [.., kk) closed inside this lane
+            emit(tr, ts);
+            tr = r[kk];
+#pragma unroll
+            for (int t = 0; t < NV; ++t) ts[t] = 0.0;
           }
-        }
-        const int rn = __shfl_down_sync(0xffffffffu, r, 1);
-        if (ok && (lane == 31 || rn != r)) {
 #pragma unroll
-          for (int t = 0; t < NV; ++t) acc[r * NV + t] += x[t];
+          for (int t = 0; t < NV; ++t) ts[t] += x[kk][t];
         }
-        __syncwarp();
       }
+      // warp segmented scan of the tail runs: a single-run lane continues
+      // the previous lane's tail run when the rows match
+      const int ptr = __shfl_up_sync(0xffffffffu, tr, 1);
+      bool f = !single || lane == 0 || ptr != tr;
+      double v[NV];
+#pragma unroll
+      for (int t = 0; t < NV; ++t) v[t] = ts[t];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const bool fp = __shfl_up_sync(0xffffffffu, f, o);
+        double vp[NV];
+#pragma unroll
+        for (int t = 0; t < NV; ++t) vp[t] = __shfl_up_sync(0xffffffffu, v[t], o);
+        if (lane >= o && !f) {
+#pragma unroll
+          for (int t = 0; t < NV; ++t) v[t] += vp[t];
+          f = fp;
+        }
+      }
+      // head run of a multi-run lane closes with the carry of the lanes before
+      double carry[NV];
+#pragma unroll
+      for (int t = 0; t < NV; ++t) carry[t] = __shfl_up_sync(0xffffffffu, v[t], 1);
+      const int nhr = __shfl_down_sync(0xffffffffu, hr, 1);
+      if (!single) {
+        double tot[NV];
+#pragma unroll
+        for (int t = 0; t < NV; ++t) tot[t] = hs[t] + ((lane > 0 && ptr == hr) ? carry[t] : 0.0);
+        emit(hr, tot);
+      }
+      // tail run ends here unless the next lane starts with the same row
+      if (lane == 31 || nhr != tr) emit(tr, v);
+      __syncwarp();
     }
     __syncthreads();  // everyone is done with slab `cur` before it is refilled
+    if (tid == 0) {   // boundary rows, merged in warp order (deterministic)
+      for (int w = 0; w < nw; ++w) {
+        const int r1 = bndr[2 * w], r2 = bndr[2 * w + 1];
+        if (r1 >= 0)
+          for (int t = 0; t < NV; ++t) acc[(size_t)r1 * NV + t] += bndv[(2 * w) * NV + t];
+        if (r2 >= 0 && r2 != r1)
+          for (int t = 0; t < NV; ++t) acc[(size_t)r2 * NV + t] += bndv[(2 * w + 1) * NV + t];
+      }
+    }
+    __syncthreads();
     cur ^= 1;
     s = sn;
   }
@@ -258,15 +330,30 @@ __global__ void k_tile_keys(const int* rowid, const int* ci, long long nnz, int 
   }
 }
 
-__global__ void k_tile_pack(const int* perm, const int* rowid, const int* ci, const double* v,
-                            long long nnz, int RB, int W, unsigned* pk, double* tv) {
+// scatter sorted entry k into its 4-padded sub-tile position
+__global__ void k_tile_pack(const int* perm, const int* skey, const long long* ts_raw,
+                            const long long* ts_pad, const int* rowid, const int* ci,
+                            const double* v, long long nnz, int RB, int W, unsigned* pk,
+                            double* tv) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long k = tid; k < nnz; k += nt) {
     const int s = perm[k];
-    pk[k] = ((unsigned)(rowid[s] % RB) << 16) | (unsigned)(ci[s] % W);
-    tv[k] = v[s];
+    const int t = skey[k];
+    const long long pos = ts_pad[t] + (k - ts_raw[t]);
+    pk[pos] = ((unsigned)(rowid[s] % RB) << 16) | (unsigned)(ci[s] % W);
+    tv[pos] = v[s];
   }
+}
+__global__ void k_fill_pad(unsigned* pk, double* tv, long long n) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long k = tid; k < n; k += nt) { pk[k] = 0xffff0000u; tv[k] = 0.0; }
+}
+__global__ void k_pad4(const long long* ts_raw, long long ntile, long long* cnt) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long t = tid; t < ntile; t += nt) cnt[t] = (ts_raw[t + 1] - ts_raw[t] + 3) & ~3LL;
 }
 
 }  // namespace scs
