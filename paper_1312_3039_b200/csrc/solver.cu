@@ -931,7 +931,9 @@ void launch_mat(scs_handle* h, int mat, const Epi& epi) {
   constexpr int NV = Epi::NV, STRIDE = Epi::STRIDE;
   const Tiled& T = mat == 0 ? h->tA : h->tAt;
   const int sub = h->tsub[mat][NV], splits = h->tsplit[mat][NV];
-  const size_t smem = 2 * (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8;
+  const int splits_ = h->tsplit[mat][NV];
+  const size_t smem = 2 * (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8 +
+                      2 * (size_t)((T.S + splits_ - 1) / splits_ + 1);
   set_tiled_smem<NV, STRIDE, Epi>(smem);
   const int ctas = T.NB * sub * splits;
   k_tiled<NV, STRIDE, Epi><<<ctas, kTileThreads, smem, h->st>>>(T, epi, sub, splits, h->Ptile);
@@ -949,9 +951,10 @@ void tile_shapes(scs_handle* h, int mat, const Tiled& T, long long nnz) {
   for (int NV = 1; NV <= 2; ++NV) {
     double best = 1e300;
     for (int sub = 1; sub <= kTileNsub; sub *= 2) {
-      const size_t smem = 2 * (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8;
-      if (smem > 200 * 1024) continue;
       for (int splits = 1; splits <= 64 && splits <= T.S; splits *= 2) {
+        const size_t smem = 2 * (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8 +
+                            2 * (size_t)((T.S + splits - 1) / splits + 1);
+        if (smem > 200 * 1024) continue;
         const double ctas = (double)T.NB * sub * splits;
         const double stream = 12.0 * nnz + 8.0 * NV * T.rows;
         const double slabs = (double)T.NB * sub * T.cols * NV * 8.0;

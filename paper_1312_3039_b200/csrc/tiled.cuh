@@ -57,12 +57,85 @@ __device__ __forceinline__ void slab_issue(const double* __restrict__ xb, long l
   asm volatile("cp.async.commit_group;");
 }
 
-__device__ __forceinline__ int next_tile(const Tiled& T, long long tb0, int fsb, int s, int s_hi) {
-  for (; s < s_hi; ++s) {
-    const long long tb = tb0 + (long long)s * kTileNsub;
-    if (__ldg(T.ts + tb) != __ldg(T.ts + tb + fsb)) return s;
+// Ordered list of the non-empty tiles of this CTA's slab range, built in
+// parallel (ballot compaction + block prefix) into shared memory.
+__device__ __forceinline__ int tile_list(const Tiled& T, long long tb0, int fsb, int s_lo,
+                                         int s_hi, unsigned short* list, int* wcount) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  int total = 0;
+  for (int base = s_lo; base < s_hi; base += blockDim.x) {
+    const int s = base + tid;
+    bool ne = false;
+    if (s < s_hi) {
+      const long long tb = tb0 + (long long)s * kTileNsub;
+      ne = __ldg(T.ts + tb) != __ldg(T.ts + tb + fsb);
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, ne);
+    if (lane == 0) wcount[warp] = __popc(mask);
+    __syncthreads();
+    int before = 0, all = 0;
+    for (int w = 0; w < nw; ++w) {
+      const int cw = wcount[w];
+      if (w < warp) before += cw;
+      all += cw;
+    }
+    if (ne) list[total + before + __popc(mask & ((1u << lane) - 1))] = (unsigned short)(s - s_lo);
+    total += all;
+    __syncthreads();
   }
-  return s_hi;
+  return total;
+}
+
+// Boundary runs of the 32 warps (rows nondecreasing in warp order, equal
+// rows adjacent) folded into the accumulators by warp 0 with one segmented
+// scan: deterministic, no serial loop.
+template <int NV>
+__device__ __forceinline__ void merge_bounds(const int* bndr, const double* bndv, double* acc) {
+  const int lane = threadIdx.x & 31;
+  int r1 = bndr[2 * lane], r2 = bndr[2 * lane + 1];
+  double v1[NV], v2[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) { v1[t] = bndv[(2 * lane) * NV + t]; v2[t] = bndv[(2 * lane + 1) * NV + t]; }
+  if (r2 == r1) {  // one run: everything is in slot 1
+#pragma unroll
+    for (int t = 0; t < NV; ++t) v1[t] += v2[t];
+    r2 = -4;
+  }
+  // lane item = (head run r1, tail run r2 or r1)
+  const bool two = r2 >= 0;
+  const int tr = two ? r2 : r1;
+  double ts[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) ts[t] = two ? v2[t] : v1[t];
+  const int ptr = __shfl_up_sync(0xffffffffu, tr, 1);
+  bool f = two || lane == 0 || ptr != tr;
+  double v[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) v[t] = ts[t];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const bool fp = __shfl_up_sync(0xffffffffu, f, o);
+    double vp[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) vp[t] = __shfl_up_sync(0xffffffffu, v[t], o);
+    if (lane >= o && !f) {
+#pragma unroll
+      for (int t = 0; t < NV; ++t) v[t] += vp[t];
+      f = fp;
+    }
+  }
+  double carry[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) carry[t] = __shfl_up_sync(0xffffffffu, v[t], 1);
+  const int nhr = __shfl_down_sync(0xffffffffu, r1, 1);
+  if (two && r1 >= 0) {
+#pragma unroll
+    for (int t = 0; t < NV; ++t) acc[(size_t)r1 * NV + t] += v1[t] + ((lane > 0 && ptr == r1) ? carry[t] : 0.0);
+  }
+  if (tr >= 0 && (lane == 31 || nhr != tr)) {
+#pragma unroll
+    for (int t = 0; t < NV; ++t) acc[(size_t)tr * NV + t] += v[t];
+  }
 }
 
 template <int NV, int STRIDE, class Epi>
@@ -75,6 +148,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   double* acc = sm + 2 * (size_t)T.W * NV;  // rows of this CTA * NV
   __shared__ int bndr[2 * (kTileThreads / 32)];
   __shared__ double bndv[2 * (kTileThreads / 32) * NV];
+  __shared__ int wcount[kTileThreads / 32];
+  unsigned short* tlist = reinterpret_cast<unsigned short*>(acc + (size_t)(T.RB / sub) * NV);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int sp = blockIdx.x % splits;
   const int rest = blockIdx.x / splits;
@@ -93,11 +168,14 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const int wc = (int)((T.cols - c0) < T.W ? (T.cols - c0) : T.W);
     slab_issue<NV, STRIDE>(epi.xb, c0, wc, dst);
   };
-  int s = next_tile(T, tb0, fsb, s_lo, s_hi);
+  const int ntl = tile_list(T, tb0, fsb, s_lo, s_hi, tlist, wcount);
+  int li = 0;
+  int s = ntl > 0 ? s_lo + tlist[0] : s_hi;
   if (s < s_hi) slab_of(s, slabs);
   int cur = 0;
   while (s < s_hi) {
-    const int sn = next_tile(T, tb0, fsb, s + 1, s_hi);
+    ++li;
+    const int sn = li < ntl ? s_lo + tlist[li] : s_hi;
     if (sn < s_hi) {
       slab_of(sn, slabs + (size_t)(cur ^ 1) * T.W * NV);
       asm volatile("cp.async.wait_group 1;");
@@ -227,15 +305,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       __syncwarp();
     }
     __syncthreads();  // everyone is done with slab `cur` before it is refilled
-    if (tid == 0) {   // boundary rows, merged in warp order (deterministic)
-      for (int w = 0; w < nw; ++w) {
-        const int r1 = bndr[2 * w], r2 = bndr[2 * w + 1];
-        if (r1 >= 0)
-          for (int t = 0; t < NV; ++t) acc[(size_t)r1 * NV + t] += bndv[(2 * w) * NV + t];
-        if (r2 >= 0 && r2 != r1)
-          for (int t = 0; t < NV; ++t) acc[(size_t)r2 * NV + t] += bndv[(2 * w + 1) * NV + t];
-      }
-    }
+    if (warp == 0) merge_bounds<NV>(bndr, bndv, acc);  // warp-order fold of shared rows
     __syncthreads();
     cur ^= 1;
     s = sn;
