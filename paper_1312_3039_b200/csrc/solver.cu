@@ -909,14 +909,18 @@ void launch_spmv(scs_handle* h, const Csr& M, int L, const Epi& epi) {
   h->launches++;
 }
 
+// Opt the tiled kernel into the device's full dynamic shared memory once
+// (a per-launch, size-dependent setting would race between handles).
 template <int NV, int STRIDE, class Epi>
-void set_tiled_smem(size_t bytes) {
-  static size_t done = 0;
-  if (bytes > 48 * 1024 && bytes > done) {
-    CK(cudaFuncSetAttribute(k_tiled<NV, STRIDE, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)bytes));
-    done = bytes;
-  }
+void set_tiled_smem(int dev, size_t bytes) {
+  static std::once_flag once;
+  static int optin = 0;
+  std::call_once(once, [&] {
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(k_tiled<NV, STRIDE, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         optin);
+  });
+  if (bytes > (size_t)optin) throw Fail{SCS_EINVAL, "tiled SpMV: shared memory budget exceeded"};
 }
 
 // SpMV with the matrix A (mat = 0) or A^T (mat = 1): slab-tiled kernel when
@@ -934,9 +938,10 @@ void launch_mat(scs_handle* h, int mat, const Epi& epi) {
   const int splits_ = h->tsplit[mat][NV];
   const size_t smem = 2 * (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8 +
                       2 * (size_t)((T.S + splits_ - 1) / splits_ + 1);
-  set_tiled_smem<NV, STRIDE, Epi>(smem);
+  set_tiled_smem<NV, STRIDE, Epi>(h->dev, smem);
   const int ctas = T.NB * sub * splits;
   k_tiled<NV, STRIDE, Epi><<<ctas, kTileThreads, smem, h->st>>>(T, epi, sub, splits, h->Ptile);
+  CK(cudaPeekAtLastError());
   h->launches++;
   if (splits > 1) {
     k_tiled_combine<Epi><<<elem_grid(h, T.rows), kBlock, 0, h->st>>>(h->Ptile, splits, T.rows, epi);
