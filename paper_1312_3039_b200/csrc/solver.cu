@@ -916,9 +916,15 @@ void set_tiled_smem(int dev, size_t bytes) {
   static std::once_flag once;
   static int optin = 0;
   std::call_once(once, [&] {
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncSetAttribute(k_tiled<NV, STRIDE, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         optin);
+    int dev_optin = 0;
+    cudaDeviceGetAttribute(&dev_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_tiled<NV, STRIDE, Epi>);
+    optin = dev_optin - (int)fa.sharedSizeBytes;  // dynamic = opt-in minus static
+    if (cudaFuncSetAttribute(k_tiled<NV, STRIDE, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin) != cudaSuccess)
+      optin = 48 * 1024 - (int)fa.sharedSizeBytes;
+    cudaGetLastError();
   });
   if (bytes > (size_t)optin) throw Fail{SCS_EINVAL, "tiled SpMV: shared memory budget exceeded"};
 }
@@ -941,7 +947,7 @@ void launch_mat(scs_handle* h, int mat, const Epi& epi) {
   set_tiled_smem<NV, STRIDE, Epi>(h->dev, smem);
   const int ctas = T.NB * sub * splits;
   k_tiled<NV, STRIDE, Epi><<<ctas, kTileThreads, smem, h->st>>>(T, epi, sub, splits, h->Ptile);
-  CK(cudaPeekAtLastError());
+  CK(cudaGetLastError());
   h->launches++;
   if (splits > 1) {
     k_tiled_combine<Epi><<<elem_grid(h, T.rows), kBlock, 0, h->st>>>(h->Ptile, splits, T.rows, epi);
