@@ -188,8 +188,12 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const long long e0 = __ldg(T.ts + tb), e1 = __ldg(T.ts + tb + fsb);
     // warp w owns the 4-aligned entry run [ws, we) of the (4-padded) tile;
     // rows it shares with neighbouring warps go to its boundary slots
+    // (only min(nw, groups) warps take work, so no empty range sits between
+    // two warps that share a row -- the merge scan relies on that)
     const long long q4 = (e1 - e0) >> 2;
-    const long long ws = e0 + 4 * (q4 * warp / nw), we = e0 + 4 * (q4 * (warp + 1) / nw);
+    const long long na = q4 < nw ? q4 : nw;
+    const long long ws = warp < na ? e0 + 4 * (q4 * warp / na) : e1;
+    const long long we = warp < na ? e0 + 4 * (q4 * (warp + 1) / na) : e1;
     int fr = -2, lr = -3;
     if (we > ws) {
       const unsigned pf = __ldg(T.pk + ws) >> 16, pl = __ldg(T.pk + we - 1) >> 16;
