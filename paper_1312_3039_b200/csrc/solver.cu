@@ -983,14 +983,35 @@ void tile_shapes(scs_handle* h, int mat, const Tiled& T, long long nnz) {
   }
 }
 
-// Re-lay a CSR matrix out as slab tiles (stable device radix sort on the
-// tile key keeps the row-major order inside each tile).
-void build_tiled(scs_handle* h, const Csr& M, long long cols, Tiled& T) {
-  const long long rows = M.rows, nnz = M.rp ? 0 : 0;
-  (void)nnz;
-  long long nz = 0;
-  CK(cudaMemcpyAsync(&nz, M.rp + rows, sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+template <class T>
+void exclusive_scan(scs_handle* h, const T* in, T* out, long long n) {
+  size_t bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n, h->st));
+  void* tmp = dalloc<char>(h, bytes);
+  CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, (int)n, h->st));
   CK(cudaStreamSynchronize(h->st));
+  dfree(h, tmp);
+}
+template <class T>
+T read_dev(scs_handle* h, const T* p) {
+  T v{};
+  CK(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return v;
+}
+__global__ void k_key_hi(const unsigned long long* k2, long long n, int* out) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) out[i] = (int)(k2[i] >> 20);
+}
+
+// Re-lay a CSR matrix out as slab tiles with SELL-style sub-tiles
+// (tiled.cuh): entries sorted by sub-tile (stable radix sort keeps the
+// row-major order), row segments found, segments sorted by (sub-tile,
+// length desc), grouped 32 per chunk and scattered column-interleaved.
+void build_tiled(scs_handle* h, const Csr& M, long long cols, Tiled& T) {
+  const long long rows = M.rows;
+  const long long nz = read_dev(h, M.rp + rows);
   T.rows = rows;
   T.cols = cols;
   T.RB = 16384;
@@ -998,7 +1019,9 @@ void build_tiled(scs_handle* h, const Csr& M, long long cols, Tiled& T) {
   T.S = (int)((cols + T.W - 1) / T.W);
   T.NB = (int)((rows + T.RB - 1) / T.RB);
   const long long ntile = (long long)T.NB * T.S * kTileNsub;
-  if (ntile >= (1LL << 31) - 1) throw Fail{SCS_EINVAL, "too many tiles"};
+  if (ntile >= (1LL << 31) - 1 || nz >= (1LL << 31) - 1)
+    throw Fail{SCS_EINVAL, "tiled layout: too many tiles or nonzeros"};
+  // 1. entries by sub-tile
   int* rowid = dalloc<int>(h, nz);
   int* key = dalloc<int>(h, nz);
   int* skey = dalloc<int>(h, nz);
@@ -1009,39 +1032,100 @@ void build_tiled(scs_handle* h, const Csr& M, long long cols, Tiled& T) {
   k_iota<<<elem_grid(h, nz), kBlock, 0, h->st>>>(perm_in, nz);
   int bits = 1;
   while ((1LL << bits) < ntile) ++bits;
-  size_t tmp_bytes = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const int*)key, skey,
-                                     (const int*)perm_in, perm, (int)nz, 0, bits, h->st));
-  void* tmp = dalloc<char>(h, tmp_bytes);
-  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, (const int*)key, skey, (const int*)perm_in,
-                                     perm, (int)nz, 0, bits, h->st));
-  // sub-tile starts, each sub-tile padded to a multiple of 4 entries so a
-  // lane's 4 entries are one 16-B index load and one 32-B value load
-  long long* ts_raw = dalloc<long long>(h, ntile + 1);
-  long long* cnt = dalloc<long long>(h, ntile + 1);
-  long long* ts = dalloc<long long>(h, ntile + 1);
-  k_rowptr<<<elem_grid(h, ntile + 1), kBlock, 0, h->st>>>(skey, nz, ntile, ts_raw);
-  k_pad4<<<elem_grid(h, ntile), kBlock, 0, h->st>>>(ts_raw, ntile, cnt);
-  CK(cudaMemsetAsync(cnt + ntile, 0, sizeof(long long), h->st));
-  size_t scan_bytes = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt, ts, (int)(ntile + 1), h->st));
-  void* scan_tmp = dalloc<char>(h, scan_bytes);
-  CK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, cnt, ts, (int)(ntile + 1), h->st));
-  long long npad = 0;
-  CK(cudaMemcpyAsync(&npad, ts + ntile, sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+  {
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const int*)key, skey, (const int*)perm_in, perm,
+                                       (int)nz, 0, bits, h->st));
+    void* tmp = dalloc<char>(h, tb);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, (const int*)key, skey, (const int*)perm_in, perm,
+                                       (int)nz, 0, bits, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    dfree(h, tmp);
+  }
+  dfree(h, key);
+  // 2. row segments
+  int* flag = perm_in;  // reuse
+  int* incl = dalloc<int>(h, nz);
+  k_seg_flags<<<elem_grid(h, nz), kBlock, 0, h->st>>>(skey, perm, rowid, nz, flag);
+  {
+    size_t tb = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flag, incl, (int)nz, h->st));
+    void* tmp = dalloc<char>(h, tb);
+    CK(cub::DeviceScan::InclusiveSum(tmp, tb, flag, incl, (int)nz, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    dfree(h, tmp);
+  }
+  const long long nseg = read_dev(h, incl + nz - 1);
+  long long* seg_start = dalloc<long long>(h, nseg);
+  k_seg_starts<<<elem_grid(h, nz), kBlock, 0, h->st>>>(flag, incl, nz, seg_start);
+  dfree(h, incl);
+  // 3. segments by (sub-tile, length desc)
+  unsigned long long* key2 = dalloc<unsigned long long>(h, nseg);
+  unsigned long long* key2s = dalloc<unsigned long long>(h, nseg);
+  int* tile_of = dalloc<int>(h, nseg);
+  int* sidx = dalloc<int>(h, nseg);
+  int* order = dalloc<int>(h, nseg);
+  k_seg_keys<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(seg_start, nseg, nz, skey, key2, tile_of);
+  k_iota<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(sidx, nseg);
+  {
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned long long*)key2, key2s,
+                                       (const int*)sidx, order, (int)nseg, 0, 20 + bits, h->st));
+    void* tmp = dalloc<char>(h, tb);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, (const unsigned long long*)key2, key2s,
+                                       (const int*)sidx, order, (int)nseg, 0, 20 + bits, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    dfree(h, tmp);
+  }
+  int* tile_sorted = tile_of;  // reuse
+  k_key_hi<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(key2s, nseg, tile_sorted);
+  dfree(h, key2);
+  dfree(h, key2s);
+  dfree(h, sidx);
+  // 4. chunks
+  long long* tss = dalloc<long long>(h, ntile + 1);
+  long long* nch = dalloc<long long>(h, ntile + 1);
+  long long* cs = dalloc<long long>(h, ntile + 1);
+  k_rowptr<<<elem_grid(h, ntile + 1), kBlock, 0, h->st>>>(tile_sorted, nseg, ntile, tss);
+  k_tile_chunks<<<elem_grid(h, ntile), kBlock, 0, h->st>>>(tss, ntile, nch);
+  CK(cudaMemsetAsync(nch + ntile, 0, sizeof(long long), h->st));
+  exclusive_scan(h, nch, cs, ntile + 1);
+  const long long nchunk = read_dev(h, cs + ntile);
+  long long* csz = dalloc<long long>(h, nchunk + 1);
+  long long* co = dalloc<long long>(h, nchunk + 1);
+  k_chunk_sizes<<<elem_grid(h, ntile), kBlock, 0, h->st>>>(tss, cs, ntile, order, seg_start, nseg,
+                                                            nz, csz);
+  CK(cudaMemsetAsync(csz + nchunk, 0, sizeof(long long), h->st));
+  exclusive_scan(h, csz, co, nchunk + 1);
+  const long long nent = read_dev(h, co + nchunk);
+  // 5. scatter
+  unsigned short* rid = dalloc<unsigned short>(h, nchunk * 32);
+  unsigned short* col = dalloc<unsigned short>(h, nent);
+  double* tv = dalloc<double>(h, nent);
+  k_fill_u16<<<elem_grid(h, nchunk * 32), kBlock, 0, h->st>>>(rid, nchunk * 32, 0xffff);
+  k_fill_u16<<<elem_grid(h, nent), kBlock, 0, h->st>>>(col, nent, 0);
+  CK(cudaMemsetAsync(tv, 0, std::max<long long>(nent, 1) * sizeof(double), h->st));
+  k_sell_scatter<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(tss, cs, co, order, tile_sorted, seg_start,
+                                                           nseg, nz, perm, rowid, M.ci, M.v, T.RB,
+                                                           T.W, rid, col, tv);
   CK(cudaStreamSynchronize(h->st));
-  unsigned* pk = dalloc<unsigned>(h, npad);
-  double* tv = dalloc<double>(h, npad);
-  k_fill_pad<<<elem_grid(h, npad), kBlock, 0, h->st>>>(pk, tv, npad);
-  k_tile_pack<<<elem_grid(h, nz), kBlock, 0, h->st>>>(perm, skey, ts_raw, ts, rowid, M.ci, M.v, nz,
-                                                       T.RB, T.W, pk, tv);
-  CK(cudaStreamSynchronize(h->st));
-  dfree(h, scan_tmp);
-  dfree(h, cnt);
-  dfree(h, ts_raw);
-  T.ts = ts;
-  T.pk = pk;
+  dfree(h, csz);
+  dfree(h, nch);
+  dfree(h, tss);
+  dfree(h, order);
+  dfree(h, tile_sorted);
+  dfree(h, seg_start);
+  dfree(h, perm_in);
+  dfree(h, perm);
+  dfree(h, skey);
+  dfree(h, rowid);
+  T.cs = cs;
+  T.co = co;
+  T.rid = rid;
+  T.col = col;
   T.v = tv;
+  dbg("tiled layout rows=%lld cols=%lld nnz=%lld segments=%lld chunks=%lld entries=%lld (pad %.1f%%)",
+      rows, cols, nz, nseg, nchunk, nent, nz ? 100.0 * (nent - nz) / nz : 0.0);
 }
 
 void setup_tiled(scs_handle* h) {

@@ -6,18 +6,21 @@
 // removes the gathers from the memory system:
 //
 //  * the matrix is re-laid out once (after equilibration) into tiles
-//    (row block of RB rows) x (column slab of W columns); a tile's entries
-//    are contiguous, in row-major order, each stored as a packed
-//    (row - block start, col - slab start) pair of 16-bit offsets plus the
-//    fp64 value: 12 bytes per nonzero, as CSR;
-//  * a CTA owns a row block (or a quarter of one) and walks the column
-//    slabs of its range: it stages the slab of the gather vector in shared
-//    memory with coalesced loads (L2 traffic ~ |x| per row block instead of
-//    32 B per nonzero), then each warp streams a row-aligned, contiguous run
-//    of the tile's entries, gathers from shared memory, and folds the
-//    products into per-row shared accumulators with a warp segmented scan
-//    (rows are contiguous runs, so each row's partial sums are combined in
-//    a fixed order: the result is deterministic);
+//    (row block of RB rows) x (column slab of W columns), each split into
+//    kTileNsub row sub-tiles.  Inside a sub-tile the row segments are
+//    sorted by length and grouped 32 to a chunk (SELL-C-sigma with C = 32,
+//    sigma = the sub-tile); a chunk stores its entries column-interleaved
+//    (step k of all 32 lanes contiguous): fp64 value + 16-bit column
+//    offset, 10 bytes per nonzero, plus one 16-bit row id per lane;
+//  * a CTA owns a row block (or part of one) and walks the column slabs of
+//    its range: it stages the slab of the gather vector in shared memory
+//    with cp.async (double-buffered; L2 traffic ~ |x| per row block instead
+//    of 32 B per nonzero); each lane then sums one row segment in registers
+//    -- coalesced 256 B value / 64 B column loads per step, gathers from
+//    shared memory, no shuffles -- and adds it to its row's shared
+//    accumulator (each row has one segment per sub-tile, so the update is
+//    exclusive and the order of a row's partial sums is fixed: the result
+//    is deterministic);
 //  * after the last slab the CTA runs the same per-row epilogue (Epi::row)
 //    as the CSR kernel, coalesced, or -- when the slab range is split over
 //    several CTAs to fill the GPU -- writes per-split partial rows that
@@ -35,9 +38,11 @@ constexpr int kTileNsub = 4;  // row sub-blocks per format row block
 struct Tiled {
   long long rows, cols;
   int RB, W, S, NB;             // rows per block, columns per slab, #slabs, #blocks
-  const long long* ts;          // (NB * S) * kTileNsub + 1 sub-tile starts
-  const unsigned* pk;           // (row_rel << 16) | col_rel
-  const double* v;
+  const long long* cs;          // (NB * S) * kTileNsub + 1: first chunk of each sub-tile
+  const long long* co;          // nchunk + 1: first entry of each chunk (32 * width each)
+  const unsigned short* rid;    // 32 per chunk: row - block start, 0xffff = idle lane
+  const unsigned short* col;    // per entry: column - slab start
+  const double* v;              // per entry value (0 for padding)
 };
 
 // async copy of one gather-vector slab (NV values per column) into smem
@@ -68,7 +73,7 @@ __device__ __forceinline__ int tile_list(const Tiled& T, long long tb0, int fsb,
     bool ne = false;
     if (s < s_hi) {
       const long long tb = tb0 + (long long)s * kTileNsub;
-      ne = __ldg(T.ts + tb) != __ldg(T.ts + tb + fsb);
+      ne = __ldg(T.cs + tb) != __ldg(T.cs + tb + fsb);
     }
     const unsigned mask = __ballot_sync(0xffffffffu, ne);
     if (lane == 0) wcount[warp] = __popc(mask);
@@ -86,58 +91,6 @@ __device__ __forceinline__ int tile_list(const Tiled& T, long long tb0, int fsb,
   return total;
 }
 
-// Boundary runs of the 32 warps (rows nondecreasing in warp order, equal
-// rows adjacent) folded into the accumulators by warp 0 with one segmented
-// scan: deterministic, no serial loop.
-template <int NV>
-__device__ __forceinline__ void merge_bounds(const int* bndr, const double* bndv, double* acc) {
-  const int lane = threadIdx.x & 31;
-  int r1 = bndr[2 * lane], r2 = bndr[2 * lane + 1];
-  double v1[NV], v2[NV];
-#pragma unroll
-  for (int t = 0; t < NV; ++t) { v1[t] = bndv[(2 * lane) * NV + t]; v2[t] = bndv[(2 * lane + 1) * NV + t]; }
-  if (r2 == r1) {  // one run: everything is in slot 1
-#pragma unroll
-    for (int t = 0; t < NV; ++t) v1[t] += v2[t];
-    r2 = -4;
-  }
-  // lane item = (head run r1, tail run r2 or r1)
-  const bool two = r2 >= 0;
-  const int tr = two ? r2 : r1;
-  double ts[NV];
-#pragma unroll
-  for (int t = 0; t < NV; ++t) ts[t] = two ? v2[t] : v1[t];
-  const int ptr = __shfl_up_sync(0xffffffffu, tr, 1);
-  bool f = two || lane == 0 || ptr != tr;
-  double v[NV];
-#pragma unroll
-  for (int t = 0; t < NV; ++t) v[t] = ts[t];
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const bool fp = __shfl_up_sync(0xffffffffu, f, o);
-    double vp[NV];
-#pragma unroll
-    for (int t = 0; t < NV; ++t) vp[t] = __shfl_up_sync(0xffffffffu, v[t], o);
-    if (lane >= o && !f) {
-#pragma unroll
-      for (int t = 0; t < NV; ++t) v[t] += vp[t];
-      f = fp;
-    }
-  }
-  double carry[NV];
-#pragma unroll
-  for (int t = 0; t < NV; ++t) carry[t] = __shfl_up_sync(0xffffffffu, v[t], 1);
-  const int nhr = __shfl_down_sync(0xffffffffu, r1, 1);
-  if (two && r1 >= 0) {
-#pragma unroll
-    for (int t = 0; t < NV; ++t) acc[(size_t)r1 * NV + t] += v1[t] + ((lane > 0 && ptr == r1) ? carry[t] : 0.0);
-  }
-  if (tr >= 0 && (lane == 31 || nhr != tr)) {
-#pragma unroll
-    for (int t = 0; t < NV; ++t) acc[(size_t)tr * NV + t] += v[t];
-  }
-}
-
 template <int NV, int STRIDE, class Epi>
 __global__ void __launch_bounds__(kTileThreads, 1)
     k_tiled(Tiled T, Epi epi0, int sub, int splits, double* P) {
@@ -146,8 +99,6 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   extern __shared__ double sm[];
   double* slabs = sm;                       // 2 x W * NV (double buffer)
   double* acc = sm + 2 * (size_t)T.W * NV;  // rows of this CTA * NV
-  __shared__ int bndr[2 * (kTileThreads / 32)];
-  __shared__ double bndv[2 * (kTileThreads / 32) * NV];
   __shared__ int wcount[kTileThreads / 32];
   unsigned short* tlist = reinterpret_cast<unsigned short*>(acc + (size_t)(T.RB / sub) * NV);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -185,132 +136,40 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     __syncthreads();  // slab s visible to the whole CTA
     const double* slab = slabs + (size_t)cur * T.W * NV;
     const long long tb = tb0 + (long long)s * kTileNsub;
-    const long long e0 = __ldg(T.ts + tb), e1 = __ldg(T.ts + tb + fsb);
-    // warp w owns the 4-aligned entry run [ws, we) of the (4-padded) tile;
-    // rows it shares with neighbouring warps go to its boundary slots
-    // (only min(nw, groups) warps take work, so no empty range sits between
-    // two warps that share a row -- the merge scan relies on that)
-    const long long q4 = (e1 - e0) >> 2;
-    const long long na = q4 < nw ? q4 : nw;
-    const long long ws = warp < na ? e0 + 4 * (q4 * warp / na) : e1;
-    const long long we = warp < na ? e0 + 4 * (q4 * (warp + 1) / na) : e1;
-    int fr = -2, lr = -3;
-    if (we > ws) {
-      const unsigned pf = __ldg(T.pk + ws) >> 16, pl = __ldg(T.pk + we - 1) >> 16;
-      fr = pf == 0xffffu ? -2 : (int)pf - rel0;
-      lr = pl == 0xffffu ? -3 : (int)pl - rel0;
-    }
-    if (lane == 0) {
-      bndr[warp * 2] = fr;
-      bndr[warp * 2 + 1] = lr;
+    const long long c_lo = __ldg(T.cs + tb), c_hi = __ldg(T.cs + tb + fsb);
+    for (long long ch = c_lo + warp; ch < c_hi; ch += nw) {
+      const long long off = __ldg(T.co + ch);
+      const int wid = (int)((__ldg(T.co + ch + 1) - off) >> 5);
+      const unsigned rr = __ldg(T.rid + ch * 32 + lane);
+      const double* vp = T.v + off + lane;
+      const unsigned short* cp = T.col + off + lane;
+      double sum[NV];
 #pragma unroll
-      for (int t = 0; t < NV; ++t) { bndv[(warp * 2) * NV + t] = 0.0; bndv[(warp * 2 + 1) * NV + t] = 0.0; }
-    }
-    __syncwarp();
-    auto emit = [&](int r, const double* v) {
-      if (r < 0) return;
-      double* dst = r == fr ? bndv + (warp * 2) * NV : (r == lr ? bndv + (warp * 2 + 1) * NV
-                                                                 : acc + (size_t)r * NV);
+      for (int t = 0; t < NV; ++t) sum[t] = 0.0;
+      int k = 0;
+      for (; k + 4 <= wid; k += 4) {  // four steps of the chunk in flight
+        double a[4];
+        int c[4];
 #pragma unroll
-      for (int t = 0; t < NV; ++t) dst[t] += v[t];
-    };
-    for (long long e = ws; e < we; e += 128) {
-      const long long kb = e + 4 * lane;  // this lane's 4 contiguous entries
-      unsigned p[4];
-      double a[4];
-      if (kb + 3 < we) {
-        const uint4 pv = __ldcs(reinterpret_cast<const uint4*>(T.pk + kb));
-        p[0] = pv.x; p[1] = pv.y; p[2] = pv.z; p[3] = pv.w;
-        double d0, d1, d2, d3;
-        asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
-                     : "=d"(d0), "=d"(d1), "=d"(d2), "=d"(d3) : "l"(T.v + kb));
-        a[0] = d0; a[1] = d1; a[2] = d2; a[3] = d3;
-      } else {
+        for (int u = 0; u < 4; ++u) { a[u] = __ldcs(vp + (k + u) * 32); c[u] = __ldcs(cp + (k + u) * 32); }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) { p[k] = 0xffff0000u; a[k] = 0.0; }
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int t = 0; t < NV; ++t) sum[t] = fma(a[u], slab[c[u] * NV + t], sum[t]);
       }
-      int r[4];
-      double x[4][NV];
+      for (; k < wid; ++k) {
+        const double a = __ldcs(vp + k * 32);
+        const int c = __ldcs(cp + k * 32);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const unsigned rr = p[k] >> 16;
-        const bool ok = rr != 0xffffu;
-        r[k] = ok ? (int)rr - rel0 : -1 - (lane * 4 + k);  // padding: unique, never matches
-        const int c = (int)(p[k] & 0xffffu);
-#pragma unroll
-        for (int t = 0; t < NV; ++t) x[k][t] = ok ? a[k] * slab[c * NV + t] : 0.0;
+        for (int t = 0; t < NV; ++t) sum[t] = fma(a, slab[c * NV + t], sum[t]);
       }
-      // lane-local folding: head run, closed middle runs (emitted), tail run
-      double hs[NV], ts[NV];
+      if (rr != 0xffffu) {
+        const int r = (int)rr - rel0;  // one segment per row per sub-tile: exclusive
 #pragma unroll
-      for (int t = 0; t < NV; ++t) hs[t] = x[0][t];
-      const int hr = r[0];
-      int k = 1;
-#pragma unroll
-      for (int kk = 1; kk < 4; ++kk)
-        if (k == kk && r[kk] == hr) {
-#pragma unroll
-          for (int t = 0; t < NV; ++t) hs[t] += x[kk][t];
-          ++k;
-        }
-      const bool single = k == 4;
-      int tr = hr;
-#pragma unroll
-      for (int t = 0; t < NV; ++t) ts[t] = hs[t];
-      if (!single) {
-        tr = r[k];
-#pragma unroll
-        for (int t = 0; t < NV; ++t) ts[t] = 0.0;
-#pragma unroll
-        for (int kk = 1; kk < 4; ++kk) {
-          if (kk < k) continue;
-          if (r[kk] != tr) {  // run [.., kk) closed inside this lane
-            emit(tr, ts);
-            tr = r[kk];
-#pragma unroll
-            for (int t = 0; t < NV; ++t) ts[t] = 0.0;
-          }
-#pragma unroll
-          for (int t = 0; t < NV; ++t) ts[t] += x[kk][t];
-        }
+        for (int t = 0; t < NV; ++t) acc[(size_t)r * NV + t] += sum[t];
       }
-      // warp segmented scan of the tail runs: a single-run lane continues
-      // the previous lane's tail run when the rows match
-      const int ptr = __shfl_up_sync(0xffffffffu, tr, 1);
-      bool f = !single || lane == 0 || ptr != tr;
-      double v[NV];
-#pragma unroll
-      for (int t = 0; t < NV; ++t) v[t] = ts[t];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const bool fp = __shfl_up_sync(0xffffffffu, f, o);
-        double vp[NV];
-#pragma unroll
-        for (int t = 0; t < NV; ++t) vp[t] = __shfl_up_sync(0xffffffffu, v[t], o);
-        if (lane >= o && !f) {
-#pragma unroll
-          for (int t = 0; t < NV; ++t) v[t] += vp[t];
-          f = fp;
-        }
-      }
-      // head run of a multi-run lane closes with the carry of the lanes before
-      double carry[NV];
-#pragma unroll
-      for (int t = 0; t < NV; ++t) carry[t] = __shfl_up_sync(0xffffffffu, v[t], 1);
-      const int nhr = __shfl_down_sync(0xffffffffu, hr, 1);
-      if (!single) {
-        double tot[NV];
-#pragma unroll
-        for (int t = 0; t < NV; ++t) tot[t] = hs[t] + ((lane > 0 && ptr == hr) ? carry[t] : 0.0);
-        emit(hr, tot);
-      }
-      // tail run ends here unless the next lane starts with the same row
-      if (lane == 31 || nhr != tr) emit(tr, v);
-      __syncwarp();
     }
     __syncthreads();  // everyone is done with slab `cur` before it is refilled
-    if (warp == 0) merge_bounds<NV>(bndr, bndv, acc);  // warp-order fold of shared rows
-    __syncthreads();
     cur ^= 1;
     s = sn;
   }
@@ -404,30 +263,83 @@ __global__ void k_tile_keys(const int* rowid, const int* ci, long long nnz, int 
   }
 }
 
-// scatter sorted entry k into its 4-padded sub-tile position
-__global__ void k_tile_pack(const int* perm, const int* skey, const long long* ts_raw,
-                            const long long* ts_pad, const int* rowid, const int* ci,
-                            const double* v, long long nnz, int RB, int W, unsigned* pk,
-                            double* tv) {
+// --- SELL-style sub-tile layout ---------------------------------------------
+// entries are already sorted by sub-tile (stable: row-major inside)
+__global__ void k_seg_flags(const int* skey, const int* perm, const int* rowid, long long nnz,
+                            int* flag) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
-  for (long long k = tid; k < nnz; k += nt) {
-    const int s = perm[k];
-    const int t = skey[k];
-    const long long pos = ts_pad[t] + (k - ts_raw[t]);
-    pk[pos] = ((unsigned)(rowid[s] % RB) << 16) | (unsigned)(ci[s] % W);
-    tv[pos] = v[s];
+  for (long long k = tid; k < nnz; k += nt)
+    flag[k] = (k == 0 || skey[k] != skey[k - 1] || rowid[perm[k]] != rowid[perm[k - 1]]) ? 1 : 0;
+}
+// seg_start[seg] = first entry of each row segment (flag prefix sum = seg + 1)
+__global__ void k_seg_starts(const int* flag, const int* incl, long long nnz, long long* seg_start) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long k = tid; k < nnz; k += nt)
+    if (flag[k]) seg_start[incl[k] - 1] = k;
+}
+// sort key of a segment: (sub-tile, length descending)
+__global__ void k_seg_keys(const long long* seg_start, long long nseg, long long nnz,
+                           const int* skey, unsigned long long* key2, int* tile_of) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long q = tid; q < nseg; q += nt) {
+    const long long a = seg_start[q], b = q + 1 < nseg ? seg_start[q + 1] : nnz;
+    const int t = skey[a];
+    tile_of[q] = t;
+    key2[q] = ((unsigned long long)t << 20) | (unsigned long long)((1 << 20) - 1 - (b - a));
   }
 }
-__global__ void k_fill_pad(unsigned* pk, double* tv, long long n) {
+// chunks per sub-tile from the (sorted) segment counts
+__global__ void k_tile_chunks(const long long* tss, long long ntile, long long* nch) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
-  for (long long k = tid; k < n; k += nt) { pk[k] = 0xffff0000u; tv[k] = 0.0; }
+  for (long long t = tid; t < ntile; t += nt) nch[t] = (tss[t + 1] - tss[t] + 31) / 32;
 }
-__global__ void k_pad4(const long long* ts_raw, long long ntile, long long* cnt) {
+// entries per chunk = 32 * length of its first (longest) segment
+__global__ void k_chunk_sizes(const long long* tss, const long long* cs, long long ntile,
+                              const int* order, const long long* seg_start, long long nseg,
+                              long long nnz, long long* csz) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
-  for (long long t = tid; t < ntile; t += nt) cnt[t] = (ts_raw[t + 1] - ts_raw[t] + 3) & ~3LL;
+  for (long long t = tid; t < ntile; t += nt) {
+    for (long long c = cs[t]; c < cs[t + 1]; ++c) {
+      const long long p = tss[t] + (c - cs[t]) * 32;
+      const long long q = order[p];
+      const long long len = (q + 1 < nseg ? seg_start[q + 1] : nnz) - seg_start[q];
+      csz[c] = 32 * len;
+    }
+  }
+}
+__global__ void k_sell_scatter(const long long* tss, const long long* cs, const long long* co,
+                               const int* order, const int* tile_sorted,
+                               const long long* seg_start, long long nseg, long long nnz,
+                               const int* perm, const int* rowid, const int* ci, const double* v,
+                               int RB, int W, unsigned short* rid, unsigned short* col,
+                               double* tv) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long p = tid; p < nseg; p += nt) {
+    const int t = tile_sorted[p];
+    const long long pos = p - tss[t];
+    const long long c = cs[t] + pos / 32;
+    const int lane = (int)(pos % 32);
+    const long long q = order[p];
+    const long long a = seg_start[q], b = q + 1 < nseg ? seg_start[q + 1] : nnz;
+    rid[c * 32 + lane] = (unsigned short)(rowid[perm[a]] % RB);
+    const long long base = co[c] + lane;
+    for (long long e = a; e < b; ++e) {
+      const int s = perm[e];
+      col[base + (e - a) * 32] = (unsigned short)(ci[s] % W);
+      tv[base + (e - a) * 32] = v[s];
+    }
+  }
+}
+__global__ void k_fill_u16(unsigned short* x, long long n, unsigned short val) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) x[i] = val;
 }
 
 }  // namespace scs
