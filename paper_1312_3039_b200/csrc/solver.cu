@@ -796,7 +796,7 @@ struct scs_handle {
   Csr A{}, At{};
   int LA = 32, LAt = 32;
   // slab-tiled copies (tiled.cuh) and their launch shapes per NV
-  bool tiled = false;
+  bool tiled_m[2] = {false, false};  // [A, A^T]
   Tiled tA{}, tAt{};
   int tsub[2][3] = {}, tsplit[2][3] = {};  // [matrix][NV]
   double* Ptile = nullptr;
@@ -933,7 +933,7 @@ void set_tiled_smem(int dev, size_t bytes) {
 // the problem is large, CSR kernel otherwise.
 template <class Epi>
 void launch_mat(scs_handle* h, int mat, const Epi& epi) {
-  if (!h->tiled) {
+  if (!h->tiled_m[mat]) {
     if (mat == 0) launch_spmv(h, h->A, h->LA, epi);
     else launch_spmv(h, h->At, h->LAt, epi);
     return;
@@ -1128,25 +1128,37 @@ void build_tiled(scs_handle* h, const Csr& M, long long cols, Tiled& T) {
       rows, cols, nz, nseg, nchunk, nent, nz ? 100.0 * (nent - nz) / nz : 0.0);
 }
 
+// Tiling pays when a row meets a slab often enough: the expected row
+// segment per (row, slab) tile, nnz/row * W/cols, must be a few entries;
+// for very wide matrices with short rows (config 5) the per-slab CTA
+// synchronisation outweighs the gather savings and the CSR kernel stays.
 void setup_tiled(scs_handle* h) {
   const char* env = getenv("SCS_TILED");
-  const bool want = env ? atoi(env) != 0 : h->nnz >= 4000000LL;
-  if (!want || h->nnz == 0) return;
-  build_tiled(h, h->A, h->n, h->tA);
-  build_tiled(h, h->At, h->m, h->tAt);
-  tile_shapes(h, 0, h->tA, h->nnz);
-  tile_shapes(h, 1, h->tAt, h->nnz);
+  const int force = env ? atoi(env) : -1;  // 0 off, 1 on, unset: heuristic
+  if (force == 0 || h->nnz == 0) return;
+  const double W = 4096.0;
+  for (int mat = 0; mat < 2; ++mat) {
+    const double rows = mat == 0 ? h->m : h->n, cols = mat == 0 ? h->n : h->m;
+    const double seg = (double)h->nnz / std::max(rows, 1.0) * std::min(1.0, W / std::max(cols, 1.0));
+    const bool want = force == 1 || (h->nnz >= 4000000LL && seg >= 3.0);
+    if (!want) continue;
+    Tiled& T = mat == 0 ? h->tA : h->tAt;
+    build_tiled(h, mat == 0 ? h->A : h->At, mat == 0 ? h->n : h->m, T);
+    tile_shapes(h, mat, T, h->nnz);
+    h->tiled_m[mat] = true;
+  }
   size_t need = 0;
   for (int mat = 0; mat < 2; ++mat)
     for (int NV = 1; NV <= 2; ++NV) {
       const Tiled& T = mat == 0 ? h->tA : h->tAt;
-      if (h->tsplit[mat][NV] > 1) need = std::max<size_t>(need, (size_t)h->tsplit[mat][NV] * (size_t)T.rows * NV);
+      if (h->tiled_m[mat] && h->tsplit[mat][NV] > 1)
+        need = std::max<size_t>(need, (size_t)h->tsplit[mat][NV] * (size_t)T.rows * NV);
     }
   if (need) h->Ptile = dalloc<double>(h, need);
-  h->tiled = true;
-  dbg("tiled: A NB=%d S=%d (sub,split) nv1=(%d,%d) nv2=(%d,%d); At NB=%d S=%d nv1=(%d,%d) nv2=(%d,%d)",
-      h->tA.NB, h->tA.S, h->tsub[0][1], h->tsplit[0][1], h->tsub[0][2], h->tsplit[0][2], h->tAt.NB,
-      h->tAt.S, h->tsub[1][1], h->tsplit[1][1], h->tsub[1][2], h->tsplit[1][2]);
+  dbg("tiled: A=%d (NB=%d S=%d nv1=(%d,%d) nv2=(%d,%d)) At=%d (NB=%d S=%d nv1=(%d,%d) nv2=(%d,%d))",
+      (int)h->tiled_m[0], h->tA.NB, h->tA.S, h->tsub[0][1], h->tsplit[0][1], h->tsub[0][2],
+      h->tsplit[0][2], (int)h->tiled_m[1], h->tAt.NB, h->tAt.S, h->tsub[1][1], h->tsplit[1][1],
+      h->tsub[1][2], h->tsplit[1][2]);
 }
 
 // A pass over the local rows.  Row-sharded: its (y-part) totals are
