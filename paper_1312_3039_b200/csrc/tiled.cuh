@@ -137,63 +137,36 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const double* slab = slabs + (size_t)cur * T.W * NV;
     const long long tb = tb0 + (long long)s * kTileNsub;
     const long long c_lo = __ldg(T.cs + tb), c_hi = __ldg(T.cs + tb + fsb);
-    // blocks of 8 consecutive chunks per warp: the 9 chunk offsets of a block
-    // come from one load (lanes 0..8) and are broadcast by shuffles; two
-    // chunks' first four steps are loaded before either is consumed
-    for (long long cb = c_lo + 8LL * warp; cb < c_hi; cb += 8LL * nw) {
-      const int nb = (int)((c_hi - cb) < 8 ? (c_hi - cb) : 8);
-      const long long myco = lane <= nb ? __ldg(T.co + cb + lane) : 0;
-      for (int j = 0; j < nb; j += 2) {
-        const bool two = j + 1 < nb;
-        const long long offA = __shfl_sync(0xffffffffu, myco, j);
-        const long long offB = __shfl_sync(0xffffffffu, myco, j + 1);
-        const long long endB = __shfl_sync(0xffffffffu, myco, two ? j + 2 : j + 1);
-        const int wA = (int)((offB - offA) >> 5);
-        const int wB = two ? (int)((endB - offB) >> 5) : 0;
-        const unsigned rA = __ldg(T.rid + (cb + j) * 32 + lane);
-        const unsigned rB = two ? __ldg(T.rid + (cb + j + 1) * 32 + lane) : 0xffffu;
-        double aA[4], aB[4];
-        int cA[4], cB[4];
+    for (long long ch = c_lo + warp; ch < c_hi; ch += nw) {
+      const long long off = __ldg(T.co + ch);
+      const int wid = (int)((__ldg(T.co + ch + 1) - off) >> 5);
+      const unsigned rr = __ldg(T.rid + ch * 32 + lane);
+      const double* vp = T.v + off + lane;
+      const unsigned short* cp = T.col + off + lane;
+      double sum[NV];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool okA = u < wA, okB = u < wB;
-          aA[u] = okA ? __ldcs(T.v + offA + u * 32 + lane) : 0.0;
-          cA[u] = okA ? __ldcs(T.col + offA + u * 32 + lane) : 0;
-          aB[u] = okB ? __ldcs(T.v + offB + u * 32 + lane) : 0.0;
-          cB[u] = okB ? __ldcs(T.col + offB + u * 32 + lane) : 0;
-        }
-        double sA[NV], sB[NV];
+      for (int t = 0; t < NV; ++t) sum[t] = 0.0;
+      int k = 0;
+      for (; k + 4 <= wid; k += 4) {  // four steps of the chunk in flight
+        double a[4];
+        int c[4];
 #pragma unroll
-        for (int t = 0; t < NV; ++t) { sA[t] = 0.0; sB[t] = 0.0; }
+        for (int u = 0; u < 4; ++u) { a[u] = __ldcs(vp + (k + u) * 32); c[u] = __ldcs(cp + (k + u) * 32); }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int t = 0; t < NV; ++t) {
-            if (u < wA) sA[t] = fma(aA[u], slab[cA[u] * NV + t], sA[t]);
-            if (u < wB) sB[t] = fma(aB[u], slab[cB[u] * NV + t], sB[t]);
-          }
-        }
-        for (int k = 4; k < wA; ++k) {  // long segments (rare when rows are short)
-          const double a = __ldcs(T.v + offA + k * 32 + lane);
-          const int c = __ldcs(T.col + offA + k * 32 + lane);
+          for (int t = 0; t < NV; ++t) sum[t] = fma(a[u], slab[c[u] * NV + t], sum[t]);
+      }
+      for (; k < wid; ++k) {
+        const double a = __ldcs(vp + k * 32);
+        const int c = __ldcs(cp + k * 32);
 #pragma unroll
-          for (int t = 0; t < NV; ++t) sA[t] = fma(a, slab[c * NV + t], sA[t]);
-        }
-        for (int k = 4; k < wB; ++k) {
-          const double a = __ldcs(T.v + offB + k * 32 + lane);
-          const int c = __ldcs(T.col + offB + k * 32 + lane);
+        for (int t = 0; t < NV; ++t) sum[t] = fma(a, slab[c * NV + t], sum[t]);
+      }
+      if (rr != 0xffffu) {
+        const int r = (int)rr - rel0;  // one segment per row per sub-tile: exclusive
 #pragma unroll
-          for (int t = 0; t < NV; ++t) sB[t] = fma(a, slab[c * NV + t], sB[t]);
-        }
-        // one segment per row per sub-tile: the accumulator updates are exclusive
-        if (rA != 0xffffu) {
-#pragma unroll
-          for (int t = 0; t < NV; ++t) acc[(size_t)((int)rA - rel0) * NV + t] += sA[t];
-        }
-        if (rB != 0xffffu) {
-#pragma unroll
-          for (int t = 0; t < NV; ++t) acc[(size_t)((int)rB - rel0) * NV + t] += sB[t];
-        }
+        for (int t = 0; t < NV; ++t) acc[(size_t)r * NV + t] += sum[t];
       }
     }
     __syncthreads();  // everyone is done with slab `cur` before it is refilled
