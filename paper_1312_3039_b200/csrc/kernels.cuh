@@ -60,6 +60,7 @@ struct Vec {
   double *r, *Gp;             // CG vectors (n)
   double *X2, *Y2;            // interleaved gather vectors
   double *Axw;                // A cg_warm (m), from the previous EpiAFinal
+  double *Aux;                // A u_x (m) for the split residual epilogue
   double *q;                  // A p (m)
   double *zy;                 // z_y = rhs_y + A x (m)
   double *part;               // kMaxRed * kMaxGrid partials
@@ -168,7 +169,7 @@ __device__ __forceinline__ void row_dot(const Csr& A, long long k0, long long k1
 // matrix stream is the only dependent latency per row.  Epi::load() reads
 // the Ctl flags once and says whether the whole launch is a no-op.
 template <int L, class Epi>
-__global__ void __launch_bounds__(kBlock) k_spmv(Csr A, Epi epi0) {
+__global__ void __launch_bounds__(kBlock, Epi::MINB) k_spmv(Csr A, Epi epi0) {
   Epi epi = epi0;
   if (!epi.load()) return;
   constexpr int kGroups = 32 / L;
@@ -251,7 +252,14 @@ __global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows
   }
   epi.extra(red);
   if constexpr (Epi::NR > 0) {
-    if (grid_sum_last<Epi::NR>(red, epi.V.part, &epi.V.ctl->counter)) epi.finish(red);
+    if (grid_sum_last<Epi::NR>(red, epi.V.part, &epi.V.ctl->counter)) {
+      if (epi.defer) {
+        if (threadIdx.x == 0)
+          for (int t = 0; t < Epi::NR; ++t) epi.V.dred[t] = red[t];
+      } else {
+        epi.finish(red);
+      }
+    }
   }
 }
 
@@ -274,6 +282,7 @@ struct EpiBase {
   const double* xb;  // gather base
   int pend;          // residual check of the previous iteration rides along
   int defer;         // row-sharded: totals go to V.dred for an all-reduce
+  static constexpr int MINB = 1;  // min resident CTAs per SM (register cap)
   struct Pre {};
   __device__ void pre(long long, Pre&) const {}
   __device__ void extra(double*) const {}
@@ -476,6 +485,69 @@ struct EpiResAt : EpiBase {
     Ctl* c = V.ctl;
     finish_residuals(c, utau(), c->sums[0], c->sums[1], c->sums[2], tot[0], tot[1], tot[2]);
     c->check_pending = 0;
+  }
+};
+
+// ---- split epilogues (CSR path): the SpMV only stores its products, a
+// coalesced elementwise pass (k_rows) does the per-row work.  On the CSR
+// kernel a heavy per-row epilogue costs more than re-reading two m-vectors.
+
+// merged first CG A pass, plain: q = A p and (check due) Aux = A u_x
+struct EpiApPlain2 : EpiBase {
+  static constexpr int NV = 2, STRIDE = 2, NR = 0;
+  __device__ bool load() {
+    const Ctl* c = V.ctl;
+    pend = c->check_pending;
+    return !c->stop && (!c->cg_done || pend);
+  }
+  __device__ void row(long long i, const double (&s)[2], const Pre&, double*) const {
+    V.q[i] = s[0];
+    if (pend) V.Aux[i] = s[1];
+  }
+  __device__ void finish(const double*) const {}
+};
+// ... then the residual terms of A u_x and the termination check
+// (scaling.py:466-489, solver.py:359-363): EpiAp<true>'s epilogue over Aux
+struct EpiResY : EpiBase {
+  static constexpr int NV = 1, STRIDE = 1, NR = 3;
+  __device__ bool load() {
+    const Ctl* c = V.ctl;
+    pend = c->check_pending;
+    return !c->stop && pend;
+  }
+  struct Pre { double vs, d, b, uy, ut; };
+  __device__ void pre(long long i, Pre& p) const {
+    p.vs = V.v[V.n + i]; p.d = V.Dinv[i]; p.b = V.b[i]; p.uy = V.Y2[2 * i + 1]; p.ut = utau();
+  }
+  __device__ void row(long long i, const double (&s)[1], const Pre& p, double* red) const {
+    const double t = s[0] + p.vs;
+    const double pr = p.d * (t / p.ut - p.b);
+    const double ub = p.d * t;
+    red[0] += pr * pr;
+    red[1] += ub * ub;
+    red[2] += p.b * p.uy;
+  }
+  __device__ void finish(const double* tot) const {
+    if (threadIdx.x) return;
+    Ctl* c = V.ctl;
+    finish_residuals(c, utau(), tot[0], tot[1], tot[2], c->sums[3], c->sums[4], c->sums[5]);
+    c->check_pending = 0;
+    if (c->stop) c->k_sched -= 1;  // the speculative iteration never happened
+  }
+};
+// final A pass, plain: Axw = A x
+struct EpiAxPlain : EpiBase {
+  static constexpr int NV = 1, STRIDE = 1, NR = 0;
+  __device__ bool load() { return !V.ctl->stop; }
+  __device__ void row(long long i, const double (&s)[1], const Pre&, double*) const { V.Axw[i] = s[0]; }
+  __device__ void finish(const double*) const {}
+};
+// ... then z_y = rhs_y + A x and h'p (EpiAFinal's epilogue over Axw)
+struct EpiZy : EpiAFinal {
+  __device__ void row(long long i, const double (&s)[1], const Pre& p, double* red) const {
+    const double z = p.ry + s[0];
+    zy_out[i] = z;
+    red[1] += p.b * z;
   }
 };
 

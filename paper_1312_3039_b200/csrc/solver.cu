@@ -800,6 +800,7 @@ struct scs_handle {
   Tiled tA{}, tAt{};
   int tsub[2][3] = {}, tsplit[2][3] = {};  // [matrix][NV]
   double* Ptile = nullptr;
+  size_t l2_persist = 0, l2_window_max = 0;  // L2 set-aside for gather vectors
   // cones
   Cones K{};
   int nseg = 0, nseg_g = 0;
@@ -895,16 +896,47 @@ void allreduce(scs_handle* h, double* d, size_t n) {
   if (h->sharded && n) h->comm->allreduce(h->st, d, n);
 }
 
+// CSR SpMV launch.  When the gathered vector is large (A^T passes of the
+// 1e9-nonzero problem gather 80-160 MB, comparable to the 126 MB L2), the
+// launch carries an L2 access-policy window marking it persisting, so the
+// evict-first matrix stream cannot push it out (h->l2_persist bytes set
+// aside at create; 0 = off).
+template <int L, class Epi>
+void launch_spmv_l(scs_handle* h, const Csr& M, const Epi& epi, int grid, size_t gbytes) {
+  if (h->l2_persist == 0 || gbytes < ((size_t)16 << 20)) {
+    k_spmv<L, Epi><<<grid, kBlock, 0, h->st>>>(M, epi);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = h->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+  at[0].val.accessPolicyWindow.base_ptr = (void*)epi.xb;
+  at[0].val.accessPolicyWindow.num_bytes = std::min(gbytes, h->l2_window_max);
+  at[0].val.accessPolicyWindow.hitRatio =
+      (float)std::min(1.0, (double)h->l2_persist / (double)at[0].val.accessPolicyWindow.num_bytes);
+  at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_spmv<L, Epi>, M, epi));
+}
+
 template <class Epi>
 void launch_spmv(scs_handle* h, const Csr& M, int L, const Epi& epi) {
   const long long work = M.rows * (long long)L;
   const int grid = elem_grid(h, work);
+  const long long gcols = (&M == &h->A) ? h->n : h->m;  // gathered vector length
+  const size_t gbytes = (size_t)gcols * Epi::STRIDE * sizeof(double);
   switch (L) {
-    case 2: k_spmv<2, Epi><<<grid, kBlock, 0, h->st>>>(M, epi); break;
-    case 4: k_spmv<4, Epi><<<grid, kBlock, 0, h->st>>>(M, epi); break;
-    case 8: k_spmv<8, Epi><<<grid, kBlock, 0, h->st>>>(M, epi); break;
-    case 16: k_spmv<16, Epi><<<grid, kBlock, 0, h->st>>>(M, epi); break;
-    default: k_spmv<32, Epi><<<grid, kBlock, 0, h->st>>>(M, epi); break;
+    case 2: launch_spmv_l<2, Epi>(h, M, epi, grid, gbytes); break;
+    case 4: launch_spmv_l<4, Epi>(h, M, epi, grid, gbytes); break;
+    case 8: launch_spmv_l<8, Epi>(h, M, epi, grid, gbytes); break;
+    case 16: launch_spmv_l<16, Epi>(h, M, epi, grid, gbytes); break;
+    default: launch_spmv_l<32, Epi>(h, M, epi, grid, gbytes); break;
   }
   h->launches++;
 }
@@ -1191,6 +1223,42 @@ void at_pass(scs_handle* h, Epi epi) {
   allreduce(h, h->Traw, (size_t)h->n * Epi::NV);
   k_rows<Epi><<<elem_grid(h, h->n), kBlock, 0, h->st>>>(h->Traw, h->n, epi);
   h->launches++;
+}
+
+// Elementwise epilogue over an m-vector of A products (split CSR path);
+// its y-part totals are all-reduced when rows are sharded.
+template <class Epi>
+void y_rows(scs_handle* h, const double* T, Epi epi) {
+  epi.defer = (h->sharded && Epi::NR > 0) ? 1 : 0;
+  k_rows<Epi><<<elem_grid(h, h->m), kBlock, 0, h->st>>>(T, h->m, epi);
+  h->launches++;
+  if (epi.defer) {
+    allreduce(h, h->V.dred, Epi::NR);
+    k_finish<Epi><<<1, 32, 0, h->st>>>(epi);
+    h->launches++;
+  }
+}
+
+// final A pass of solve_kkt: z_y = rhs_y + A x (embedding.py:113)
+void a_final(scs_handle* h, const Vec& V, double* zy_out, int setup) {
+  if (!h->tiled_m[0]) {
+    EpiAxPlain ax{};
+    ax.V = V;
+    ax.xb = V.x;
+    launch_mat(h, 0, ax);
+    EpiZy ez{};
+    ez.V = V;
+    ez.zy_out = zy_out;
+    ez.setup = setup;
+    y_rows(h, V.Axw, ez);
+    return;
+  }
+  EpiAFinal ef{};
+  ef.V = V;
+  ef.xb = V.x;
+  ef.zy_out = zy_out;
+  ef.setup = setup;
+  a_pass(h, ef);
 }
 
 // ---------------------------------------------------------------------------
@@ -1542,7 +1610,15 @@ void check_err(scs_handle* h) {
 // one CG step (A p, A^T, update, p update); the first step of an ADMM
 // iteration also closes the previous iteration's termination check
 void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p, bool merged) {
-  if (merged) {
+  if (merged && !h->tiled_m[0]) {  // CSR: plain SpMV + elementwise residual pass
+    EpiApPlain2 ea{};
+    ea.V = V;
+    ea.xb = V.X2;
+    launch_mat(h, 0, ea);
+    EpiResY ry{};
+    ry.V = V;
+    y_rows(h, V.Aux, ry);
+  } else if (merged) {
     EpiAp<true> ea{};
     ea.V = V;
     ea.xb = V.X2;
@@ -1602,12 +1678,7 @@ void solve_g(scs_handle* h) {
     for (long long i = 0; i < batch; ++i) cg_step(h, G, cap, true, false);
     done_steps += batch;
   }
-  EpiAFinal ef{};
-  ef.V = G;
-  ef.xb = G.x;
-  ef.zy_out = h->V.gy;
-  ef.setup = 1;
-  a_pass(h, ef);
+  a_final(h, G, h->V.gy, 1);
   pull_ctl(h);
   check_err(h);
   if (c->denom < 1.0 - 1e-9)
@@ -1631,12 +1702,7 @@ void enqueue_iteration(scs_handle* h) {
   at_pass(h, e0);
   const long long cgm = h->set.cg_max;
   for (long long i = 0; i < cgm; ++i) cg_step(h, V, cgm, i + 1 < cgm, i == 0);
-  EpiAFinal ef{};
-  ef.V = V;
-  ef.xb = V.x;
-  ef.zy_out = V.zy;
-  ef.setup = 0;
-  a_pass(h, ef);
+  a_final(h, V, V.zy, 0);
   const long long work = std::max<long long>(h->n + h->K.z + h->K.l, 1);
   int g_tail = std::max(elem_grid(h, work), std::min(h->K.n_chunk, h->grid_full));
   g_tail = std::max(g_tail, std::min((int)((h->K.n_ssoc * 32LL + kBlock - 1) / kBlock), h->grid_full));
@@ -1876,6 +1942,21 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     h->grid_full = h->sms * (2048 / kBlock);
     if (h->grid_full > kMaxGrid) h->grid_full = kMaxGrid;
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    {
+      // opt-in (SCS_L2_PERSIST=1): measured slower at config 5 -- the
+      // set-aside shrinks the L2 left for everything else
+      const char* env = getenv("SCS_L2_PERSIST");
+      int maxp = 0, maxw = 0;
+      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->dev);
+      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, h->dev);
+      if (env && atoi(env) != 0 && maxp > 0 && maxw > 0 &&
+          cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) == cudaSuccess) {
+        h->l2_persist = (size_t)maxp;
+        h->l2_window_max = (size_t)maxw;
+      }
+      cudaGetLastError();
+      dbg("L2 persisting set-aside %zu bytes, window max %zu", h->l2_persist, h->l2_window_max);
+    }
     h->m = P->m;
     h->n = P->n;
     h->m_glob = P->m_global > 0 ? P->m_global : P->m;
@@ -1959,6 +2040,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     V.Y2 = dalloc<double>(h, 2 * m);
     V.rhs_y = dalloc<double>(h, m);
     V.Axw = dalloc<double>(h, m);
+    V.Aux = dalloc<double>(h, m);
     V.q = dalloc<double>(h, m);
     V.zy = dalloc<double>(h, m);
     V.Dinv = dalloc<double>(h, m);
