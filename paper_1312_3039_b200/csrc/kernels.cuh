@@ -134,27 +134,26 @@ __device__ __forceinline__ void row_dot(const Csr& A, long long k0, long long k1
                                         const double* __restrict__ xb, double (&s)[NV]) {
 #pragma unroll
   for (int t = 0; t < NV; ++t) s[t] = 0.0;
-  long long k = k0 + gl;
-  for (; k + 3 * L < k1; k += 4 * L) {
+  // every step issues up to four predicated (column, value) loads per lane
+  // before any gather, so short rows keep as many loads in flight as long ones
+  for (long long k = k0 + gl; k < k1; k += 4 * L) {
     int c[4];
     double a[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { c[u] = __ldcs(A.ci + k + u * L); a[u] = __ldcs(A.v + k + u * L); }
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = k + u * L < k1;
+      c[u] = ok ? __ldcs(A.ci + k + u * L) : 0;
+      a[u] = ok ? __ldcs(A.v + k + u * L) : 0.0;
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      double g[NV];
-      gather<NV, STRIDE>(xb, c[u], g);
+      if (k + u * L < k1) {
+        double g[NV];
+        gather<NV, STRIDE>(xb, c[u], g);
 #pragma unroll
-      for (int t = 0; t < NV; ++t) s[t] = fma(a[u], g[t], s[t]);
+        for (int t = 0; t < NV; ++t) s[t] = fma(a[u], g[t], s[t]);
+      }
     }
-  }
-  for (; k < k1; k += L) {
-    const int c = __ldcs(A.ci + k);
-    const double a = __ldcs(A.v + k);
-    double g[NV];
-    gather<NV, STRIDE>(xb, c, g);
-#pragma unroll
-    for (int t = 0; t < NV; ++t) s[t] = fma(a, g[t], s[t]);
   }
   // all 32 lanes reach the shuffles: the row loop below is warp-uniform
 #pragma unroll
