@@ -883,13 +883,12 @@ int elem_grid(scs_handle* h, long long work) {
   return (int)std::max<long long>(1, std::min<long long>(g, h->grid_full));
 }
 
+// lanes per row: about 8 nonzeros per lane (two predicated 4-load steps)
 int pick_lanes(long long nnz, long long rows) {
   const double avg = rows ? (double)nnz / (double)rows : 0.0;
-  if (avg <= 2.5) return 2;
-  if (avg <= 6) return 4;
-  if (avg <= 12) return 8;
-  if (avg <= 24) return 16;
-  return 32;
+  int L = 2;
+  while (L < 32 && L * 8 < avg) L *= 2;
+  return L;
 }
 
 void allreduce(scs_handle* h, double* d, size_t n) {
@@ -1473,6 +1472,8 @@ void build_matrices(scs_handle* h, const scs_problem* P) {
   h->A = Csr{rp, ci, av, m};
   h->LA = pick_lanes(nnz, m);
   h->LAt = pick_lanes(nnz, n);
+  if (const char* e = getenv("SCS_LANES_A")) h->LA = atoi(e);     // tuning overrides
+  if (const char* e = getenv("SCS_LANES_AT")) h->LAt = atoi(e);
 }
 
 double dev_scalar(scs_handle* h, int idx = 0) {
