@@ -4,7 +4,7 @@ timeout 200 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python -m pytest tests -m gpu -q --timeout 300 -o timeout_method=thread > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
 grep -E "^(FAILED|ERROR)|passed|failed|Error |assert" gpurun_out/pytest_gpu.log | head -30
 for cfg in ${CFGS:-c3 c5}; do
-  timeout 600 python bench.py --config $cfg --steps 20 --no-cpu > gpurun_out/bench_$cfg.log 2>&1; echo ${cfg}_rc=$?
+  timeout 600 python bench.py --config $cfg --steps 20 --no-cpu --no-tte > gpurun_out/bench_$cfg.log 2>&1; echo ${cfg}_rc=$?
 done
 python - <<'PY'
 import json, glob
