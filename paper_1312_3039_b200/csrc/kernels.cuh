@@ -230,9 +230,11 @@ struct EpiRaw : Inner {
   __device__ void finish(const double*) const {}
 };
 
-// Row-sharded A^T pass, part 2: the epilogue over the all-reduced products.
+// Row-sharded or row-banded A^T pass, part 2: the epilogue over the
+// all-reduced products, or over the sum of `nsum` band partials (in band
+// order; stride rows * NV).
 template <class Epi>
-__global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows, Epi epi0) {
+__global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows, int nsum, Epi epi0) {
   Epi epi = epi0;
   if (!epi.load()) return;
   constexpr int NR = Epi::NR > 0 ? Epi::NR : 1;
@@ -247,6 +249,9 @@ __global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows
     double s[Epi::NV];
 #pragma unroll
     for (int t = 0; t < Epi::NV; ++t) s[t] = T[j * Epi::NV + t];
+    for (int b = 1; b < nsum; ++b)
+#pragma unroll
+      for (int t = 0; t < Epi::NV; ++t) s[t] += T[(b * rows + j) * Epi::NV + t];
     epi.row(j, s, pre, red);
   }
   epi.extra(red);

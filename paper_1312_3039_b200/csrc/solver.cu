@@ -454,6 +454,52 @@ __global__ void k_gather_csr(const int* perm, const int* colidx, const double* v
     av[k] = vals[s];
   }
 }
+// Row bands of A for the A^T passes (L2 blocking, see setup_bands): the
+// banded CSR(A^T) has S*n rows; row s*n + j holds the entries of column j
+// whose row index lies in band s, in their original order.  One warp per
+// column; per-warp band counters in shared memory; __match_any_sync groups
+// the lanes of a 32-entry step by band, so placement is stable.
+__global__ void __launch_bounds__(kBlock) k_band_pass(Csr At, int band_rows, int S, long long n,
+                                                      const long long* base, long long* cnt,
+                                                      int* ci2, double* v2) {
+  __shared__ long long sc[kBlock / 32][32];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long j = w; j < n; j += nw) {
+    sc[wi][lane] = (base && lane < S) ? base[(long long)lane * n + j] : 0;
+    __syncwarp();
+    const long long k0 = At.rp[j], k1 = At.rp[j + 1];
+    for (long long kb = k0; kb < k1; kb += 32) {
+      const long long k = kb + lane;
+      const bool ok = k < k1;
+      const int r = ok ? At.ci[k] : 0;
+      const int b = ok ? min(r / band_rows, S - 1) : -1;
+      const unsigned mm = __match_any_sync(0xffffffffu, b);
+      const long long at = sc[wi][b < 0 ? 0 : b];
+      __syncwarp();
+      if (ok && base) {
+        const long long d = at + __popc(mm & ((1u << lane) - 1u));
+        ci2[d] = r;
+        v2[d] = At.v[k];
+      }
+      if (ok && lane == __ffs(mm) - 1) sc[wi][b] = at + __popc(mm);
+      __syncwarp();
+    }
+    if (!base && lane < S) cnt[(long long)lane * n + j] = sc[wi][lane];
+    __syncwarp();
+  }
+}
+// out[i] = sum over bands of P[s*len + i], bands in order (== k_rows' sum)
+__global__ void k_band_sum(const double* P, long long len, int S, double* out) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < len; i += nt) {
+    double s = P[i];
+    for (int b = 1; b < S; ++b) s += P[b * len + i];
+    out[i] = s;
+  }
+}
 // per-row Euclidean norm (scaling.py:397-401), warp per row
 __global__ void k_row_norms(Csr A, double* out) {
   const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -800,6 +846,10 @@ struct scs_handle {
   Tiled tA{}, tAt{};
   int tsub[2][3] = {}, tsplit[2][3] = {};  // [matrix][NV]
   double* Ptile = nullptr;
+  // row-banded CSR(A^T) (setup_bands): S*n rows, raw band partials
+  int nband = 1, LAb = 32;
+  Csr Ab{};
+  double* Praw = nullptr;
   size_t l2_persist = 0, l2_window_max = 0;  // L2 set-aside for gather vectors
   // cones
   Cones K{};
@@ -1192,6 +1242,54 @@ void setup_tiled(scs_handle* h) {
       h->tsub[1][2], h->tsplit[1][2]);
 }
 
+// L2 blocking of the A^T passes.  Their gathered vectors (q: 8m bytes, the
+// first pass's interleaved Y2: 16m) exceed the 126 MB L2 at config 5
+// (m = 1e7), so random gathers miss to DRAM (ncu: 20-43 GB read per pass for
+// 12 GB of matrix).  Splitting A's rows into S bands of <= 32 MB of Y2 and
+// streaming CSR(A^T) band by band (row s*n + j = column j restricted to band
+// s) keeps every band's slice L2-resident; the partial products per band are
+// summed by the epilogue kernel.  Used when 16m > 64 MB and A^T is not
+// slab-tiled; SCS_BANDS=k forces k bands (1 = off).
+void setup_bands(scs_handle* h) {
+  if (h->tiled_m[1] || h->nnz == 0 || h->m < 2) return;
+  const char* env = getenv("SCS_BANDS");
+  long long S = env ? atoll(env) : -1;
+  if (S < 0) {
+    const double y2 = 16.0 * (double)h->m, budget = 32.0 * (1 << 20);
+    S = (y2 > 2 * budget && h->nnz >= 50000000LL) ? (long long)std::ceil(y2 / budget) : 1;
+  }
+  S = std::min<long long>(std::min<long long>(S, 32), h->m);
+  if (S <= 1) return;
+  const long long n = h->n, nnz = h->nnz;
+  const int band_rows = (int)((h->m + S - 1) / S);
+  S = (h->m + band_rows - 1) / band_rows;
+  if (S * n >= (1LL << 31) - 1) return;
+  long long* cnt = dalloc<long long>(h, S * n + 1);
+  long long* rpb = dalloc<long long>(h, S * n + 1);
+  CK(cudaMemsetAsync(cnt, 0, (S * n + 1) * sizeof(long long), h->st));
+  const int grid = elem_grid(h, n * 32);
+  k_band_pass<<<grid, kBlock, 0, h->st>>>(h->At, band_rows, (int)S, n, nullptr, cnt, nullptr, nullptr);
+  CK(cudaGetLastError());
+  exclusive_scan(h, cnt, rpb, S * n + 1);
+  dfree(h, cnt);
+  int* ci2 = dalloc<int>(h, nnz);
+  double* v2 = dalloc<double>(h, nnz);
+  k_band_pass<<<grid, kBlock, 0, h->st>>>(h->At, band_rows, (int)S, n, rpb, nullptr, ci2, v2);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(h->st));
+  // the unbanded copy is not used after setup
+  dfree(h, (void*)h->At.ci);
+  dfree(h, (void*)h->At.v);
+  h->At.ci = nullptr;
+  h->At.v = nullptr;
+  h->Ab = Csr{rpb, ci2, v2, S * n};
+  h->nband = (int)S;
+  h->LAb = pick_lanes(nnz, S * n);
+  if (const char* e = getenv("SCS_LANES_AT")) h->LAb = atoi(e);
+  h->Praw = dalloc<double>(h, 2 * S * n);
+  dbg("bands: S=%lld band_rows=%d LAb=%d", S, band_rows, h->LAb);
+}
+
 // A pass over the local rows.  Row-sharded: its (y-part) totals are
 // all-reduced and finished by k_finish.
 template <class Epi>
@@ -1208,19 +1306,38 @@ void a_pass(scs_handle* h, Epi epi) {
 // A^T pass.  Row-sharded: raw partial products of the local rows, one
 // all-reduce of NV n-vectors, then the epilogue on the reduced products
 // (its reductions are over replicated x-space data: no further all-reduce).
+// Row-banded (setup_bands): raw products per band, the epilogue kernel sums
+// the band partials in band order.
 template <class Epi>
 void at_pass(scs_handle* h, Epi epi) {
   epi.defer = 0;
-  if (!h->sharded) {
+  const bool banded = h->nband > 1;
+  if (!h->sharded && !banded) {
     launch_mat(h, 1, epi);
     return;
   }
+  const long long n = h->n;
   EpiRaw<Epi> raw{};
   static_cast<Epi&>(raw) = epi;
-  raw.T = h->Traw;
-  launch_mat(h, 1, raw);
-  allreduce(h, h->Traw, (size_t)h->n * Epi::NV);
-  k_rows<Epi><<<elem_grid(h, h->n), kBlock, 0, h->st>>>(h->Traw, h->n, epi);
+  const double* T = h->Traw;
+  int nsum = 1;
+  if (banded) {
+    raw.T = h->Praw;
+    launch_spmv(h, h->Ab, h->LAb, raw);
+    if (h->sharded) {
+      k_band_sum<<<elem_grid(h, n * Epi::NV), kBlock, 0, h->st>>>(h->Praw, n * Epi::NV, h->nband,
+                                                                  h->Traw);
+      h->launches++;
+    } else {
+      T = h->Praw;
+      nsum = h->nband;
+    }
+  } else {
+    raw.T = h->Traw;
+    launch_mat(h, 1, raw);
+  }
+  allreduce(h, h->Traw, (size_t)n * Epi::NV);
+  k_rows<Epi><<<elem_grid(h, n), kBlock, 0, h->st>>>(T, n, nsum, epi);
   h->launches++;
 }
 
@@ -1229,7 +1346,7 @@ void at_pass(scs_handle* h, Epi epi) {
 template <class Epi>
 void y_rows(scs_handle* h, const double* T, Epi epi) {
   epi.defer = (h->sharded && Epi::NR > 0) ? 1 : 0;
-  k_rows<Epi><<<elem_grid(h, h->m), kBlock, 0, h->st>>>(T, h->m, epi);
+  k_rows<Epi><<<elem_grid(h, h->m), kBlock, 0, h->st>>>(T, h->m, 1, epi);
   h->launches++;
   if (epi.defer) {
     allreduce(h, h->V.dred, Epi::NR);
@@ -2070,6 +2187,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     k_recip<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->E, n, (double*)V.Einv);
     dbg("equilibrated mean_col=%g mean_row=%g", h->mean_col, h->mean_row);
     setup_tiled(h);
+    setup_bands(h);
     scale_vectors(h);
     dbg("scaled sigma=%g rho=%g", h->sigma, h->rho);
     solve_g(h);
@@ -2337,7 +2455,7 @@ int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms, double* 
         EpiAtGp eg{};
         eg.V = h->V;
         eg.xb = h->V.q;
-        launch_mat(h, 1, eg);
+        at_pass(h, eg);  // banded: the raw pass + band-sum epilogue
       }
     };
     one();
