@@ -94,8 +94,20 @@ typedef struct {
   int32_t normalize;
   int32_t sweeps;
   int32_t device;   /* CUDA ordinal */
-  int32_t fast;     /* 0: reference algorithm (parity); 1: opt-in fast mode */
+  int32_t fast;     /* 0: reference algorithm (parity mode); else SCS_FAST_* bits */
 } scs_settings;
+
+/* Opt-in modes, reported separately from parity mode:
+ * SCS_FAST_PCG        Jacobi-preconditioned CG, M = diag(I + A^T A) of the
+ *                     scaled A (the north star's "diagonally preconditioned
+ *                     CG"; changes the iterates)
+ * SCS_FAST_RECURRENCE A x of the CG iterate carried by recurrence
+ *                     (A x += alpha A p) instead of a final matrix pass,
+ *                     refreshed directly every 20 iterations (rounding-level
+ *                     deviation from the reference, 5 matrix passes
+ *                     per iteration instead of 6). */
+#define SCS_FAST_PCG 1
+#define SCS_FAST_RECURRENCE 2
 
 /* Distributed launch (row sharding); NULL -> single GPU.  Rank k passes
  * rows [bounds[k], bounds[k+1]) (scs_problem.row_lo / m / m_global).  Ranks

@@ -467,11 +467,14 @@ def termination(res: Res, eps):
 # ---------------------------------------------------------------------------
 # linear system: CG on I + A^T A (sparse_linalg.py:450-487, embedding.py:86-197)
 # ---------------------------------------------------------------------------
-def cg(A: Csc, rhs, x0, tol, max_iter):
+def cg(A: Csc, rhs, x0, tol, max_iter, minv=None):
     """Plain warm-started CG; returns (x, iterations).
 
     The reference's final exact residual (sparse_linalg.py:486) is dropped by
     its only caller (embedding.py:110) and is not computed here.
+    ``minv`` (opt-in, not in the reference -- parity unpinned): Jacobi
+    preconditioner, p = M^-1 r, alpha/beta from r'M^-1 r; the stopping test
+    stays on ||r|| as in the reference.
     """
     if tol <= 0:
         raise ValueError("cg_solve: tol must be positive")
@@ -486,8 +489,12 @@ def cg(A: Csc, rhs, x0, tol, max_iter):
         raise ValueError("cg_solve: non-finite residual")
     if res <= tol:
         return x, 0
-    p = r.copy()
-    rs = res * res
+    if minv is None:
+        p = r.copy()
+        rs = res * res
+    else:
+        p = minv * r
+        rs = r @ p
     it = 0
     for _ in range(max_iter):
         Gp = gram(p)
@@ -503,8 +510,14 @@ def cg(A: Csc, rhs, x0, tol, max_iter):
             raise ValueError("cg_solve: non-finite residual")
         if np.sqrt(rs_new) <= tol:
             break
-        p = r + (rs_new / rs) * p
-        rs = rs_new
+        if minv is None:
+            p = r + (rs_new / rs) * p
+            rs = rs_new
+        else:
+            z = minv * r
+            rz = r @ z
+            p = z + (rz / rs) * p
+            rs = rz
     return x, it
 
 
@@ -513,12 +526,13 @@ class OracleSolver:
 
     def __init__(self, A: Csc, b, c, cone, *, alpha=1.5, max_iters=2500,
                  eps=(1e-3,) * 5, check_interval=1, cg_max=2, cg_tol=None,
-                 normalize=True, sweeps=10):
+                 normalize=True, sweeps=10, precond=False):
         self.cone = cone_from_spec(cone)
         self.A0, self.b0, self.c0 = A, np.asarray(b, float), np.asarray(c, float)
         self.alpha, self.max_iters, self.eps = alpha, max_iters, tuple(eps)
         self.check_interval, self.cg_max, self.cg_tol = check_interval, cg_max, cg_tol
         self.normalize, self.sweeps = normalize, sweeps
+        self.precond = precond
         self.cg_iters_total = 0
         self._rescale()
         self.cg_warm = np.zeros(A.n)
@@ -532,12 +546,17 @@ class OracleSolver:
             self.A, self.b, self.c = self.A0, self.b0.copy(), self.c0.copy()
             self.D, self.E = np.ones(self.A0.m), np.ones(self.A0.n)
             self.sigma = self.rho = 1.0
+        self.minv = None
+        if self.precond:  # opt-in Jacobi PCG on diag(I + A^T A)
+            colsq = np.bincount(np.repeat(np.arange(self.A.n), np.diff(self.A.colptr)),
+                                self.A.vals * self.A.vals, minlength=self.A.n)
+            self.minv = 1.0 / (1.0 + colsq)
 
     def _kkt(self, w, tol, max_iter):
         """solve_kkt indirect branch (embedding.py:101-114)."""
         n = self.A.n
         rhs = w[:n] - mul_t(self.A, w[n:])
-        zx, it = cg(self.A, rhs, self.cg_warm, tol, max_iter)
+        zx, it = cg(self.A, rhs, self.cg_warm, tol, max_iter, self.minv)
         self.cg_warm = zx.copy()
         self.cg_iters_total += it
         return np.concatenate([zx, w[n:] + mul(self.A, zx)])

@@ -55,8 +55,11 @@ _STATUS_BY_CODE = {0: Status.SOLVED, 1: Status.INFEASIBLE, 2: Status.UNBOUNDED,
 @dataclass
 class Settings:
     """Solver settings (solver.py:52-84).  linsys_mode must be "indirect":
-    this framework replaces the reference's indirect (CG) path; ``fast``
-    enables the opt-in non-parity optimisations."""
+    this framework replaces the reference's indirect (CG) path.  Opt-in
+    modes, reported separately from parity mode:
+    ``precond`` -- Jacobi-preconditioned CG on diag(I + A^T A) (changes the
+    iterates); ``fast`` -- A x of the CG iterate by recurrence
+    instead of a final matrix pass (rounding-level deviation)."""
 
     alpha: float = 1.5
     max_iters: int = 2500
@@ -74,6 +77,7 @@ class Settings:
     warm_start: tuple = None
     device: int = 0
     fast: bool = False
+    precond: bool = False
 
     def __post_init__(self):
         if not 0.0 < self.alpha < 2.0:
@@ -403,7 +407,7 @@ class Workspace:
             check_interval=st.check_interval, cg_max=st.cg_max,
             cg_tol=st.cg_tol if st.cg_tol is not None else 0.0,
             normalize=int(bool(st.normalize)), sweeps=st.sweeps, device=st.device,
-            fast=int(bool(st.fast)))
+            fast=(1 if getattr(st, "precond", False) else 0) | (2 if st.fast else 0))
         dist = None
         if self._dist is not None:
             sp = self._dist

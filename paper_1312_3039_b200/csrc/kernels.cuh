@@ -57,6 +57,7 @@ struct Vec {
   double *gx, *gy;            // g = M^-1 h
   double *rhs_x, *rhs_y;      // rhs = w[:-1] - w_tau h
   double *x;                  // CG iterate == cg_warm (embedding.py:111)
+  const double* Minv;         // opt-in Jacobi PCG: 1 / diag(I + A^T A); nullptr = plain CG
   double *r, *Gp;             // CG vectors (n)
   double *X2, *Y2;            // interleaved gather vectors
   double *Axw;                // A cg_warm (m), from the previous EpiAFinal
@@ -299,22 +300,29 @@ struct EpiBase {
 // that iterate (dual residual / infeasibility, scaling.py:484-490).  One
 // 128-bit gather per nonzero serves both products.
 struct EpiAtFirst : EpiBase {
-  static constexpr int NV = 2, STRIDE = 2, NR = 4;
+  static constexpr int NV = 2, STRIDE = 2, NR = 5;
   __device__ bool load() {
     pend = V.ctl->check_pending;
     return !V.ctl->stop;
   }
-  struct Pre { double rx, x, ei, c, ux, ut; };
+  struct Pre { double rx, x, mi, ei, c, ux, ut; };
   __device__ void pre(long long j, Pre& p) const {
     p.rx = V.rhs_x[j];
     p.x = V.x[j];
+    if (V.Minv) p.mi = V.Minv[j];
     if (pend) { p.ei = V.Einv[j]; p.c = V.c[j]; p.ux = V.X2[2 * j + 1]; p.ut = utau(); }
   }
   __device__ void row(long long j, const double (&s)[2], const Pre& p, double* red) const {
     const double r = (p.rx - p.x) - s[0];
     V.r[j] = r;
-    V.X2[2 * j] = r;
     red[0] += r * r;
+    if (V.Minv) {  // opt-in PCG: p = z = M^-1 r, carry r'z
+      const double z = p.mi * r;
+      V.X2[2 * j] = z;
+      red[4] += r * z;
+    } else {
+      V.X2[2 * j] = r;
+    }
     if (pend) {
       const double du = p.ei * (s[1] / p.ut + p.c);
       const double inf = p.ei * s[1];
@@ -332,7 +340,7 @@ struct EpiAtFirst : EpiBase {
     if (!isfinite(res)) { c->err |= ERR_CG_NONFINITE; c->stop = 1; c->cg_done = 1; return; }
     if (res <= c->tol) { c->cg_done = 1; return; }
     c->cg_done = 0;
-    c->rs = res * res;
+    c->rs = V.Minv ? tot[4] : res * res;
   }
 };
 
@@ -539,10 +547,16 @@ struct EpiResY : EpiBase {
     if (c->stop) c->k_sched -= 1;  // the speculative iteration never happened
   }
 };
-// final A pass, plain: Axw = A x
+// final A pass, plain: Axw = A x.  Opt-in recurrence mode (gate > 0): A x
+// is carried by k_cg_update (Axw += alpha q) and this pass only refreshes
+// it directly every `gate` iterations (bounds the rounding drift).
 struct EpiAxPlain : EpiBase {
   static constexpr int NV = 1, STRIDE = 1, NR = 0;
-  __device__ bool load() { return !V.ctl->stop; }
+  int gate;
+  __device__ bool load() {
+    const Ctl* c = V.ctl;
+    return !c->stop && (gate <= 0 || c->k_sched % gate == 0);
+  }
   __device__ void row(long long i, const double (&s)[1], const Pre&, double*) const { V.Axw[i] = s[0]; }
   __device__ void finish(const double*) const {}
 };

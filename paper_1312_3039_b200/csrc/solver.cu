@@ -78,12 +78,14 @@ __global__ void k_prep_finish(Vec V) {
   prep_finish(V.ctl, V.dred[0]);
 }
 
-// x += alpha p; r -= alpha Gp; r'r -> stop test / beta (sparse_linalg.py:476-485)
-__global__ void __launch_bounds__(kBlock) k_cg_update(Vec V, long long cap) {
+// x += alpha p; r -= alpha Gp; r'r -> stop test / beta (sparse_linalg.py:476-485).
+// Opt-in PCG: beta from r'M^-1 r.  Opt-in recurrence (recur): A x is carried
+// as Axw += alpha q over the m rows (the final A pass is then skipped).
+__global__ void __launch_bounds__(kBlock) k_cg_update(Vec V, long long cap, int recur) {
   Ctl* c = V.ctl;
   if (c->stop || c->cg_done) return;
   const double a = c->cg_alpha;
-  double red[1] = {0.0};
+  double red[2] = {0.0, 0.0};
   const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
   const long long nt = (long long)gridDim.x * kBlock;
   for (long long j = tid; j < V.n; j += nt) {
@@ -91,25 +93,32 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(Vec V, long long cap) {
     const double r = V.r[j] - a * V.Gp[j];
     V.r[j] = r;
     red[0] += r * r;
+    if (V.Minv) red[1] += r * (V.Minv[j] * r);
   }
-  if (grid_sum_last<1>(red, V.part, &c->counter) && threadIdx.x == 0) {
+  if (recur)
+    for (long long i = tid; i < V.m; i += nt) V.Axw[i] += a * V.q[i];
+  if (grid_sum_last<2>(red, V.part, &c->counter) && threadIdx.x == 0) {
     c->cg_it += 1;
     const double rs_new = red[0];
     if (!isfinite(rs_new)) { c->err |= ERR_CG_NONFINITE; c->stop = 1; c->cg_done = 1; return; }
     if (sqrt(rs_new) <= c->tol || c->cg_it >= cap) { c->cg_done = 1; return; }
-    c->cg_beta = rs_new / c->rs;
-    c->rs = rs_new;
+    const double rb = V.Minv ? red[1] : rs_new;
+    c->cg_beta = rb / c->rs;
+    c->rs = rb;
   }
 }
 
-// p = r + beta p (sparse_linalg.py:484)
+// p = r + beta p (sparse_linalg.py:484); PCG: p = M^-1 r + beta p
 __global__ void __launch_bounds__(kBlock) k_cg_p(Vec V) {
   Ctl* c = V.ctl;
   if (c->stop || c->cg_done) return;
   const double be = c->cg_beta;
   const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
   const long long nt = (long long)gridDim.x * kBlock;
-  for (long long j = tid; j < V.n; j += nt) V.X2[2 * j] = V.r[j] + be * V.X2[2 * j];
+  if (V.Minv)
+    for (long long j = tid; j < V.n; j += nt) V.X2[2 * j] = V.Minv[j] * V.r[j] + be * V.X2[2 * j];
+  else
+    for (long long j = tid; j < V.n; j += nt) V.X2[2 * j] = V.r[j] + be * V.X2[2 * j];
 }
 
 // relaxed point of element i of the (x, y) part:
@@ -848,6 +857,8 @@ struct scs_handle {
   double* Ptile = nullptr;
   // row-banded CSR(A^T) (setup_bands): S*n rows, raw band partials
   int nband = 1, LAb = 32;
+  int recur_refresh = 20;  // opt-in recurrence: direct A x every k iterations
+  double* Minv = nullptr;  // opt-in PCG diagonal
   Csr Ab{};
   double* Praw = nullptr;
   size_t l2_persist = 0, l2_window_max = 0;  // L2 set-aside for gather vectors
@@ -1242,6 +1253,26 @@ void setup_tiled(scs_handle* h) {
       h->tsub[1][2], h->tsplit[1][2]);
 }
 
+__global__ void k_pcg_diag(const double* colsq, long long n, double* out) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long j = tid; j < n; j += nt) out[j] = 1.0 / (1.0 + colsq[j]);
+}
+
+// Opt-in Jacobi PCG: M^-1 = 1 / (1 + ||A_hat e_j||^2) from the equilibrated
+// CSR(A^T) (column sums all-reduced when rows are sharded); before
+// setup_bands, which drops the unbanded copy.
+void setup_pcg(scs_handle* h) {
+  if (!(h->set.fast & SCS_FAST_PCG)) return;
+  const long long n = h->n;
+  h->Minv = dalloc<double>(h, n);
+  k_row_sumsq<<<elem_grid(h, n * 32), kBlock, 0, h->st>>>(h->At, h->tmp_n);
+  allreduce(h, h->tmp_n, n);
+  k_pcg_diag<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->tmp_n, n, h->Minv);
+  CK(cudaStreamSynchronize(h->st));
+  h->V.Minv = h->Minv;
+}
+
 // L2 blocking of the A^T passes.  Their gathered vectors (q: 8m bytes, the
 // first pass's interleaved Y2: 16m) exceed the 126 MB L2 at config 5
 // (m = 1e7), so random gathers miss to DRAM (ncu: 20-43 GB read per pass for
@@ -1357,10 +1388,12 @@ void y_rows(scs_handle* h, const double* T, Epi epi) {
 
 // final A pass of solve_kkt: z_y = rhs_y + A x (embedding.py:113)
 void a_final(scs_handle* h, const Vec& V, double* zy_out, int setup) {
-  if (!h->tiled_m[0]) {
+  const bool recur = !setup && (h->set.fast & SCS_FAST_RECURRENCE);
+  if (!h->tiled_m[0] || recur) {
     EpiAxPlain ax{};
     ax.V = V;
     ax.xb = V.x;
+    ax.gate = recur ? h->recur_refresh : 0;
     launch_mat(h, 0, ax);
     EpiZy ez{};
     ez.V = V;
@@ -1727,7 +1760,7 @@ void check_err(scs_handle* h) {
 
 // one CG step (A p, A^T, update, p update); the first step of an ADMM
 // iteration also closes the previous iteration's termination check
-void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p, bool merged) {
+void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p, bool merged, bool recur) {
   if (merged && !h->tiled_m[0]) {  // CSR: plain SpMV + elementwise residual pass
     EpiApPlain2 ea{};
     ea.V = V;
@@ -1751,7 +1784,8 @@ void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p, bool merge
   eg.V = V;
   eg.xb = V.q;
   at_pass(h, eg);
-  k_cg_update<<<elem_grid(h, h->n), kBlock, 0, h->st>>>(V, cap);
+  k_cg_update<<<elem_grid(h, recur ? std::max(h->n, h->m) : h->n), kBlock, 0, h->st>>>(V, cap,
+                                                                                    recur ? 1 : 0);
   h->launches++;
   if (with_p) {
     k_cg_p<<<elem_grid(h, h->n), kBlock, 0, h->st>>>(V);
@@ -1793,7 +1827,7 @@ void solve_g(scs_handle* h) {
     if (c->cg_done) break;
     const long long batch = std::min<long long>(32, cap - done_steps);
     if (batch <= 0) break;
-    for (long long i = 0; i < batch; ++i) cg_step(h, G, cap, true, false);
+    for (long long i = 0; i < batch; ++i) cg_step(h, G, cap, true, false, false);
     done_steps += batch;
   }
   a_final(h, G, h->V.gy, 1);
@@ -1819,7 +1853,8 @@ void enqueue_iteration(scs_handle* h) {
   e0.xb = V.Y2;
   at_pass(h, e0);
   const long long cgm = h->set.cg_max;
-  for (long long i = 0; i < cgm; ++i) cg_step(h, V, cgm, i + 1 < cgm, i == 0);
+  const bool recur = (h->set.fast & SCS_FAST_RECURRENCE) != 0;
+  for (long long i = 0; i < cgm; ++i) cg_step(h, V, cgm, i + 1 < cgm, i == 0, recur);
   a_final(h, V, V.zy, 0);
   const long long work = std::max<long long>(h->n + h->K.z + h->K.l, 1);
   int g_tail = std::max(elem_grid(h, work), std::min(h->K.n_chunk, h->grid_full));
@@ -2037,6 +2072,7 @@ static void validate(const scs_problem* P, const scs_settings* S) {
     throw Fail{SCS_EINVAL, "max_iters and check_interval must be >= 1"};
   if (S->cg_max < 1) throw Fail{SCS_EINVAL, "cg_max must be >= 1"};
   if (S->sweeps < 0) throw Fail{SCS_EINVAL, "sweeps must be >= 0"};
+  if (S->fast & ~(SCS_FAST_PCG | SCS_FAST_RECURRENCE)) throw Fail{SCS_EINVAL, "unknown fast-mode bits"};
   if (P->z < 0 || P->l < 0 || P->ep < 0) throw Fail{SCS_EINVAL, "cone dimensions must be nonnegative"};
   if (P->colptr[0] != 0) throw Fail{SCS_EINVAL, "colptr must start at 0 and end at nnz"};
   for (long long j = 0; j < P->n; ++j)
@@ -2054,6 +2090,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     validate(P, S);
     dbg("validated");
     h->set = *S;
+    if (const char* e = getenv("SCS_RECUR_REFRESH")) h->recur_refresh = std::max(1, atoi(e));
     h->dev = S->device;
     CK(cudaSetDevice(h->dev));
     CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev));
@@ -2187,6 +2224,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     k_recip<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->E, n, (double*)V.Einv);
     dbg("equilibrated mean_col=%g mean_row=%g", h->mean_col, h->mean_row);
     setup_tiled(h);
+    setup_pcg(h);
     setup_bands(h);
     scale_vectors(h);
     dbg("scaled sigma=%g rho=%g", h->sigma, h->rho);

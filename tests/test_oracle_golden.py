@@ -138,3 +138,17 @@ def test_exp_cone_moreau_kkt():
         np.testing.assert_allclose(p - O.proj_exp_dual(-v), v, atol=1e-9 * scale)
         # idempotence
         np.testing.assert_allclose(O.proj_exp_primal(p), p, atol=1e-9 * scale)
+
+
+def test_oracle_pcg_reaches_reference_outcome():
+    """Opt-in Jacobi PCG (not in the reference): same status and objectives
+    within the solve tolerance as the reference's plain-CG solve."""
+    d = load("ref_portfolio")
+    s = _solver(d)
+    s.precond = True
+    s._rescale()
+    s._refresh()
+    out = s.solve()
+    assert out["status"] == d["status"]
+    tol = 10 * d["settings"]["eps_gap"]
+    assert abs(out["primal_obj"] - float(d["primal_obj"])) <= tol * (1 + abs(float(d["primal_obj"])))

@@ -30,8 +30,13 @@ def launches(path, out, title):
     for r in data:
         by.setdefault(r[idi], {"name": r[ki]})[r[mi]] = float(r[vi].replace(",", ""))
     seq = list(by.values())
-    idx = [j for j, s in enumerate(seq) if "k_prep" in s["name"]]
-    st, en = idx[-2], idx[-1]
+    idx = [j for j, s in enumerate(seq) if "k_prep" in s["name"] and "finish" not in s["name"]]
+    if len(idx) >= 2:
+        st, en = idx[-2], idx[-1]
+    else:  # one profiled iteration (tools/ncu_iteration.py): up to the cone step
+        st = idx[0]
+        tail = [j for j, s in enumerate(seq) if j > st and "k_cone_apply" in s["name"]]
+        en = (tail[0] + 1) if tail else len(seq)
     lines = [f"# {title}", "# one ADMM iteration (the last complete one in the capture);",
              "# ncu per-launch times are cold-cache and serialised: compare shares",
              f"{'kernel':64s} {'us':>9s} {'share':>6s} {'DRAM rd GB':>10s} {'wr GB':>7s} {'L2 hit %':>8s}"]
