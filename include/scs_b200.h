@@ -195,6 +195,24 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q,
                      int64_t ns, const int64_t* s, int64_t ep, int kind,
                      int64_t n, const double* x, double* out, int device);
 
+/* Independent solution checker (replaces the per-block
+ * loop of the reference's `conesplit check`, cli.py:174-199): cone-membership
+ * margins of a stacked host vector of length m, one per block in the order
+ * zero (primal only: -max|v|), nonnegative (min v), each SOC (v0 - ||v1:||),
+ * each PSD (minimum eigenvalue of the unpacked svec block), each exponential
+ * cone (-distance to K_exp, or to K_exp* when dual).  nout must equal
+ * scs_cone_margin_count(...).  Stateless (no handle): device `device`. */
+int64_t scs_cone_margin_count(int64_t z, int64_t l, int64_t nq, int64_t ns, int64_t ep,
+                              int32_t dual);
+int scs_cone_margins(const double* vec, int64_t m, int64_t z, int64_t l, int64_t nq,
+                     const int64_t* q, int64_t ns, const int64_t* s, int64_t ep, int32_t dual,
+                     int32_t device, double* out, int64_t nout);
+/* ... and its products Ax = A x, Aty = A^T y of the unscaled CSC matrix
+ * (spmv / spmv_t in cli.py:209-210, 234, 263); either output may be NULL. */
+int scs_check_products(int64_t m, int64_t n, const int64_t* colptr, const int64_t* rowidx,
+                       const double* vals, const double* x, const double* y, double* Ax,
+                       double* Aty, int32_t device);
+
 /* Benchmark hooks (bench.py): device time of k back-to-back iterations
  * (CUDA events on the solver stream; no host sync inside) after the state
  * of scs_begin; and the average device time of one launch of a single

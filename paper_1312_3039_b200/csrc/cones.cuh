@@ -41,7 +41,7 @@ __device__ __forceinline__ double exp_sign_fn(double rho, double r0, double s0, 
   return a * e * e - b - t0 * q * e;
 }
 
-__device__ void exp_proj_primal(double r0, double s0, double t0, double* out) {
+__device__ inline void exp_proj_primal(double r0, double s0, double t0, double* out) {
   if (exp_in_primal(r0, s0, t0)) { out[0] = r0; out[1] = s0; out[2] = t0; return; }
   if (exp_in_dual(-r0, -s0, -t0)) { out[0] = 0.0; out[1] = 0.0; out[2] = 0.0; return; }
   if (r0 <= 0.0 && s0 <= 0.0) { out[0] = r0; out[1] = 0.0; out[2] = fmax(t0, 0.0); return; }
@@ -105,7 +105,7 @@ __device__ __forceinline__ int rr_player(int slot, int step, int kk) {
 // sweeps; _kernels.py:137-191).  The parallel (round-robin) rotation order
 // differs from the reference's row-cyclic order; the projection it feeds is
 // unique, so results agree to rounding.  Returns false on non-convergence.
-__device__ bool block_jacobi(double* M, double* V, int k, double* cs, double* sn,
+__device__ inline bool block_jacobi(double* M, double* V, int k, double* cs, double* sn,
                              int* pp, int* qq, double* dpp, double* dqq) {
   const int tid = threadIdx.x;
   for (int e = tid; e < k * k; e += blockDim.x) V[e] = (e / k == e % k) ? 1.0 : 0.0;

@@ -33,6 +33,7 @@ EXPORTS = (
     "scs_last_error", "scs_abi_version", "scs_nccl_unique_id",
     "scs_partition_rows", "scs_gen_lasso", "scs_bench_iters", "scs_bench_kernel",
     "scs_emu_group_create", "scs_emu_group_destroy", "scs_allreduce",
+    "scs_cone_margin_count", "scs_cone_margins", "scs_check_products",
 )
 
 
@@ -99,6 +100,13 @@ def load():
         "scs_project_cone": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, i64p, C.c_int64, i64p,
                                        C.c_int64, C.c_int, C.c_int64, f64p, f64p, C.c_int]),
         "scs_bench_iters": (C.c_int, [hp, C.c_int64, f64p]),
+        "scs_cone_margin_count": (C.c_int64, [C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                              C.c_int64, C.c_int32]),
+        "scs_check_products": (C.c_int, [C.c_int64, C.c_int64, i64p, i64p, f64p, f64p, f64p,
+                                         f64p, f64p, C.c_int32]),
+        "scs_cone_margins": (C.c_int, [f64p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, i64p,
+                                       C.c_int64, i64p, C.c_int64, C.c_int32, C.c_int32, f64p,
+                                       C.c_int64]),
         "scs_bench_kernel": (C.c_int, [hp, C.c_int, C.c_int64, f64p, f64p]),
         "scs_destroy": (None, [hp]),
         "scs_emu_group_create": (C.c_void_p, [C.c_int32]),
@@ -154,6 +162,33 @@ def project_cone(x, cone, kind="dual", n=0, device=0):
                                ptr(q, i64p), s.size, ptr(s, i64p), int(cone.get("ep", 0)),
                                k, int(n), ptr(x), ptr(out), int(device)))
     return out
+
+
+def cone_margins(vec, cone, dual=False, device=0):
+    """Device cone-membership margins per block (scs_cone_margins)."""
+    lib = load()
+    vec = f64(vec)
+    q = i64(cone.get("q", ()))
+    s = i64(cone.get("s", ()))
+    z, l, ep = int(cone.get("z", 0)), int(cone.get("l", 0)), int(cone.get("ep", 0))
+    cnt = lib.scs_cone_margin_count(z, l, q.size, s.size, ep, int(bool(dual)))
+    out = np.empty(cnt, np.float64)
+    check(lib.scs_cone_margins(ptr(vec), vec.size, z, l, q.size, ptr(q, i64p), s.size,
+                               ptr(s, i64p), ep, int(bool(dual)), int(device), ptr(out), cnt))
+    return out
+
+
+def check_products(A, x=None, y=None, device=0):
+    """Device A x and/or A^T y of a CSC SparseMatrix (scs_check_products)."""
+    lib = load()
+    cp, ri, va = i64(A.colptr), i64(A.rowidx), f64(A.vals)
+    ax = np.empty(A.nrows) if x is not None else None
+    aty = np.empty(A.ncols) if y is not None else None
+    xx = f64(x) if x is not None else None
+    yy = f64(y) if y is not None else None
+    check(lib.scs_check_products(A.nrows, A.ncols, ptr(cp, i64p), ptr(ri, i64p), ptr(va),
+                                 ptr(xx), ptr(yy), ptr(ax), ptr(aty), int(device)))
+    return ax, aty
 
 
 def gen_lasso(p, q, nnz_f, seed=1, row_lo=0, row_hi=0, threads=0):

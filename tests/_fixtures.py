@@ -43,3 +43,13 @@ def rel(a, b):
     a = np.asarray(a, float)
     b = np.asarray(b, float)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)) if b.size else 0.0
+
+
+def check_golden():
+    """Reference checker reports (tests/golden/make_check_golden.py)."""
+    z = np.load(os.path.join(GOLDEN, "check_golden.npz"))
+    meta = json.loads(str(z["meta"]))
+    for rep in meta:
+        rep["vecs"] = {k: z[f"{rep['tag']}.{k}"] for k in ("x", "y", "s", "certificate")
+                       if f"{rep['tag']}.{k}" in z.files}
+    return meta
