@@ -71,6 +71,7 @@ struct Vec {
   double *chunk_part;         // big-SOC chunk partial norms
   double *soc_fac;            // 3 per big SOC: mode, head, scale
   double *cone_red;           // [c'u~x, b'u~y, err, then (||z||^2, t0) per global big SOC]
+  double *dbg;                // SCS_DEBUG_PSD: first non-converged PSD block (flag, side, svec)
   Ctl* ctl;
 };
 
@@ -233,9 +234,11 @@ struct EpiRaw : Inner {
 
 // Row-sharded or row-banded A^T pass, part 2: the epilogue over the
 // all-reduced products, or over the sum of `nsum` band partials (in band
-// order; stride rows * NV).
+// order; stride rows * NV), or -- split long rows, `seg` != nullptr -- over
+// the sum of row i's pieces seg[i] .. seg[i+1]-1 (in order).
 template <class Epi>
-__global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows, int nsum, Epi epi0) {
+__global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows, int nsum, Epi epi0,
+                                                 const long long* seg = nullptr) {
   Epi epi = epi0;
   if (!epi.load()) return;
   constexpr int NR = Epi::NR > 0 ? Epi::NR : 1;
@@ -248,11 +251,20 @@ __global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows
     typename Epi::Pre pre;
     epi.pre(j, pre);
     double s[Epi::NV];
+    if (seg) {
+      const long long v0 = seg[j], v1 = seg[j + 1];
 #pragma unroll
-    for (int t = 0; t < Epi::NV; ++t) s[t] = T[j * Epi::NV + t];
-    for (int b = 1; b < nsum; ++b)
+      for (int t = 0; t < Epi::NV; ++t) s[t] = T[v0 * Epi::NV + t];
+      for (long long v = v0 + 1; v < v1; ++v)
 #pragma unroll
-      for (int t = 0; t < Epi::NV; ++t) s[t] += T[(b * rows + j) * Epi::NV + t];
+        for (int t = 0; t < Epi::NV; ++t) s[t] += T[v * Epi::NV + t];
+    } else {
+#pragma unroll
+      for (int t = 0; t < Epi::NV; ++t) s[t] = T[j * Epi::NV + t];
+      for (int b = 1; b < nsum; ++b)
+#pragma unroll
+        for (int t = 0; t < Epi::NV; ++t) s[t] += T[(b * rows + j) * Epi::NV + t];
+    }
     epi.row(j, s, pre, red);
   }
   epi.extra(red);

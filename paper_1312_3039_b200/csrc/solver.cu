@@ -318,8 +318,50 @@ __global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K, int defer)
 
 // Big SOC apply (block per chunk) and PSD blocks (block per PSD, Jacobi in
 // shared memory, or in global scratch for sides beyond the smem budget).
+// One PSD block (cones.py:147-191): unpack svec of the relaxed point (off-
+// diagonals / sqrt 2), Jacobi, X = V diag(max(lambda, 0)) V^T repacked.
+template <class G>
+__device__ void psd_block(const G& g, const Vec& V, Ctl* c, long long o, int k, double corr,
+                          double al, double* M, double* Vv, double* cs, double* sn, int* pp,
+                          int* qq, double* dpp, double* dqq) {
+  const int len = k * (k + 1) / 2;
+  for (int e = g.rank(); e < len; e += g.size()) {
+    int i, j;
+    svec_rc(e, k, i, j);
+    const Relax r = relax_y(V, o + e, corr, al);
+    const double val = (i == j) ? r.t : r.t / 1.4142135623730951;
+    M[i * k + j] = val;
+    M[j * k + i] = val;
+  }
+  g.sync();
+  const bool ok = group_jacobi(g, M, Vv, k, cs, sn, pp, qq, dpp, dqq);
+  if (!ok) {
+    if (g.rank() == 0) {
+      atomicOr(&c->err, ERR_JACOBI);
+      if (V.dbg && atomicCAS(reinterpret_cast<unsigned long long*>(V.dbg), 0ull, 1ull) == 0ull) {
+        V.dbg[1] = k;
+        for (int e = 0; e < len; ++e) V.dbg[2 + e] = relax_y(V, o + e, corr, al).t;
+      }
+    }
+    g.sync();
+    return;
+  }
+  for (int e = g.rank(); e < len; e += g.size()) {
+    int i, j;
+    svec_rc(e, k, i, j);
+    double x = 0.0;
+    for (int t = 0; t < k; ++t) {
+      const double lam = M[t * k + t];
+      if (lam > 0.0) x += Vv[i * k + t] * lam * Vv[j * k + t];
+    }
+    const Relax r = relax_y(V, o + e, corr, al);
+    store_y(V, o + e, r.ub, (i == j) ? x : x * 1.4142135623730951);
+  }
+  g.sync();
+}
+
 __global__ void __launch_bounds__(kBlock) k_cone_apply(Vec V, Cones K, double* psd_scratch,
-                                                       int smem_side) {
+                                                       int smem_side, int warp_side) {
   Ctl* c = V.ctl;
   if (c->stop) return;
   const double corr = c->corr, al = c->alpha;
@@ -342,10 +384,11 @@ __global__ void __launch_bounds__(kBlock) k_cone_apply(Vec V, Cones K, double* p
   extern __shared__ double smem[];
   __shared__ double cs[128], sn[128], dpp[128], dqq[128];
   __shared__ int pp[128], qq[128];
+  // blocks of side > kWarpPsd: one CTA each
   for (int b = blockIdx.x; b < K.n_psd; b += gridDim.x) {
     const int k = K.psd_side[b];
+    if (k <= warp_side) continue;
     const long long o = K.psd_off[b];
-    const int len = k * (k + 1) / 2;
     double* M;
     double* Vv;
     if (k <= smem_side) { M = smem; Vv = smem + k * k; }
@@ -353,34 +396,20 @@ __global__ void __launch_bounds__(kBlock) k_cone_apply(Vec V, Cones K, double* p
       M = psd_scratch + (size_t)2 * blockIdx.x * K.max_side * K.max_side;
       Vv = M + (size_t)k * k;
     }
-    // unpack svec (cones.py:53-64): off-diagonals / sqrt(2)
-    for (int e = threadIdx.x; e < len; e += kBlock) {
-      int i, j;
-      svec_rc(e, k, i, j);
-      const Relax r = relax_y(V, o + e, corr, al);
-      const double val = (i == j) ? r.t : r.t / 1.4142135623730951;
-      M[i * k + j] = val;
-      M[j * k + i] = val;
-    }
-    __syncthreads();
-    const bool ok = block_jacobi(M, Vv, k, cs, sn, pp, qq, dpp, dqq);
-    if (!ok) {
-      if (threadIdx.x == 0) atomicOr(&c->err, ERR_JACOBI);
-      continue;
-    }
-    // X = V diag(max(lambda, 0)) V^T, repacked (cones.py:187-191)
-    for (int e = threadIdx.x; e < len; e += kBlock) {
-      int i, j;
-      svec_rc(e, k, i, j);
-      double x = 0.0;
-      for (int t = 0; t < k; ++t) {
-        const double lam = M[t * k + t];
-        if (lam > 0.0) x += Vv[i * k + t] * lam * Vv[j * k + t];
-      }
-      const Relax r = relax_y(V, o + e, corr, al);
-      store_y(V, o + e, r.ub, (i == j) ? x : x * 1.4142135623730951);
-    }
-    __syncthreads();
+    psd_block(CtaGroup{}, V, c, o, k, corr, al, M, Vv, cs, sn, pp, qq, dpp, dqq);
+  }
+  // small blocks: one warp each, per-warp slices of the dynamic smem
+  constexpr int kW = kBlock / 32;
+  __shared__ double wcs[kW][8], wsn[kW][8], wdp[kW][8], wdq[kW][8];
+  __shared__ int wpp[kW][8], wqq[kW][8];
+  __syncthreads();
+  const int wi = threadIdx.x >> 5;
+  double* M = smem + (size_t)wi * 2 * kWarpPsd * kWarpPsd;
+  for (long long b = (long long)blockIdx.x * kW + wi; b < K.n_psd; b += (long long)gridDim.x * kW) {
+    const int k = K.psd_side[b];
+    if (k > warp_side) continue;
+    psd_block(WarpGroup{}, V, c, K.psd_off[b], k, corr, al, M, M + k * k, wcs[wi], wsn[wi],
+              wpp[wi], wqq[wi], wdp[wi], wdq[wi]);
   }
 }
 
@@ -858,6 +887,12 @@ struct scs_handle {
   // row-banded CSR(A^T) (setup_bands): S*n rows, raw band partials
   int nband = 1, LAb = 32;
   int recur_refresh = 20;  // opt-in recurrence: direct A x every k iterations
+  // long rows split into pieces (setup_split): [A, A^T]
+  bool split_m[2] = {false, false};
+  Csr Asp[2] = {};
+  int Lsp[2] = {2, 2};
+  long long* seg[2] = {nullptr, nullptr};  // real row -> first piece (rows + 1)
+  double* Psplit = nullptr;                // raw piece products (2 per piece)
   double* Minv = nullptr;  // opt-in PCG diagonal
   Csr Ab{};
   double* Praw = nullptr;
@@ -873,6 +908,7 @@ struct scs_handle {
   double* seg_mean = nullptr;
   double* psd_scratch = nullptr;
   int smem_side = 0;
+  int warp_side = kWarpPsd;  // PSD blocks up to this side: warp per block (SCS_PSD_WARP=0: off)
   size_t cone_smem = 0;
   int cone_red_len = 3;
   // vectors
@@ -1025,6 +1061,16 @@ void set_tiled_smem(int dev, size_t bytes) {
 // the problem is large, CSR kernel otherwise.
 template <class Epi>
 void launch_mat(scs_handle* h, int mat, const Epi& epi) {
+  if (h->split_m[mat]) {  // long rows in pieces: raw piece products, then per-row sums
+    EpiRaw<Epi> raw{};
+    static_cast<Epi&>(raw) = epi;
+    raw.T = h->Psplit;
+    launch_spmv(h, h->Asp[mat], h->Lsp[mat], raw);
+    const long long rows = mat == 0 ? h->m : h->n;
+    k_rows<Epi><<<elem_grid(h, rows), kBlock, 0, h->st>>>(h->Psplit, rows, 1, epi, h->seg[mat]);
+    h->launches++;
+    return;
+  }
   if (!h->tiled_m[mat]) {
     if (mat == 0) launch_spmv(h, h->A, h->LA, epi);
     else launch_spmv(h, h->At, h->LAt, epi);
@@ -1321,6 +1367,60 @@ void setup_bands(scs_handle* h) {
   dbg("bands: S=%lld band_rows=%d LAb=%d", S, band_rows, h->LAb);
 }
 
+// Skewed rows (SURVEY §7 hard part 1): a CSR kernel with L lanes per row
+// runs a row of R nonzeros in ~R/(4L) dependent load rounds, so one dense
+// row (config 4: the budget row and the factor rows hold all 1e5 assets)
+// costs milliseconds while the average row is tiny.  When the longest row
+// exceeds 128 x the kernel's design point (8 nonzeros per lane), rows are
+// cut into pieces of at most 32 L entries -- a refined row pointer into the
+// same (ci, v) arrays, no data movement -- the pass writes raw piece
+// products and the epilogue kernel (k_rows with `seg`) sums each row's
+// pieces in order before running the epilogue.
+void setup_split(scs_handle* h) {
+  const char* env = getenv("SCS_SPLIT");
+  const int force = env ? atoi(env) : -1;  // 0 off, 1 on (any long row), unset: heuristic
+  if (force == 0 || h->nnz == 0) return;
+  size_t need = 0;
+  for (int mat = 0; mat < 2; ++mat) {
+    if (h->tiled_m[mat] || (mat == 1 && h->nband > 1)) continue;
+    const Csr& M = mat == 0 ? h->A : h->At;
+    const long long rows = M.rows;
+    std::vector<long long> rp(rows + 1);
+    CK(cudaMemcpy(rp.data(), M.rp, (rows + 1) * sizeof(long long), cudaMemcpyDeviceToHost));
+    long long mx = 0;
+    for (long long i = 0; i < rows; ++i) mx = std::max(mx, rp[i + 1] - rp[i]);
+    const int L = mat == 0 ? h->LA : h->LAt;
+    const long long cap = force == 1 ? std::max<long long>(8, 4LL * L) : 32LL * L;
+    if (mx <= (force == 1 ? cap : 128LL * 8 * L)) continue;
+    std::vector<long long> seg(rows + 1), vrp;
+    vrp.reserve(rows + h->nnz / cap + 2);
+    for (long long i = 0; i < rows; ++i) {
+      seg[i] = (long long)vrp.size();
+      long long k = rp[i];
+      do {
+        vrp.push_back(k);
+        k += cap;
+      } while (k < rp[i + 1]);
+    }
+    seg[rows] = (long long)vrp.size();
+    vrp.push_back(rp[rows]);
+    const long long V = (long long)vrp.size() - 1;
+    long long* dv = dalloc<long long>(h, V + 1);
+    long long* ds = dalloc<long long>(h, rows + 1);
+    h2d(h, dv, vrp.data(), V + 1);
+    h2d(h, ds, seg.data(), rows + 1);
+    CK(cudaStreamSynchronize(h->st));
+    h->Asp[mat] = Csr{dv, M.ci, M.v, V};
+    h->seg[mat] = ds;
+    h->Lsp[mat] = pick_lanes(h->nnz, V);
+    h->split_m[mat] = true;
+    need = std::max<size_t>(need, 2 * (size_t)V);
+    dbg("split: mat=%d rows=%lld longest=%lld pieces=%lld cap=%lld L=%d", mat, rows, mx, V, cap,
+        h->Lsp[mat]);
+  }
+  if (need) h->Psplit = dalloc<double>(h, need);
+}
+
 // A pass over the local rows.  Row-sharded: its (y-part) totals are
 // all-reduced and finished by k_finish.
 template <class Epi>
@@ -1550,13 +1650,17 @@ void build_cones(scs_handle* h, const scs_problem* P) {
   // PSD workspace: shared memory up to ~200 KB, else global scratch
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
-  const size_t budget = (size_t)std::max(0, optin - 8 * 1024);
+  const size_t budget = (size_t)std::max(0, optin - 12 * 1024);  // minus static smem
   int side = 0;
   while ((size_t)2 * (side + 1) * (side + 1) * sizeof(double) <= budget) ++side;
   h->smem_side = std::min(side, 255);
   if (max_side > 255) throw Fail{SCS_EINVAL, "PSD side > 255 is not supported by the device Jacobi kernel"};
-  const int s_used = std::min(max_side, h->smem_side);
-  h->cone_smem = (size_t)2 * s_used * s_used * sizeof(double);
+  if (const char* e = getenv("SCS_PSD_WARP")) h->warp_side = atoi(e) ? kWarpPsd : 0;
+  const int s_used = max_side > h->warp_side ? std::min(max_side, h->smem_side) : 0;
+  // CTA-per-block region for large blocks; per-warp regions for small ones
+  h->cone_smem = std::max((size_t)2 * s_used * s_used * sizeof(double),
+                          psd_off.empty() ? (size_t)0
+                                          : (size_t)(kBlock / 32) * 2 * kWarpPsd * kWarpPsd * sizeof(double));
   if (max_side > h->smem_side)
     h->psd_scratch = dalloc<double>(h, (size_t)2 * max_side * max_side * h->grid_full);
   if (h->cone_smem > 48 * 1024)
@@ -1754,8 +1858,18 @@ void check_err(scs_handle* h) {
     throw Fail{SCS_ENONFINITE, "cg_solve: operator is not positive definite on iterates"};
   if (e & ERR_CG_NONFINITE) throw Fail{SCS_ENONFINITE, "cg_solve: non-finite residual"};
   if (e & ERR_CONE_NONFINITE) throw Fail{SCS_ENONFINITE, "project_embedding_cone: non-finite input"};
-  if (e & ERR_JACOBI)
+  if (e & ERR_JACOBI) {
+    if (h->V.dbg) {
+      const int cap = 2 + h->K.max_side * (h->K.max_side + 1) / 2;
+      std::vector<double> d(cap);
+      cudaMemcpy(d.data(), h->V.dbg, cap * sizeof(double), cudaMemcpyDeviceToHost);
+      const int k = (int)d[1];
+      fprintf(stderr, "[scs] non-converged PSD block side %d svec:", k);
+      for (int i = 0; i < k * (k + 1) / 2; ++i) fprintf(stderr, " %.17g", d[2 + i]);
+      fprintf(stderr, "\n");
+    }
     throw Fail{SCS_ENOCONV, "Jacobi eigensolver did not converge within 100 sweeps"};
+  }
 }
 
 // one CG step (A p, A^T, update, p update); the first step of an ADMM
@@ -1868,7 +1982,8 @@ void enqueue_iteration(scs_handle* h) {
   }
   if (h->K.n_chunk > 0 || h->K.n_psd > 0) {
     const int g = std::max(1, std::min(std::max(h->K.n_chunk, h->K.n_psd), h->grid_full));
-    k_cone_apply<<<g, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side);
+    k_cone_apply<<<g, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side,
+                                                      h->warp_side);
     h->launches++;
   }
 }
@@ -2205,6 +2320,11 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     V.chunk_part = dalloc<double>(h, std::max(h->K.n_chunk, 1));
     V.soc_fac = dalloc<double>(h, 3 * std::max(h->K.n_bsoc, 1));
     V.cone_red = dalloc<double>(h, h->cone_red_len);
+    if (getenv("SCS_DEBUG_PSD") && h->K.n_psd) {
+      const size_t cap = 2 + (size_t)h->K.max_side * (h->K.max_side + 1) / 2;
+      V.dbg = dalloc<double>(h, cap);
+      CK(cudaMemsetAsync(V.dbg, 0, cap * sizeof(double), h->st));
+    }
     V.xw = (!h->sharded || h->rank == 0) ? 1.0 : 0.0;
     if (h->sharded) h->Traw = dalloc<double>(h, 2 * std::max<long long>(n, 1));
     h->tmp_n = dalloc<double>(h, n);
@@ -2226,6 +2346,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     setup_tiled(h);
     setup_pcg(h);
     setup_bands(h);
+    setup_split(h);
     scale_vectors(h);
     dbg("scaled sigma=%g rho=%g", h->sigma, h->rho);
     solve_g(h);
@@ -2432,7 +2553,8 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t
     k_cone_tail<<<g, kBlock, 0, h->st>>>(V, h->K, 0);
     if (h->K.n_chunk > 0 || h->K.n_psd > 0) {
       const int ga = std::max(1, std::min(std::max(h->K.n_chunk, h->K.n_psd), h->grid_full));
-      k_cone_apply<<<ga, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side);
+      k_cone_apply<<<ga, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side,
+                                                          h->warp_side);
     }
     CK(cudaGetLastError());
     std::vector<double> res(len);

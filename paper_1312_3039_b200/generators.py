@@ -284,3 +284,86 @@ def gen_cone_mix(n_psd=50, psd_sides=(3, 4, 5, 6, 7, 8), n_exp=50, n_soc=20,
     rng.shuffle(sides)
     cone = {"z": z, "l": l, "q": [soc_dim] * n_soc, "s": sides, "ep": n_exp}
     return gen_planted(cone, n, None, seed, nnz_per_col=nnz_per_col)
+
+
+def gen_portfolio_c4(p, q, n_exp, group_sides=(2, 3, 4, 5, 6, 7), n_groups=None, seed=0,
+                     gamma=10.0, lam=1.0, kappa=1.0):
+    """Config 4 (BASELINE.json configs[3]): the reference's long-only factor
+    portfolio (gen_portfolio's encoding, generators.py:123-194) extended with
+
+    * log-utility on ``n_exp`` assets: maximise lam * sum log(p z_i) / p
+      through (u_i, 1/p, z_i) in K_exp (e^{p u_i} / p <= z_i), objective
+      -lam * sum u_i;
+    * sector concentration on ``n_groups`` disjoint asset groups of k assets
+      (k cycling through ``group_sides``): [[tau_g, z_g^T], [z_g, I_k / p]]
+      PSD (side k+1, i.e. p ||z_g||^2 <= tau_g), objective
+      + kappa * sum tau_g -- "many small PSD blocks".
+    The 1/p constants keep every block on the scale of the weights
+    (z ~ 1/p); with O(1) constants the iteration count grows ~p.
+
+    Variables (z: p, t, s, u, v, tau: n_groups, u_exp: n_exp); rows in cone
+    order zero, nonneg, SOC (p+1, q+1, 3, 3), PSD, exp.  Not
+    reference-comparable beyond the portfolio core (no exp/PSD in the
+    reference)."""
+    if not p > q >= 1:
+        raise ValueError("portfolio needs p > q >= 1")
+    rng = np.random.default_rng(seed)
+    sides = []
+    covered = 0
+    while (n_groups is None and covered + group_sides[len(sides) % len(group_sides)] <= p // 2) or \
+            (n_groups is not None and len(sides) < n_groups):
+        k = group_sides[len(sides) % len(group_sides)]
+        if covered + k > p:
+            break
+        sides.append(k)
+        covered += k
+    ng = len(sides)
+    if n_exp > p:
+        raise ValueError("n_exp must be <= p")
+    colptr0, ri0, va0, b0, c0, cone0 = gen_portfolio(p, q, seed, gamma)
+    m0, n0 = b0.size, colptr0.size - 1
+    cols0 = np.repeat(np.arange(n0), np.diff(colptr0))
+    perm = rng.permutation(p)
+    tau0 = n0
+    uexp0 = n0 + ng
+    n = n0 + ng + n_exp
+    rows, cols, vals = [ri0], [cols0], [va0]
+    # PSD blocks: svec of [[tau, z^T], [z, I]] (column-major lower triangle, sqrt2 off-diagonals)
+    r = m0
+    b_psd = []
+    at = 0
+    for g, k in enumerate(sides):
+        assets = perm[at:at + k]
+        at += k
+        side = k + 1
+        bb = np.zeros(side * (side + 1) // 2)
+        e = 0
+        for j in range(side):
+            for i in range(j, side):
+                if i == 0 and j == 0:
+                    rows.append([r + e]); cols.append([tau0 + g]); vals.append([-1.0])
+                elif j == 0:
+                    rows.append([r + e]); cols.append([assets[i - 1]]); vals.append([-math.sqrt(2.0)])
+                elif i == j:
+                    bb[e] = 1.0 / p
+                e += 1
+        b_psd.append(bb)
+        r += e
+    # exp cones (u_i, 1, z_i)
+    ex = perm[:n_exp] if n_exp else np.zeros(0, np.int64)
+    er = r + 3 * np.arange(n_exp)
+    rows += [er, er + 2]
+    cols += [uexp0 + np.arange(n_exp), ex]
+    vals += [-np.ones(n_exp), -np.ones(n_exp)]
+    b_exp = np.zeros(3 * n_exp)
+    b_exp[1::3] = 1.0 / p
+    m = r + 3 * n_exp
+    b = np.concatenate([b0] + b_psd + [b_exp])
+    c = np.concatenate([c0, kappa * np.ones(ng), -lam * np.ones(n_exp)])
+    colptr, ri, va = _csc_from_triplets(m, n, np.concatenate([np.asarray(x, np.int64) for x in rows]),
+                                        np.concatenate([np.asarray(x, np.int64) for x in cols]),
+                                        np.concatenate([np.asarray(x, float) for x in vals]))
+    cone = dict(cone0)
+    cone["s"] = [k + 1 for k in sides]
+    cone["ep"] = int(n_exp)
+    return colptr, ri, va, b, c, cone
