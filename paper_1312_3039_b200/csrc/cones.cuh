@@ -117,7 +117,7 @@ struct WarpGroup {
   __device__ void sync() const { __syncwarp(); }
   __device__ double sum(double v) const { return warp_sum(v); }
 };
-constexpr int kWarpPsd = 16;  // warp-per-block Jacobi up to this side (<= 8 pairs)
+constexpr int kWarpPsd = 16;  // sub-warp Jacobi up to this side (<= 8 pairs)
 
 // Group-cooperative Jacobi eigensolve of the symmetric k x k matrix M
 // (row-major, stride k) with eigenvectors V; same stopping rule as the
@@ -125,9 +125,12 @@ constexpr int kWarpPsd = 16;  // warp-per-block Jacobi up to this side (<= 8 pai
 // sweeps; _kernels.py:137-191).  The parallel (round-robin) rotation order
 // differs from the reference's row-cyclic order; the projection it feeds is
 // unique, so results agree to rounding.  Returns false on non-convergence.
-template <class G>
-__device__ inline bool group_jacobi(const G& g, double* M, double* V, int k, double* cs,
+// KC > 0: the side is a compile-time constant (warp path, sides <= 16), so
+// the index arithmetic (/ k, % k, % (kk - 1)) folds to multiplies.
+template <int KC, class G>
+__device__ inline bool group_jacobi(const G& g, double* M, double* V, int k_rt, double* cs,
                                     double* sn, int* pp, int* qq, double* dpp, double* dqq) {
+  const int k = KC > 0 ? KC : k_rt;
   const int tid = g.rank(), nt = g.size();
   for (int e = tid; e < k * k; e += nt) V[e] = (e / k == e % k) ? 1.0 : 0.0;
   double fro = 0.0;
@@ -219,7 +222,7 @@ __device__ inline bool group_jacobi(const G& g, double* M, double* V, int k, dou
 
 __device__ inline bool block_jacobi(double* M, double* V, int k, double* cs, double* sn, int* pp,
                                     int* qq, double* dpp, double* dqq) {
-  return group_jacobi(CtaGroup{}, M, V, k, cs, sn, pp, qq, dpp, dqq);
+  return group_jacobi<0>(CtaGroup{}, M, V, k, cs, sn, pp, qq, dpp, dqq);
 }
 
 }  // namespace scs

@@ -101,7 +101,7 @@ struct Cones {
 };
 
 constexpr int kSmallSoc = 2048;  // warp-per-cone bound
-constexpr int kChunk = 8192;     // big-SOC chunk (one CTA)
+constexpr int kChunk = 1024;     // big-SOC chunk (one CTA)
 
 // ---------------------------------------------------------------------------
 // CSR row dot products: L lanes per row, lane-strided, FMA, group shuffle.
@@ -232,6 +232,31 @@ struct EpiRaw : Inner {
   __device__ void finish(const double*) const {}
 };
 
+// Split long rows with more than kLongSeg pieces: one warp per such row sums
+// its pieces (lane-strided, then a butterfly: a fixed order) into the first
+// piece's slot before k_rows runs the epilogue.
+constexpr int kLongSeg = 32;
+template <int NV>
+__global__ void k_seg_long(double* T, const long long* seg, const long long* long_rows, long long n) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long r = w; r < n; r += nw) {
+    const long long j = long_rows[r], v0 = seg[j], v1 = seg[j + 1];
+    double s[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) s[t] = 0.0;
+    for (long long v = v0 + lane; v < v1; v += 32)
+#pragma unroll
+      for (int t = 0; t < NV; ++t) s[t] += T[v * NV + t];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) s[t] = warp_sum(s[t]);
+    if (lane == 0)
+#pragma unroll
+      for (int t = 0; t < NV; ++t) T[v0 * NV + t] = s[t];
+  }
+}
+
 // Row-sharded or row-banded A^T pass, part 2: the epilogue over the
 // all-reduced products, or over the sum of `nsum` band partials (in band
 // order; stride rows * NV), or -- split long rows, `seg` != nullptr -- over
@@ -255,9 +280,10 @@ __global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows
       const long long v0 = seg[j], v1 = seg[j + 1];
 #pragma unroll
       for (int t = 0; t < Epi::NV; ++t) s[t] = T[v0 * Epi::NV + t];
-      for (long long v = v0 + 1; v < v1; ++v)
+      if (v1 - v0 <= kLongSeg)  // longer rows were pre-summed by k_seg_long
+        for (long long v = v0 + 1; v < v1; ++v)
 #pragma unroll
-        for (int t = 0; t < Epi::NV; ++t) s[t] += T[v * Epi::NV + t];
+          for (int t = 0; t < Epi::NV; ++t) s[t] += T[v * Epi::NV + t];
     } else {
 #pragma unroll
       for (int t = 0; t < Epi::NV; ++t) s[t] = T[j * Epi::NV + t];

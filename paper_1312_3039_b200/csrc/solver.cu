@@ -320,10 +320,11 @@ __global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K, int defer)
 // shared memory, or in global scratch for sides beyond the smem budget).
 // One PSD block (cones.py:147-191): unpack svec of the relaxed point (off-
 // diagonals / sqrt 2), Jacobi, X = V diag(max(lambda, 0)) V^T repacked.
-template <class G>
-__device__ void psd_block(const G& g, const Vec& V, Ctl* c, long long o, int k, double corr,
+template <int KC, class G>
+__device__ void psd_block(const G& g, const Vec& V, Ctl* c, long long o, int k_rt, double corr,
                           double al, double* M, double* Vv, double* cs, double* sn, int* pp,
                           int* qq, double* dpp, double* dqq) {
+  const int k = KC > 0 ? KC : k_rt;
   const int len = k * (k + 1) / 2;
   for (int e = g.rank(); e < len; e += g.size()) {
     int i, j;
@@ -334,7 +335,7 @@ __device__ void psd_block(const G& g, const Vec& V, Ctl* c, long long o, int k, 
     M[j * k + i] = val;
   }
   g.sync();
-  const bool ok = group_jacobi(g, M, Vv, k, cs, sn, pp, qq, dpp, dqq);
+  const bool ok = group_jacobi<KC>(g, M, Vv, k, cs, sn, pp, qq, dpp, dqq);
   if (!ok) {
     if (g.rank() == 0) {
       atomicOr(&c->err, ERR_JACOBI);
@@ -396,20 +397,32 @@ __global__ void __launch_bounds__(kBlock) k_cone_apply(Vec V, Cones K, double* p
       M = psd_scratch + (size_t)2 * blockIdx.x * K.max_side * K.max_side;
       Vv = M + (size_t)k * k;
     }
-    psd_block(CtaGroup{}, V, c, o, k, corr, al, M, Vv, cs, sn, pp, qq, dpp, dqq);
+    psd_block<0>(CtaGroup{}, V, c, o, k, corr, al, M, Vv, cs, sn, pp, qq, dpp, dqq);
   }
-  // small blocks: one warp each, per-warp slices of the dynamic smem
+}
+
+// PSD blocks of side <= kWarpPsd: one warp each over a list of block
+// indices (largest sides first), per-warp slices of the dynamic smem.
+// (Measured on config 4's 11,111 blocks of side 3-8: a single launch with
+// a warp per block beat 8- or 16-lane groups with one launch per side --
+// the per-block Jacobi is latency-bound on its fp64 sqrt/div chain, so
+// concurrency across blocks matters more than lanes per block.)
+constexpr size_t kPsdSmallSmem = (size_t)(kBlock / 32) * 2 * kWarpPsd * kWarpPsd * sizeof(double);
+__global__ void __launch_bounds__(kBlock) k_psd_small(Vec V, Cones K, const int* list, int count) {
+  Ctl* c = V.ctl;
+  if (c->stop) return;
+  const double corr = c->corr, al = c->alpha;
+  extern __shared__ double smem[];
   constexpr int kW = kBlock / 32;
   __shared__ double wcs[kW][8], wsn[kW][8], wdp[kW][8], wdq[kW][8];
   __shared__ int wpp[kW][8], wqq[kW][8];
-  __syncthreads();
   const int wi = threadIdx.x >> 5;
   double* M = smem + (size_t)wi * 2 * kWarpPsd * kWarpPsd;
-  for (long long b = (long long)blockIdx.x * kW + wi; b < K.n_psd; b += (long long)gridDim.x * kW) {
+  for (long long t = (long long)blockIdx.x * kW + wi; t < count; t += (long long)gridDim.x * kW) {
+    const int b = list[t];
     const int k = K.psd_side[b];
-    if (k > warp_side) continue;
-    psd_block(WarpGroup{}, V, c, K.psd_off[b], k, corr, al, M, M + k * k, wcs[wi], wsn[wi],
-              wpp[wi], wqq[wi], wdp[wi], wdq[wi]);
+    psd_block<0>(WarpGroup{}, V, c, K.psd_off[b], k, corr, al, M, M + k * k, wcs[wi], wsn[wi],
+                 wpp[wi], wqq[wi], wdp[wi], wdq[wi]);
   }
 }
 
@@ -892,6 +905,8 @@ struct scs_handle {
   Csr Asp[2] = {};
   int Lsp[2] = {2, 2};
   long long* seg[2] = {nullptr, nullptr};  // real row -> first piece (rows + 1)
+  long long* long_rows[2] = {nullptr, nullptr};  // rows with > kLongSeg pieces
+  long long n_long[2] = {0, 0};
   double* Psplit = nullptr;                // raw piece products (2 per piece)
   double* Minv = nullptr;  // opt-in PCG diagonal
   Csr Ab{};
@@ -909,6 +924,8 @@ struct scs_handle {
   double* psd_scratch = nullptr;
   int smem_side = 0;
   int warp_side = kWarpPsd;  // PSD blocks up to this side: warp per block (SCS_PSD_WARP=0: off)
+  int n_psd_small = 0;
+  const int* psd_small_list = nullptr;  // their block indices, largest side first
   size_t cone_smem = 0;
   int cone_red_len = 3;
   // vectors
@@ -1066,6 +1083,11 @@ void launch_mat(scs_handle* h, int mat, const Epi& epi) {
     static_cast<Epi&>(raw) = epi;
     raw.T = h->Psplit;
     launch_spmv(h, h->Asp[mat], h->Lsp[mat], raw);
+    if (h->n_long[mat]) {
+      k_seg_long<Epi::NV><<<elem_grid(h, h->n_long[mat] * 32), kBlock, 0, h->st>>>(
+          h->Psplit, h->seg[mat], h->long_rows[mat], h->n_long[mat]);
+      h->launches++;
+    }
     const long long rows = mat == 0 ? h->m : h->n;
     k_rows<Epi><<<elem_grid(h, rows), kBlock, 0, h->st>>>(h->Psplit, rows, 1, epi, h->seg[mat]);
     h->launches++;
@@ -1404,6 +1426,14 @@ void setup_split(scs_handle* h) {
     }
     seg[rows] = (long long)vrp.size();
     vrp.push_back(rp[rows]);
+    std::vector<long long> lr;
+    for (long long i = 0; i < rows; ++i)
+      if (seg[i + 1] - seg[i] > kLongSeg) lr.push_back(i);
+    if (!lr.empty()) {
+      h->long_rows[mat] = dalloc<long long>(h, lr.size());
+      h2d(h, h->long_rows[mat], lr.data(), lr.size());
+      h->n_long[mat] = (long long)lr.size();
+    }
     const long long V = (long long)vrp.size() - 1;
     long long* dv = dalloc<long long>(h, V + 1);
     long long* ds = dalloc<long long>(h, rows + 1);
@@ -1658,9 +1688,17 @@ void build_cones(scs_handle* h, const scs_problem* P) {
   if (const char* e = getenv("SCS_PSD_WARP")) h->warp_side = atoi(e) ? kWarpPsd : 0;
   const int s_used = max_side > h->warp_side ? std::min(max_side, h->smem_side) : 0;
   // CTA-per-block region for large blocks; per-warp regions for small ones
-  h->cone_smem = std::max((size_t)2 * s_used * s_used * sizeof(double),
-                          psd_off.empty() ? (size_t)0
-                                          : (size_t)(kBlock / 32) * 2 * kWarpPsd * kWarpPsd * sizeof(double));
+  h->cone_smem = (size_t)2 * s_used * s_used * sizeof(double);
+  h->n_psd_small = 0;
+  {
+    std::vector<int> small;
+    for (size_t b = 0; b < psd_side.size(); ++b)
+      if (psd_side[b] <= h->warp_side) small.push_back((int)b);
+    std::stable_sort(small.begin(), small.end(),
+                     [&](int a, int b) { return psd_side[a] > psd_side[b]; });
+    h->n_psd_small = (int)small.size();
+    if (!small.empty()) h->psd_small_list = up_i(small);
+  }
   if (max_side > h->smem_side)
     h->psd_scratch = dalloc<double>(h, (size_t)2 * max_side * max_side * h->grid_full);
   if (h->cone_smem > 48 * 1024)
@@ -1951,6 +1989,8 @@ void solve_g(scs_handle* h) {
     throw Fail{SCS_ESETUP, "Schur denominator " + std::to_string(c->denom) + " below 1"};
 }
 
+void launch_cone_apply(scs_handle* h, const Vec& V);
+
 // one ADMM iteration: the kernel sequence of kernels.cuh (with all-reduces
 // between kernels when rows are sharded)
 void enqueue_iteration(scs_handle* h) {
@@ -1980,10 +2020,23 @@ void enqueue_iteration(scs_handle* h) {
     k_cone_finish<<<1, kBlock, 0, h->st>>>(V, h->K);
     h->launches++;
   }
-  if (h->K.n_chunk > 0 || h->K.n_psd > 0) {
-    const int g = std::max(1, std::min(std::max(h->K.n_chunk, h->K.n_psd), h->grid_full));
+  launch_cone_apply(h, V);
+}
+
+// big SOCs and large PSD blocks (CTA each), then small PSD blocks (warp each)
+void launch_cone_apply(scs_handle* h, const Vec& V) {
+  const int n_big = h->K.n_psd - h->n_psd_small;
+  if (h->K.n_chunk > 0 || n_big > 0) {
+    const int g = std::max(1, std::min(std::max(h->K.n_chunk, n_big), h->grid_full));
     k_cone_apply<<<g, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side,
                                                       h->warp_side);
+    h->launches++;
+  }
+  if (h->n_psd_small > 0) {
+    const long long g = std::min<long long>((h->n_psd_small + kBlock / 32 - 1) / (kBlock / 32),
+                                            (long long)h->sms * 32);
+    k_psd_small<<<(int)g, kBlock, kPsdSmallSmem, h->st>>>(V, h->K, h->psd_small_list,
+                                                          h->n_psd_small);
     h->launches++;
   }
 }
@@ -2551,11 +2604,7 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t
     int g = std::max(elem_grid(h, work), std::min(h->K.n_chunk, h->grid_full));
     g = std::max(g, std::min((int)((h->K.n_ssoc * 32LL + kBlock - 1) / kBlock), h->grid_full));
     k_cone_tail<<<g, kBlock, 0, h->st>>>(V, h->K, 0);
-    if (h->K.n_chunk > 0 || h->K.n_psd > 0) {
-      const int ga = std::max(1, std::min(std::max(h->K.n_chunk, h->K.n_psd), h->grid_full));
-      k_cone_apply<<<ga, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side,
-                                                          h->warp_side);
-    }
+    launch_cone_apply(h, V);
     CK(cudaGetLastError());
     std::vector<double> res(len);
     d2h(h, res.data(), V.u, len);
