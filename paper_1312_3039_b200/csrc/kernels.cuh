@@ -60,6 +60,7 @@ struct Vec {
   const double* Minv;         // opt-in Jacobi PCG: 1 / diag(I + A^T A); nullptr = plain CG
   double *r, *Gp;             // CG vectors (n)
   double *X2, *Y2;            // interleaved gather vectors
+  double *P1;                 // compact copy of p = X2[2j] (stride-1 gathers of the later CG A passes)
   double *Axw;                // A cg_warm (m), from the previous EpiAFinal
   double *Aux;                // A u_x (m) for the split residual epilogue
   double *q;                  // A p (m)
@@ -357,9 +358,11 @@ struct EpiAtFirst : EpiBase {
     if (V.Minv) {  // opt-in PCG: p = z = M^-1 r, carry r'z
       const double z = p.mi * r;
       V.X2[2 * j] = z;
+      V.P1[j] = z;
       red[4] += r * z;
     } else {
       V.X2[2 * j] = r;
+      V.P1[j] = r;
     }
     if (pend) {
       const double du = p.ei * (s[1] / p.ut + p.c);
@@ -387,7 +390,8 @@ struct EpiAtFirst : EpiBase {
 // that iteration's termination check (solver.py:359-363).
 template <bool MERGED>
 struct EpiAp : EpiBase {
-  static constexpr int NV = MERGED ? 2 : 1, STRIDE = 2, NR = MERGED ? 3 : 0;
+  // MERGED gathers [p, u_x] from X2; plain passes gather p from its compact copy P1
+  static constexpr int NV = MERGED ? 2 : 1, STRIDE = MERGED ? 2 : 1, NR = MERGED ? 3 : 0;
   __device__ bool load() {
     const Ctl* c = V.ctl;
     pend = MERGED ? c->check_pending : 0;
@@ -613,6 +617,19 @@ struct EpiPlain : EpiBase {
   double* out;
   __device__ bool load() { return true; }
   __device__ void row(long long i, const double (&s)[1], const Pre&, double*) const { out[i] = s[0]; }
+  __device__ void finish(const double*) const {}
+};
+
+// Plain two-vector products from an interleaved vector (format self-checks).
+template <int NV_, int STRIDE_>
+struct EpiPlainN : EpiBase {
+  static constexpr int NV = NV_, STRIDE = STRIDE_, NR = 0;
+  double* out;  // rows * NV
+  __device__ bool load() { return true; }
+  __device__ void row(long long i, const double (&s)[NV], const Pre&, double*) const {
+#pragma unroll
+    for (int t = 0; t < NV; ++t) out[i * NV + t] = s[t];
+  }
   __device__ void finish(const double*) const {}
 };
 

@@ -15,6 +15,7 @@
 #include <condition_variable>
 #include <functional>
 #include <mutex>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -23,6 +24,7 @@
 #include "cones.cuh"
 #include "kernels.cuh"
 #include "tiled.cuh"
+#include "stream.cuh"
 
 #ifdef SCS_WITH_NCCL
 #include <nccl.h>
@@ -116,9 +118,17 @@ __global__ void __launch_bounds__(kBlock) k_cg_p(Vec V) {
   const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
   const long long nt = (long long)gridDim.x * kBlock;
   if (V.Minv)
-    for (long long j = tid; j < V.n; j += nt) V.X2[2 * j] = V.Minv[j] * V.r[j] + be * V.X2[2 * j];
+    for (long long j = tid; j < V.n; j += nt) {
+      const double pj = V.Minv[j] * V.r[j] + be * V.X2[2 * j];
+      V.X2[2 * j] = pj;
+      V.P1[j] = pj;
+    }
   else
-    for (long long j = tid; j < V.n; j += nt) V.X2[2 * j] = V.r[j] + be * V.X2[2 * j];
+    for (long long j = tid; j < V.n; j += nt) {
+      const double pj = V.r[j] + be * V.X2[2 * j];
+      V.X2[2 * j] = pj;
+      V.P1[j] = pj;
+    }
 }
 
 // relaxed point of element i of the (x, y) part:
@@ -697,7 +707,7 @@ __global__ void k_init_state(Vec V, const double* wx, const double* wy, const do
     }
     V.u[i] = u;
     V.v[i] = v;
-    if (i < n) { V.x[i] = 0.0; V.X2[2 * i] = 0.0; V.X2[2 * i + 1] = u; }
+    if (i < n) { V.x[i] = 0.0; V.X2[2 * i] = 0.0; V.P1[i] = 0.0; V.X2[2 * i + 1] = u; }
     if (i >= n && i < n + m) {
       V.Y2[2 * (i - n)] = 0.0;
       V.Y2[2 * (i - n) + 1] = u;
@@ -897,6 +907,16 @@ struct scs_handle {
   Tiled tA{}, tAt{};
   int tsub[2][3] = {}, tsplit[2][3] = {};  // [matrix][NV]
   double* Ptile = nullptr;
+  // TMA-streamed tiles (stream.cuh): format per matrix, schedules [matrix][pair]
+  bool stm_m[2] = {false, false};
+  Stm sF[2] = {};
+  struct Sched {
+    StmCmd* cmds = nullptr;
+    long long* coff = nullptr;
+    int G = 0, splits = 1;
+    long long ncmd = 0;
+  } ssch[2][2];
+  double* Pstm = nullptr;
   // row-banded CSR(A^T) (setup_bands): S*n rows, raw band partials
   int nband = 1, LAb = 32;
   int recur_refresh = 20;  // opt-in recurrence: direct A x every k iterations
@@ -971,7 +991,7 @@ void set_global_err(const std::string& s) {
 template <class T>
 T* dalloc(scs_handle* h, size_t count) {
   void* p = nullptr;
-  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T) + 16;  // +16: bulk-copy tails
   cudaError_t e = cudaMalloc(&p, bytes);
   if (e != cudaSuccess)
     throw Fail{SCS_ENOMEM, "cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e)};
@@ -1074,10 +1094,48 @@ void set_tiled_smem(int dev, size_t bytes) {
   if (bytes > (size_t)optin) throw Fail{SCS_EINVAL, "tiled SpMV: shared memory budget exceeded"};
 }
 
-// SpMV with the matrix A (mat = 0) or A^T (mat = 1): slab-tiled kernel when
-// the problem is large, CSR kernel otherwise.
+// Streamed-tile SpMV (stream.cuh).  NV = 1 passes run pair units (two
+// sub-blocks share every slab load), NV = 2 passes single sub-blocks; the
+// shared-memory ring gets as many 'cap'-byte stages (<= 4) as fit beside
+// the accumulators and the two slab buffers.
+template <int NV, int STRIDE, class Epi>
+void launch_stream(scs_handle* h, int mat, const Epi& epi) {
+  const Stm& F = h->sF[mat];
+  const auto& S = h->ssch[mat][NV == 1 ? 1 : 0];
+  static std::once_flag once;
+  static int optin = 0;
+  std::call_once(once, [&] {
+    int dev_optin = 0;
+    cudaDeviceGetAttribute(&dev_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_stream<NV, STRIDE, Epi>);
+    optin = dev_optin - (int)fa.sharedSizeBytes;
+    cudaFuncSetAttribute(k_stream<NV, STRIDE, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaGetLastError();
+  });
+  const size_t fixed = kStmAccBytes + 2 * (size_t)F.W * STRIDE * 8 + kStmMaxStages * (2 * 8 + 16);
+  const int NS = (int)std::min<long long>(kStmMaxStages, ((long long)optin - (long long)fixed) / F.cap);
+  if (NS < 2) throw Fail{SCS_EINVAL, "streamed SpMV: shared memory budget exceeded"};
+  const size_t smem = fixed + (size_t)NS * F.cap;
+  const Csr& M = mat == 0 ? h->A : h->At;
+  k_stream<NV, STRIDE, Epi><<<S.G, kStmThreads, smem, h->st>>>(F, S.cmds, S.coff, M, epi, S.splits,
+                                                              h->Pstm, NS);
+  CK(cudaGetLastError());
+  h->launches++;
+  if (S.splits > 1) {
+    k_tiled_combine<Epi><<<elem_grid(h, F.rows), kBlock, 0, h->st>>>(h->Pstm, S.splits, F.rows, epi);
+    h->launches++;
+  }
+}
+
+// SpMV with the matrix A (mat = 0) or A^T (mat = 1): streamed tiles, slab-
+// tiled kernel or CSR kernel, as chosen at setup.
 template <class Epi>
 void launch_mat(scs_handle* h, int mat, const Epi& epi) {
+  if (h->stm_m[mat] && ((uintptr_t)epi.xb & 15) == 0) {
+    launch_stream<Epi::NV, Epi::STRIDE, Epi>(h, mat, epi);
+    return;
+  }
   if (h->split_m[mat]) {  // long rows in pieces: raw piece products, then per-row sums
     EpiRaw<Epi> raw{};
     static_cast<Epi&>(raw) = epi;
@@ -1301,7 +1359,7 @@ void setup_tiled(scs_handle* h) {
     const double rows = mat == 0 ? h->m : h->n, cols = mat == 0 ? h->n : h->m;
     const double seg = (double)h->nnz / std::max(rows, 1.0) * std::min(1.0, W / std::max(cols, 1.0));
     const bool want = force == 1 || (h->nnz >= 4000000LL && seg >= 3.0);
-    if (!want) continue;
+    if (!want || h->stm_m[mat]) continue;
     Tiled& T = mat == 0 ? h->tA : h->tAt;
     build_tiled(h, mat == 0 ? h->A : h->At, mat == 0 ? h->n : h->m, T);
     tile_shapes(h, mat, T, h->nnz);
@@ -1319,6 +1377,432 @@ void setup_tiled(scs_handle* h) {
       (int)h->tiled_m[0], h->tA.NB, h->tA.S, h->tsub[0][1], h->tsplit[0][1], h->tsub[0][2],
       h->tsplit[0][2], (int)h->tiled_m[1], h->tAt.NB, h->tAt.S, h->tsub[1][1], h->tsplit[1][1],
       h->tsub[1][2], h->tsplit[1][2]);
+}
+
+// ---------------------------------------------------------------------------
+// TMA-streamed tiles (stream.cuh): format build and per-CTA schedules.
+// ---------------------------------------------------------------------------
+long long env_ll(const char* name, long long dflt) {
+  const char* e = getenv(name);
+  return e ? atoll(e) : dflt;
+}
+
+// Host-side tile table of one streamed matrix, kept only during setup.
+struct StmTiles {
+  int NB = 0, S = 0;
+  std::vector<char> tiled;            // per sub-block: 1 tiled, 0 CSR
+  std::vector<long long> pf;          // per tile: first piece (-1: none)
+  std::vector<int> np;                // per tile: pieces
+  std::vector<long long> slots;       // per tile
+  std::vector<unsigned long long> poff;
+  std::vector<unsigned> pslots;
+  std::vector<long long> nnz_sb;      // per sub-block (CSR units' cost)
+};
+
+// Units -> LPT over persistent CTAs -> flat command lists (stream.cuh).
+void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T) {
+  const Stm& F = h->sF[mat];
+  struct Unit { long long sb0; int nsb; bool csr; int s_lo, s_hi, sp; double cost; };
+  std::vector<Unit> units;
+  long long ntiled = 0;
+  for (long long sb = 0; sb < T.NB;) {
+    if (!T.tiled[sb]) {
+      units.push_back({sb, 1, true, 0, 0, 0, 0.0});
+      ++sb;
+      continue;
+    }
+    const int nsb = (pair && sb + 1 < T.NB && T.tiled[sb + 1]) ? 2 : 1;
+    units.push_back({sb, nsb, false, 0, T.S, 0, 0.0});
+    ++ntiled;
+    sb += nsb;
+  }
+  const int G0 = h->sms;
+  int splits = 1;
+  if (ntiled > 0 && ntiled < 4LL * G0)
+    splits = (int)std::min<long long>(std::min<long long>(32, T.S), (4LL * G0 + ntiled - 1) / ntiled);
+  splits = (int)env_ll("SCS_STREAM_SPLITS", splits);
+  splits = std::max(1, std::min(splits, std::max(1, T.S)));
+  if (splits > 255) splits = 255;
+  const double slab_cost = (double)F.W * 8.0 * (pair ? 1.5 : 2.0);
+  std::vector<Unit> all;
+  for (const Unit& u : units) {
+    if (u.csr) {
+      Unit v = u;
+      v.cost = 44.0 * (double)T.nnz_sb[u.sb0] + 16.0 * kStmRS + 2e4;
+      all.push_back(v);
+      continue;
+    }
+    // per-slab slots of this unit, split into `splits` equal-slot slab ranges
+    std::vector<double> cum(T.S + 1, 0.0);
+    std::vector<int> nslab(T.S + 1, 0);
+    for (int s = 0; s < T.S; ++s) {
+      double a = 0.0;
+      bool any = false;
+      for (int q = 0; q < u.nsb; ++q) {
+        const long long t = (u.sb0 + q) * T.S + s;
+        a += 12.0 * (double)T.slots[t] + 2048.0 * T.np[t];  // + per-stage overhead
+        any = any || T.np[t] > 0;
+      }
+      cum[s + 1] = cum[s] + a + (any ? slab_cost : 0.0);
+    }
+    int lo = 0;
+    for (int sp = 0; sp < splits; ++sp) {
+      int hi = T.S;
+      if (sp + 1 < splits) {
+        const double target = cum[T.S] * (sp + 1) / splits;
+        hi = (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+        hi = std::max(lo, std::min(hi, T.S));
+      }
+      Unit v = u;
+      v.s_lo = lo;
+      v.s_hi = hi;
+      v.sp = sp;
+      v.cost = cum[hi] - cum[lo] + 2e4 * u.nsb;
+      all.push_back(v);
+      lo = hi;
+    }
+  }
+  const int G = (int)std::max<long long>(1, std::min<long long>(G0, (long long)all.size()));
+  std::vector<int> ord(all.size());
+  for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return all[a].cost > all[b].cost; });
+  std::vector<std::vector<int>> cta(G);
+  std::priority_queue<std::pair<double, int>, std::vector<std::pair<double, int>>,
+                      std::greater<std::pair<double, int>>> pq;
+  for (int g = 0; g < G; ++g) pq.push({0.0, g});
+  for (int i : ord) {
+    auto top = pq.top();
+    pq.pop();
+    cta[top.second].push_back(i);
+    pq.push({top.first + all[i].cost, top.second});
+  }
+  std::vector<StmCmd> cmds;
+  std::vector<long long> coff(G + 1, 0);
+  for (int g = 0; g < G; ++g) {
+    coff[g] = (long long)cmds.size();
+    for (int ui : cta[g]) {
+      const Unit& u = all[ui];
+      const size_t first = cmds.size();
+      const unsigned short pf = (unsigned short)(u.nsb == 2 ? STM_PAIR : 0);
+      if (u.csr) {
+        StmCmd c{};
+        c.row0 = u.sb0 * kStmRS;
+        c.flags = STM_CSR | STM_END;
+        cmds.push_back(c);
+        continue;
+      }
+      for (int s = u.s_lo; s < u.s_hi; ++s)
+        for (int q = 0; q < u.nsb; ++q) {
+          const long long t = (u.sb0 + q) * T.S + s;
+          for (int j = 0; j < T.np[t]; ++j) {
+            const long long p = T.pf[t] + j;
+            StmCmd c{};
+            c.off = T.poff[p];
+            c.bytes = (unsigned)(kStmHdr + 12ULL * T.pslots[p]);
+            c.slab = (unsigned)s;
+            c.row0 = u.sb0 * kStmRS;
+            c.flags = pf;
+            c.half = (unsigned char)q;
+            c.sp = (unsigned char)u.sp;
+            cmds.push_back(c);
+          }
+        }
+      if (cmds.size() == first) {  // nothing in range: header-only stage closes the unit
+        StmCmd c{};
+        c.row0 = u.sb0 * kStmRS;
+        c.flags = pf;
+        c.sp = (unsigned char)u.sp;
+        cmds.push_back(c);
+      }
+      cmds.back().flags |= STM_END;
+    }
+  }
+  coff[G] = (long long)cmds.size();
+  auto& S = h->ssch[mat][pair];
+  S.cmds = dalloc<StmCmd>(h, cmds.size());
+  S.coff = dalloc<long long>(h, G + 1);
+  h2d(h, S.cmds, cmds.data(), cmds.size());
+  h2d(h, S.coff, coff.data(), G + 1);
+  S.G = G;
+  S.splits = splits;
+  S.ncmd = (long long)cmds.size();
+  dbg("stream sched mat=%d pair=%d units=%zu tiled=%lld splits=%d G=%d cmds=%zu", mat, pair,
+      all.size(), ntiled, splits, G, cmds.size());
+}
+
+void build_stream(scs_handle* h, int mat) {
+  const Csr& M = mat == 0 ? h->A : h->At;
+  const long long rows = M.rows, cols = mat == 0 ? h->n : h->m;
+  const long long nz = read_dev(h, M.rp + rows);
+  Stm& F = h->sF[mat];
+  F.rows = rows;
+  F.cols = cols;
+  F.W = (int)std::min<long long>(65536, std::max<long long>(8, env_ll("SCS_STREAM_W", 2048)));
+  F.cap = (int)(env_ll("SCS_STREAM_CAP", 32768) & ~15LL);
+  const int min_cap = kStmHdr + 12 * 32 * kStmWarps;
+  if (F.cap < min_cap) F.cap = (min_cap + 15) & ~15;
+  F.S = (int)((cols + F.W - 1) / F.W);
+  F.NB = (int)((rows + kStmRS - 1) / kStmRS);
+  const long long ntile = (long long)F.NB * F.S, nsec = ntile * kStmWarps;
+  if (nsec >= (1LL << 31) - 1 || nz >= (1LL << 31) - 1 || nz == 0)
+    throw Fail{SCS_EINVAL, "streamed layout: too many sections or nonzeros"};
+  // 1. entries by warp section (stable: row-major inside)
+  int* rowid = dalloc<int>(h, nz);
+  int* key = dalloc<int>(h, nz);
+  int* skey = dalloc<int>(h, nz);
+  int* perm_in = dalloc<int>(h, nz);
+  int* perm = dalloc<int>(h, nz);
+  k_expand_rows<<<elem_grid(h, rows * 32), kBlock, 0, h->st>>>(M.rp, rows, rowid);
+  k_stm_keys<<<elem_grid(h, nz), kBlock, 0, h->st>>>(rowid, M.ci, nz, F.W, F.S, key);
+  k_iota<<<elem_grid(h, nz), kBlock, 0, h->st>>>(perm_in, nz);
+  int bits = 1;
+  while ((1LL << bits) < nsec) ++bits;
+  {
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const int*)key, skey, (const int*)perm_in, perm,
+                                       (int)nz, 0, bits, h->st));
+    void* tmp = dalloc<char>(h, tb);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, (const int*)key, skey, (const int*)perm_in, perm,
+                                       (int)nz, 0, bits, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    dfree(h, tmp);
+  }
+  dfree(h, key);
+  // 2. row segments
+  int* flag = perm_in;
+  int* incl = dalloc<int>(h, nz);
+  k_seg_flags<<<elem_grid(h, nz), kBlock, 0, h->st>>>(skey, perm, rowid, nz, flag);
+  {
+    size_t tb = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flag, incl, (int)nz, h->st));
+    void* tmp = dalloc<char>(h, tb);
+    CK(cub::DeviceScan::InclusiveSum(tmp, tb, flag, incl, (int)nz, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    dfree(h, tmp);
+  }
+  const long long nseg = read_dev(h, incl + nz - 1);
+  long long* seg_start = dalloc<long long>(h, nseg);
+  k_seg_starts<<<elem_grid(h, nz), kBlock, 0, h->st>>>(flag, incl, nz, seg_start);
+  dfree(h, incl);
+  // 3. segments by (section, length desc)
+  unsigned long long* key2 = dalloc<unsigned long long>(h, nseg);
+  unsigned long long* key2s = dalloc<unsigned long long>(h, nseg);
+  int* sec_of = dalloc<int>(h, nseg);
+  int* sidx = dalloc<int>(h, nseg);
+  int* order = dalloc<int>(h, nseg);
+  k_seg_keys<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(seg_start, nseg, nz, skey, key2, sec_of);
+  k_iota<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(sidx, nseg);
+  {
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned long long*)key2, key2s,
+                                       (const int*)sidx, order, (int)nseg, 0, 20 + bits, h->st));
+    void* tmp = dalloc<char>(h, tb);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, (const unsigned long long*)key2, key2s,
+                                       (const int*)sidx, order, (int)nseg, 0, 20 + bits, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    dfree(h, tmp);
+  }
+  int* sec_sorted = sec_of;
+  k_key_hi<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(key2s, nseg, sec_sorted);
+  dfree(h, key2);
+  dfree(h, key2s);
+  dfree(h, sidx);
+  dfree(h, skey);
+  // 4. lanes: first-fit-decreasing per section
+  long long* sec_ptr = dalloc<long long>(h, nsec + 1);
+  k_rowptr<<<elem_grid(h, nsec + 1), kBlock, 0, h->st>>>(sec_sorted, nseg, nsec, sec_ptr);
+  int* seg_lane = dalloc<int>(h, nseg);
+  int* seg_k0 = dalloc<int>(h, nseg);
+  unsigned short* depth = dalloc<unsigned short>(h, nsec);
+  k_stm_ffd<<<elem_grid(h, nsec), kBlock, 0, h->st>>>(sec_ptr, nsec, order, seg_start, nseg, nz,
+                                                      seg_lane, seg_k0, depth);
+  CK(cudaGetLastError());
+  std::vector<unsigned short> D(nsec);
+  d2h(h, D.data(), depth, nsec);
+  std::vector<long long> rp_h(rows + 1);
+  d2h(h, rp_h.data(), M.rp, rows + 1);
+  CK(cudaStreamSynchronize(h->st));
+  dfree(h, depth);
+  dfree(h, sec_ptr);
+  // 5. host: tiled sub-blocks, pieces, blob offsets
+  StmTiles T;
+  T.NB = F.NB;
+  T.S = F.S;
+  T.tiled.assign(F.NB, 1);
+  T.pf.assign(ntile, -1);
+  T.np.assign(ntile, 0);
+  T.slots.assign(ntile, 0);
+  T.nnz_sb.assign(F.NB, 0);
+  const long long min_avg = env_ll("SCS_STREAM_MIN", 768);
+  for (long long sb = 0; sb < F.NB; ++sb) {
+    const long long r0 = sb * kStmRS, r1 = std::min(rows, r0 + kStmRS);
+    T.nnz_sb[sb] = rp_h[r1] - rp_h[r0];
+    long long sl = 0, nt = 0;
+    for (long long s = 0; s < F.S; ++s) {
+      long long a = 0;
+      for (int w = 0; w < kStmWarps; ++w) a += 32LL * D[(sb * F.S + s) * kStmWarps + w];
+      T.slots[sb * F.S + s] = a;
+      sl += a;
+      nt += a > 0;
+    }
+    // CSR units only for short rows (the consumers run them at 4 lanes per row)
+    T.tiled[sb] = (nt == 0 || sl >= min_avg * nt || T.nnz_sb[sb] > 16 * (r1 - r0)) ? 1 : 0;
+  }
+  std::vector<unsigned short> tile_kp(ntile, 1), pwsec;
+  long long npiece = 0;
+  unsigned long long bytes = 0;
+  for (long long t = 0; t < ntile; ++t) {
+    if (!T.tiled[t / F.S] || T.slots[t] == 0) continue;
+    const unsigned short* d = &D[t * kStmWarps];
+    int maxd = 0;
+    for (int w = 0; w < kStmWarps; ++w) maxd = std::max<int>(maxd, d[w]);
+    int np = (int)std::max<long long>(1, (12 * T.slots[t] + (F.cap - kStmHdr) - 1) / (F.cap - kStmHdr));
+    int kp = 0;
+    for (;; ++np) {
+      kp = (maxd + np - 1) / np;
+      long long first = 0;  // piece 0 is the largest
+      for (int w = 0; w < kStmWarps; ++w) first += std::min<int>(d[w], kp);
+      if (kStmHdr + 12LL * 32 * first <= F.cap) break;
+    }
+    np = (maxd + kp - 1) / kp;
+    tile_kp[t] = (unsigned short)kp;
+    T.pf[t] = npiece;
+    T.np[t] = np;
+    for (int j = 0; j < np; ++j) {
+      unsigned short acc = 0;
+      pwsec.push_back(0);
+      for (int w = 0; w < kStmWarps; ++w) {
+        const int st = std::max(0, std::min<int>(d[w] - j * kp, kp));
+        acc = (unsigned short)(acc + st);
+        pwsec.push_back(acc);
+      }
+      const unsigned ns = 32u * acc;
+      T.poff.push_back(bytes);
+      T.pslots.push_back(ns);
+      bytes += kStmHdr + 12ULL * ns;
+      ++npiece;
+    }
+  }
+  // 6. device blob
+  unsigned char* blob = dalloc<unsigned char>(h, std::max<unsigned long long>(bytes, 16));
+  long long* d_pf = dalloc<long long>(h, ntile);
+  unsigned short* d_kp = dalloc<unsigned short>(h, ntile);
+  unsigned long long* d_poff = dalloc<unsigned long long>(h, npiece);
+  unsigned* d_pslots = dalloc<unsigned>(h, npiece);
+  unsigned short* d_pwsec = dalloc<unsigned short>(h, pwsec.size());
+  h2d(h, d_pf, T.pf.data(), ntile);
+  h2d(h, d_kp, tile_kp.data(), ntile);
+  h2d(h, d_poff, T.poff.data(), npiece);
+  h2d(h, d_pslots, T.pslots.data(), npiece);
+  h2d(h, d_pwsec, pwsec.data(), pwsec.size());
+  if (npiece) {
+    k_stm_init<<<elem_grid(h, npiece * 32), kBlock, 0, h->st>>>(blob, d_poff, d_pslots, d_pwsec, npiece);
+    k_stm_scatter<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(sec_sorted, order, seg_start, nseg, nz,
+                                                            seg_lane, seg_k0, perm, rowid, M.ci, M.v,
+                                                            d_pf, d_kp, d_poff, d_pslots, d_pwsec,
+                                                            F.W, blob);
+    CK(cudaGetLastError());
+  }
+  CK(cudaStreamSynchronize(h->st));
+  for (void* p : {(void*)d_pf, (void*)d_kp, (void*)d_poff, (void*)d_pslots, (void*)d_pwsec,
+                  (void*)seg_lane, (void*)seg_k0, (void*)sec_sorted, (void*)order, (void*)seg_start,
+                  (void*)perm_in, (void*)perm, (void*)rowid})
+    dfree(h, p);
+  F.blob = blob;
+  long long ncsr = 0;
+  for (long long sb = 0; sb < F.NB; ++sb) ncsr += !T.tiled[sb];
+  dbg("stream layout mat=%d rows=%lld cols=%lld nnz=%lld W=%d S=%d NB=%d csr_sb=%lld pieces=%lld "
+      "bytes=%llu (%.2f B/nnz)", mat, rows, cols, nz, F.W, F.S, F.NB, ncsr, npiece, bytes,
+      (double)bytes / (double)nz);
+  for (int pair = 0; pair < 2; ++pair) build_stm_sched(h, mat, pair, T);
+}
+
+__global__ void k_hash_fill(double* x, long long n, unsigned seed) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) {
+    unsigned long long z = (unsigned long long)i * 0x9E3779B97F4A7C15ULL + seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    x[i] = (double)((z ^ (z >> 31)) >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+  }
+}
+
+// SCS_STREAM_CHECK=1: streamed products against the CSR kernel for every
+// (NV, STRIDE) shape the iteration uses; max |difference| to stderr.
+void stm_selfcheck(scs_handle* h) {
+  for (int mat = 0; mat < 2; ++mat) {
+    const long long rows = mat == 0 ? h->m : h->n, cols = mat == 0 ? h->n : h->m;
+    double* x = dalloc<double>(h, 2 * cols);
+    double* o1 = dalloc<double>(h, 2 * rows);
+    double* o2 = dalloc<double>(h, 2 * rows);
+    k_hash_fill<<<elem_grid(h, 2 * cols), kBlock, 0, h->st>>>(x, 2 * cols, 17u + mat);
+    auto cmp = [&](const char* what, long long len) {
+      std::vector<double> a(len), b(len);
+      d2h(h, a.data(), o1, len);
+      d2h(h, b.data(), o2, len);
+      CK(cudaStreamSynchronize(h->st));
+      double mx = 0.0, sc = 0.0;
+      long long arg = -1;
+      for (long long i = 0; i < len; ++i) {
+        const double d = std::fabs(a[i] - b[i]);
+        if (!(d <= mx)) { mx = d; arg = i; }
+        sc = std::max(sc, std::fabs(b[i]));
+      }
+      fprintf(stderr, "[scs] stream check mat=%d %s max|diff|=%.3e at %lld (scale %.3e)\n", mat, what,
+              mx, arg, sc);
+    };
+    {
+      EpiPlainN<1, 1> e{};
+      e.V = h->V; e.xb = x; e.out = o1;
+      launch_stream<1, 1>(h, mat, e);
+      e.out = o2;
+      launch_spmv(h, mat == 0 ? h->A : h->At, mat == 0 ? h->LA : h->LAt, e);
+      cmp("nv1s1", rows);
+    }
+    {
+      EpiPlainN<1, 2> e{};
+      e.V = h->V; e.xb = x; e.out = o1;
+      launch_stream<1, 2>(h, mat, e);
+      e.out = o2;
+      launch_spmv(h, mat == 0 ? h->A : h->At, mat == 0 ? h->LA : h->LAt, e);
+      cmp("nv1s2", rows);
+    }
+    {
+      EpiPlainN<2, 2> e{};
+      e.V = h->V; e.xb = x; e.out = o1;
+      launch_stream<2, 2>(h, mat, e);
+      e.out = o2;
+      launch_spmv(h, mat == 0 ? h->A : h->At, mat == 0 ? h->LA : h->LAt, e);
+      cmp("nv2s2", 2 * rows);
+    }
+    dfree(h, x);
+    dfree(h, o1);
+    dfree(h, o2);
+  }
+}
+
+// Streamed tiles for large matrices (SCS_STREAM=0 off, 1 force on).
+void setup_stream(scs_handle* h) {
+  const long long force = env_ll("SCS_STREAM", -1);
+  if (force == 0 || h->nnz == 0) return;
+  if (force < 0 && h->nnz < 20000000LL) return;
+  size_t need = 0;
+  for (int mat = 0; mat < 2; ++mat) {
+    // where a row meets a 4096-column slab >= 3 times on average the slab-
+    // tiled SELL kernel (tiled.cuh) is faster (config 3); streamed tiles
+    // win on wide matrices with short row segments (config 5)
+    const double rows = mat == 0 ? h->m : h->n, cols = mat == 0 ? h->n : h->m;
+    const double seg = (double)h->nnz / std::max(rows, 1.0) * std::min(1.0, 4096.0 / std::max(cols, 1.0));
+    if (force < 0 && seg >= 3.0) continue;
+    build_stream(h, mat);
+    h->stm_m[mat] = true;
+    for (int pair = 0; pair < 2; ++pair)
+      if (h->ssch[mat][pair].splits > 1)
+        need = std::max<size_t>(need, (size_t)h->ssch[mat][pair].splits * h->sF[mat].rows * 2);
+  }
+  if (need) h->Pstm = dalloc<double>(h, need);
+  if (env_ll("SCS_STREAM_CHECK", 0)) stm_selfcheck(h);
 }
 
 __global__ void k_pcg_diag(const double* colsq, long long n, double* out) {
@@ -1350,7 +1834,7 @@ void setup_pcg(scs_handle* h) {
 // summed by the epilogue kernel.  Used when 16m > 64 MB and A^T is not
 // slab-tiled; SCS_BANDS=k forces k bands (1 = off).
 void setup_bands(scs_handle* h) {
-  if (h->tiled_m[1] || h->nnz == 0 || h->m < 2) return;
+  if (h->tiled_m[1] || h->stm_m[1] || h->nnz == 0 || h->m < 2) return;
   const char* env = getenv("SCS_BANDS");
   long long S = env ? atoll(env) : -1;
   if (S < 0) {
@@ -1404,7 +1888,7 @@ void setup_split(scs_handle* h) {
   if (force == 0 || h->nnz == 0) return;
   size_t need = 0;
   for (int mat = 0; mat < 2; ++mat) {
-    if (h->tiled_m[mat] || (mat == 1 && h->nband > 1)) continue;
+    if (h->tiled_m[mat] || h->stm_m[mat] || (mat == 1 && h->nband > 1)) continue;
     const Csr& M = mat == 0 ? h->A : h->At;
     const long long rows = M.rows;
     std::vector<long long> rp(rows + 1);
@@ -1519,7 +2003,7 @@ void y_rows(scs_handle* h, const double* T, Epi epi) {
 // final A pass of solve_kkt: z_y = rhs_y + A x (embedding.py:113)
 void a_final(scs_handle* h, const Vec& V, double* zy_out, int setup) {
   const bool recur = !setup && (h->set.fast & SCS_FAST_RECURRENCE);
-  if (!h->tiled_m[0] || recur) {
+  if (!(h->tiled_m[0] || h->stm_m[0]) || recur) {
     EpiAxPlain ax{};
     ax.V = V;
     ax.xb = V.x;
@@ -1913,7 +2397,7 @@ void check_err(scs_handle* h) {
 // one CG step (A p, A^T, update, p update); the first step of an ADMM
 // iteration also closes the previous iteration's termination check
 void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p, bool merged, bool recur) {
-  if (merged && !h->tiled_m[0]) {  // CSR: plain SpMV + elementwise residual pass
+  if (merged && !(h->tiled_m[0] || h->stm_m[0])) {  // CSR: plain SpMV + elementwise residual pass
     EpiApPlain2 ea{};
     ea.V = V;
     ea.xb = V.X2;
@@ -1929,7 +2413,7 @@ void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p, bool merge
   } else {
     EpiAp<false> ea{};
     ea.V = V;
-    ea.xb = V.X2;
+    ea.xb = V.P1;
     a_pass(h, ea);
   }
   EpiAtGp eg{};
@@ -2360,6 +2844,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     V.r = dalloc<double>(h, n);
     V.Gp = dalloc<double>(h, n);
     V.X2 = dalloc<double>(h, 2 * n);
+    V.P1 = dalloc<double>(h, n);
     V.Y2 = dalloc<double>(h, 2 * m);
     V.rhs_y = dalloc<double>(h, m);
     V.Axw = dalloc<double>(h, m);
@@ -2396,6 +2881,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     k_recip<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->D, m, (double*)V.Dinv);
     k_recip<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->E, n, (double*)V.Einv);
     dbg("equilibrated mean_col=%g mean_row=%g", h->mean_col, h->mean_row);
+    setup_stream(h);
     setup_tiled(h);
     setup_pcg(h);
     setup_bands(h);
@@ -2583,6 +3069,7 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t
     V.gy = dalloc<double>(h, m);
     V.zy = dalloc<double>(h, m);
     V.X2 = dalloc<double>(h, 2 * n);
+    V.P1 = dalloc<double>(h, n);
     V.Y2 = dalloc<double>(h, 2 * m);
     double* zc = dalloc<double>(h, std::max<long long>(n, m));
     V.c = zc; V.b = zc;
@@ -2658,7 +3145,7 @@ int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms, double* 
       if (kind == 0) {
         EpiAp<false> ea{};
         ea.V = h->V;
-        ea.xb = h->V.X2;
+        ea.xb = h->V.P1;
         launch_mat(h, 0, ea);
       } else {
         EpiAtGp eg{};

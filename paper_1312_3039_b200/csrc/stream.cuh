@@ -1,0 +1,458 @@
+// stream.cuh -- TMA-streamed slab-tiled SpMV (sm_100a).
+//
+// Why: the CSR kernels are bound by the L2 slice throughput, not by HBM --
+// every random gather x[col] costs a 32-byte sector for 8-16 useful bytes
+// (config 5: 32 GB of gather sectors + 12 GB of matrix per pass,
+// profiles/r01_ncu_c5_spmv_banded.txt).  The earlier slab-tiled kernel
+// (tiled.cuh) moved the gathers into shared memory but loaded the matrix
+// with ordinary per-chunk loads whose latency it could not cover at
+// config 5's ~1-2 entries per row segment.  This kernel keeps the idea and
+// moves every byte of the matrix and of the gathered vector with the
+// Tensor Memory Accelerator's bulk copies into a multi-stage shared-memory
+// ring, so the consumers never touch global memory in the inner loop:
+//
+//  * format (built once, after equilibration): rows in sub-blocks of
+//    kStmRS = 4096 rows = 16 warp sections of 256 rows; columns in slabs of
+//    W columns.  A tile = (sub-block, slab).  Inside a warp section the row
+//    segments (a row's entries in the slab, column order kept) are packed
+//    onto 32 lanes by first-fit-decreasing into a depth of D steps; step k
+//    of all 32 lanes is contiguous (coalesced shared-memory reads, no
+//    padding but the lane tails).  Every tile is cut into pieces of at
+//    most `cap` bytes (a piece = a step range of every section) and each
+//    piece is one contiguous blob: header, fp64 values, u32 (local row << 16
+//    | column - slab start).  Sub-blocks whose tiles are too sparse to pay
+//    for a slab load (config 5: A^T rows of the t-variables, two entries
+//    each) stay CSR units, computed from the CSR arrays by the consumers;
+//  * schedule (host, at setup): a unit = one sub-block (NV = 2) or a pair of
+//    sub-blocks sharing the slab loads (NV = 1), optionally split over slab
+//    ranges when there are too few units for 148 SMs; units are placed on
+//    persistent CTAs by longest-processing-time first, and each CTA gets a
+//    flat command list (one command per piece, in order);
+//  * kernel: one producer warp walks the command list and issues, per
+//    stage, the bulk copy of the piece and -- when the slab changes -- of
+//    the slab of the gathered vector (double-buffered) onto a full
+//    mbarrier with expect_tx; 16 consumer warps wait on it, each walks its
+//    own section (lane-local running row sum, flushed into a shared
+//    accumulator when the row changes: each row lives in exactly one lane
+//    of one warp per piece, so updates are exclusive and their order is
+//    fixed -- deterministic), then releases the stage on an empty mbarrier.
+//    At the end of a unit each warp runs the pass's per-row epilogue
+//    (Epi::row) over its own rows -- or writes split partials that
+//    k_tiled_combine sums in split order -- and the CTA's reductions go
+//    through the usual deterministic grid_sum_last.
+#pragma once
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace scs {
+
+constexpr int kStmRS = 4096;        // rows per sub-block
+constexpr int kStmSecRows = 256;    // rows per warp section
+constexpr int kStmWarps = kStmRS / kStmSecRows;  // 16 consumer warps
+constexpr int kStmThreads = (kStmWarps + 1) * 32;
+constexpr int kStmHdr = 48;         // piece header bytes: u32 nslots, u16 wsec[17]
+constexpr int kStmAccBytes = 2 * kStmRS * 8;
+constexpr int kStmMaxStages = 4;
+constexpr unsigned kStmSentinel = 0xffff0000u;  // padding slot: no row
+
+enum : unsigned short { STM_END = 1, STM_CSR = 2, STM_PAIR = 4, STM_TILE = 8 };
+
+struct StmCmd {
+  unsigned long long off;  // blob byte offset
+  unsigned bytes;          // blob bytes (0: header-only stage)
+  unsigned slab;
+  long long row0;          // first row of the unit
+  unsigned short flags;
+  unsigned char half;      // sub-block within a pair unit
+  unsigned char sp;        // split index (raw partial slot)
+  unsigned pad;
+};
+static_assert(sizeof(StmCmd) == 32, "StmCmd layout");
+
+struct Stm {
+  long long rows, cols;
+  int W, S, NB, cap;
+  const unsigned char* blob;
+};
+
+struct StmCtl {  // per stage, written by the producer before its arrive
+  long long row0;
+  unsigned short flags;
+  unsigned char half, sp;
+  int xbuf;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "STM_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra STM_WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, unsigned bytes,
+                                               unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Epilogue (or raw split partials) for rows [r0, r1) owned by this lane's
+// warp, reading and clearing the shared accumulator `a` (NV per row).
+template <int NV, class Epi>
+__device__ __forceinline__ void stm_rows(Epi& epi, double* a, long long r0, int cnt, int splits,
+                                         int sp, long long rows, double* P, double* red) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < cnt; i += 32) {
+    const long long r = r0 + i;
+    double sv[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) { sv[t] = a[i * NV + t]; a[i * NV + t] = 0.0; }
+    if (splits > 1) {
+#pragma unroll
+      for (int t = 0; t < NV; ++t) P[((long long)sp * rows + r) * NV + t] = sv[t];
+    } else {
+      typename Epi::Pre pre;
+      epi.pre(r, pre);
+      epi.row(r, sv, pre, red);
+    }
+  }
+}
+
+template <int NV, int STRIDE, class Epi>
+__global__ void __launch_bounds__(kStmThreads, 1)
+    k_stream(Stm F, const StmCmd* __restrict__ cmds, const long long* __restrict__ coff, Csr M,
+             Epi epi0, int splits, double* P, int NS) {
+  Epi epi = epi0;
+  if (!epi.load()) return;
+  extern __shared__ __align__(128) unsigned char stm_sm[];
+  double* acc = reinterpret_cast<double*>(stm_sm);
+  const int xbytes = F.W * STRIDE * 8;
+  double* xbuf0 = reinterpret_cast<double*>(stm_sm + kStmAccBytes);
+  unsigned char* stages = stm_sm + kStmAccBytes + 2 * xbytes;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(stages + (size_t)NS * F.cap);
+  unsigned long long* empty = full + kStmMaxStages;
+  StmCtl* sctl = reinterpret_cast<StmCtl*>(empty + kStmMaxStages);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kStmAccBytes / 8; i += blockDim.x) acc[i] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kStmWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const long long c0 = coff[blockIdx.x], c1 = coff[blockIdx.x + 1];
+  constexpr int NR = Epi::NR > 0 ? Epi::NR : 1;
+  double red[NR];
+#pragma unroll
+  for (int t = 0; t < NR; ++t) red[t] = 0.0;
+
+  if (warp == kStmWarps) {
+    // ---------------- producer warp ----------------
+    unsigned long long pol = 0;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    long long slab_cur = -1;
+    int xb = 1;
+    long long last0 = -1, last1 = -1;  // last stage that read slab buffer 0 / 1
+    for (long long base = c0; base < c1; base += 32) {
+      StmCmd mine{};
+      if (base + lane < c1) mine = cmds[base + lane];
+      const int cnt = (int)(c1 - base < 32 ? c1 - base : 32);
+      for (int j = 0; j < cnt; ++j) {
+        const unsigned long long off = __shfl_sync(0xffffffffu, mine.off, j);
+        const unsigned bytes = __shfl_sync(0xffffffffu, mine.bytes, j);
+        const unsigned slab = __shfl_sync(0xffffffffu, mine.slab, j);
+        const long long row0 = __shfl_sync(0xffffffffu, mine.row0, j);
+        const unsigned fl = __shfl_sync(0xffffffffu, (unsigned)mine.flags | ((unsigned)mine.half << 16) |
+                                                         ((unsigned)mine.sp << 24), j);
+        const long long i = base - c0 + j;
+        const int st = (int)(i % NS);
+        if (i >= NS) mbar_wait(empty + st, (unsigned)((i / NS - 1) & 1));
+        const bool tile = bytes > 0 && !(fl & STM_CSR);
+        unsigned slab_bytes = 0;
+        long long cstart = 0;
+        if (tile && (long long)slab != slab_cur) {
+          xb ^= 1;
+          const long long jlast = xb ? last1 : last0;
+          if (jlast >= 0 && jlast > i - NS) mbar_wait(empty + (int)(jlast % NS), (unsigned)((jlast / NS) & 1));
+          slab_cur = slab;
+          cstart = (long long)slab * F.W;
+          const long long wc = F.cols - cstart < F.W ? F.cols - cstart : F.W;
+          slab_bytes = (unsigned)(((wc * STRIDE * 8) + 15) & ~15LL);
+        }
+        if (tile) {
+          if (xb) last1 = i; else last0 = i;
+        }
+        if (lane == 0) {
+          StmCtl c;
+          c.row0 = row0;
+          c.flags = (unsigned short)((fl & 0xffff) | (tile ? STM_TILE : 0));
+          c.half = (unsigned char)((fl >> 16) & 0xff);
+          c.sp = (unsigned char)(fl >> 24);
+          c.xbuf = xb;
+          sctl[st] = c;
+          if (tile) {
+            mbar_arrive_tx(full + st, slab_bytes + bytes);
+            if (slab_bytes)
+              bulk_g2s_plain(xbuf0 + (size_t)xb * (xbytes / 8), epi.xb + cstart * STRIDE, slab_bytes,
+                             full + st);
+            bulk_g2s(stages + (size_t)st * F.cap, F.blob + off, bytes, full + st, pol);
+          } else {
+            mbar_arrive(full + st);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- consumer warps ----------------
+    const long long ncmd = c1 - c0;
+    for (long long i = 0; i < ncmd; ++i) {
+      const int st = (int)(i % NS);
+      mbar_wait(full + st, (unsigned)((i / NS) & 1));
+      const StmCtl c = sctl[st];
+      if (c.flags & STM_CSR) {
+        // sparse sub-block: L = 4 lanes per row straight from CSR
+        const long long r0 = c.row0 + (long long)warp * kStmSecRows;
+        const long long rend = (r0 + kStmSecRows < F.rows) ? r0 + kStmSecRows : F.rows;
+        const int gl = lane & 3, gi = lane >> 2;
+        for (long long rb = r0; rb < rend; rb += 8) {
+          const long long r = rb + gi;
+          const bool ok = r < rend;
+          long long k0 = 0, k1 = 0;
+          if (ok) { k0 = __ldg(M.rp + r); k1 = __ldg(M.rp + r + 1); }
+          double s[NV];
+          row_dot<4, NV, STRIDE>(M, k0, k1, gl, epi.xb, s);
+          if (ok && gl == 0) {
+            if (splits > 1) {
+              for (int q = 0; q < splits; ++q)
+#pragma unroll
+                for (int t = 0; t < NV; ++t) P[((long long)q * F.rows + r) * NV + t] = q == 0 ? s[t] : 0.0;
+            } else {
+              typename Epi::Pre pre;
+              epi.pre(r, pre);
+              epi.row(r, s, pre, red);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);
+        continue;
+      }
+      const unsigned char* blob = stages + (size_t)st * F.cap;
+      if (c.flags & STM_TILE) {
+        const unsigned nslots = *reinterpret_cast<const unsigned*>(blob);
+        if (nslots) {
+          const unsigned short* wsec = reinterpret_cast<const unsigned short*>(blob + 4);
+          const int k0 = wsec[warp], k1 = wsec[warp + 1];
+          const double* vals = reinterpret_cast<const double*>(blob + kStmHdr);
+          const unsigned* idx = reinterpret_cast<const unsigned*>(blob + kStmHdr + 8 * (size_t)nslots);
+          const double* xs = xbuf0 + (size_t)c.xbuf * (xbytes / 8);
+          double* a = acc + ((size_t)c.half * kStmRS + (size_t)warp * kStmSecRows) * NV;
+          unsigned cur = 0xffffu;
+          double sum[NV];
+#pragma unroll
+          for (int t = 0; t < NV; ++t) sum[t] = 0.0;
+          int k = k0;
+          for (; k + 4 <= k1; k += 4) {
+            double v[4];
+            unsigned id[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { v[u] = vals[(k + u) * 32 + lane]; id[u] = idx[(k + u) * 32 + lane]; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const unsigned r = id[u] >> 16, col = id[u] & 0xffffu;
+              if (r != cur) {
+                if (cur != 0xffffu)
+#pragma unroll
+                  for (int t = 0; t < NV; ++t) a[cur * NV + t] += sum[t];
+                cur = r;
+#pragma unroll
+                for (int t = 0; t < NV; ++t) sum[t] = 0.0;
+              }
+#pragma unroll
+              for (int t = 0; t < NV; ++t) sum[t] = fma(v[u], xs[col * STRIDE + t], sum[t]);
+            }
+          }
+          for (; k < k1; ++k) {
+            const double v = vals[k * 32 + lane];
+            const unsigned id = idx[k * 32 + lane];
+            const unsigned r = id >> 16, col = id & 0xffffu;
+            if (r != cur) {
+              if (cur != 0xffffu)
+#pragma unroll
+                for (int t = 0; t < NV; ++t) a[cur * NV + t] += sum[t];
+              cur = r;
+#pragma unroll
+              for (int t = 0; t < NV; ++t) sum[t] = 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < NV; ++t) sum[t] = fma(v, xs[col * STRIDE + t], sum[t]);
+          }
+          if (cur != 0xffffu)
+#pragma unroll
+            for (int t = 0; t < NV; ++t) a[cur * NV + t] += sum[t];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+      if (c.flags & STM_END) {
+        __syncwarp();  // this warp's accumulator updates are visible to all its lanes
+        const int nsb = (c.flags & STM_PAIR) ? 2 : 1;
+        for (int h = 0; h < nsb; ++h) {
+          const long long r0 = c.row0 + (long long)h * kStmRS + (long long)warp * kStmSecRows;
+          const long long left = F.rows - r0;
+          const int cnt = left <= 0 ? 0 : (int)(left < kStmSecRows ? left : kStmSecRows);
+          double* a = acc + ((size_t)h * kStmRS + (size_t)warp * kStmSecRows) * NV;
+          stm_rows<NV>(epi, a, r0, cnt, splits, c.sp, F.rows, P, red);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  if (splits > 1) return;  // k_tiled_combine runs the epilogue and the reductions
+  epi.extra(red);
+  if constexpr (Epi::NR > 0) {
+    if (grid_sum_last<Epi::NR>(red, epi.V.part, &epi.V.ctl->counter)) {
+      if (epi.defer) {
+        if (threadIdx.x == 0)
+          for (int t = 0; t < Epi::NR; ++t) epi.V.dred[t] = red[t];
+      } else {
+        epi.finish(red);
+      }
+    }
+  }
+}
+
+// ---- format build (setup) ----------------------------------------------------
+// section key of every entry: (sub-block, slab) tile * 16 + warp section
+__global__ void k_stm_keys(const int* rowid, const int* ci, long long nnz, int W, int S, int* key) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long k = tid; k < nnz; k += nt) {
+    const int r = rowid[k], c = ci[k];
+    key[k] = (int)((((long long)(r / kStmRS) * S + c / W) * kStmWarps) + (r % kStmRS) / kStmSecRows);
+  }
+}
+
+// First-fit-decreasing of one section's row segments (sorted by length,
+// descending) onto 32 lanes of depth D = max(longest, ceil(E / 32)),
+// raising D until everything fits.  One thread per section.
+__global__ void k_stm_ffd(const long long* sec_ptr, long long nsec, const int* order,
+                          const long long* seg_start, long long nseg, long long nnz, int* seg_lane,
+                          int* seg_k0, unsigned short* depth) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long s = tid; s < nsec; s += nt) {
+    const long long p0 = sec_ptr[s], p1 = sec_ptr[s + 1];
+    if (p0 == p1) { depth[s] = 0; continue; }
+    auto len = [&](long long p) {
+      const long long q = order[p];
+      return (int)((q + 1 < nseg ? seg_start[q + 1] : nnz) - seg_start[q]);
+    };
+    long long E = 0;
+    for (long long p = p0; p < p1; ++p) E += len(p);
+    int D = (int)((E + 31) / 32);
+    const int l0 = len(p0);
+    if (l0 > D) D = l0;
+    int load[32];
+    for (;;) {
+      for (int l = 0; l < 32; ++l) load[l] = 0;
+      bool ok = true;
+      for (long long p = p0; p < p1 && ok; ++p) {
+        const int L = len(p);
+        int l = 0;
+        while (l < 32 && load[l] + L > D) ++l;
+        if (l == 32) { ok = false; break; }
+        seg_lane[p] = l;
+        seg_k0[p] = load[l];
+        load[l] += L;
+      }
+      if (ok) break;
+      ++D;
+    }
+    depth[s] = (unsigned short)D;
+  }
+}
+
+// piece headers + padding (values 0, sentinel rows): one warp per piece
+__global__ void k_stm_init(unsigned char* blob, const unsigned long long* poff, const unsigned* pslots,
+                           const unsigned short* pwsec, long long npiece) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long p = w; p < npiece; p += nw) {
+    unsigned char* b = blob + poff[p];
+    const unsigned ns = pslots[p];
+    if (lane == 0) *reinterpret_cast<unsigned*>(b) = ns;
+    if (lane < kStmWarps + 1)
+      reinterpret_cast<unsigned short*>(b + 4)[lane] = pwsec[p * (kStmWarps + 1) + lane];
+    double* v = reinterpret_cast<double*>(b + kStmHdr);
+    unsigned* id = reinterpret_cast<unsigned*>(b + kStmHdr + 8 * (size_t)ns);
+    for (unsigned k = lane; k < ns; k += 32) { v[k] = 0.0; id[k] = kStmSentinel; }
+  }
+}
+
+// scatter every entry of a tiled sub-block into its piece
+__global__ void k_stm_scatter(const int* sec_sorted, const int* order, const long long* seg_start,
+                              long long nseg, long long nnz, const int* seg_lane, const int* seg_k0,
+                              const int* perm, const int* rowid, const int* ci, const double* val,
+                              const long long* tile_pf, const unsigned short* tile_kp,
+                              const unsigned long long* poff, const unsigned* pslots,
+                              const unsigned short* pwsec, int W, unsigned char* blob) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long p = tid; p < nseg; p += nt) {
+    const int sec = sec_sorted[p];
+    const long long tile = sec / kStmWarps;
+    const int w = sec % kStmWarps;
+    const long long pf = tile_pf[tile];
+    if (pf < 0) continue;  // CSR sub-block
+    const int kp = tile_kp[tile];
+    const long long q = order[p];
+    const long long a = seg_start[q], b = q + 1 < nseg ? seg_start[q + 1] : nnz;
+    const int lane = seg_lane[p], k0 = seg_k0[p];
+    const unsigned rl = (unsigned)(rowid[perm[a]] % kStmSecRows);
+    for (long long e = a; e < b; ++e) {
+      const int k = k0 + (int)(e - a);
+      const long long piece = pf + k / kp;
+      const int kk = k % kp;
+      unsigned char* bl = blob + poff[piece];
+      const unsigned ns = pslots[piece];
+      const long long slot = ((long long)pwsec[piece * (kStmWarps + 1) + w] + kk) * 32 + lane;
+      const int s = perm[e];
+      reinterpret_cast<double*>(bl + kStmHdr)[slot] = val[s];
+      reinterpret_cast<unsigned*>(bl + kStmHdr + 8 * (size_t)ns)[slot] = (rl << 16) | (unsigned)(ci[s] % W);
+    }
+  }
+}
+
+}  // namespace scs
