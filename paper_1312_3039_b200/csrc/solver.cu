@@ -1418,8 +1418,9 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T) {
   }
   const int G0 = h->sms;
   int splits = 1;
-  if (ntiled > 0 && ntiled < 4LL * G0)
-    splits = (int)std::min<long long>(std::min<long long>(32, T.S), (4LL * G0 + ntiled - 1) / ntiled);
+  // enough units for longest-processing-time balance (>= ~16 per CTA)
+  if (ntiled > 0 && ntiled < 16LL * G0)
+    splits = (int)std::min<long long>(std::min<long long>(32, T.S), (16LL * G0 + ntiled - 1) / ntiled);
   splits = (int)env_ll("SCS_STREAM_SPLITS", splits);
   splits = std::max(1, std::min(splits, std::max(1, T.S)));
   if (splits > 255) splits = 255;
@@ -1546,10 +1547,10 @@ void build_stream(scs_handle* h, int mat) {
   const long long ntile = (long long)F.NB * F.S, nsec = ntile * kStmWarps;
   if (nsec >= (1LL << 31) - 1 || nz >= (1LL << 31) - 1 || nz == 0)
     throw Fail{SCS_EINVAL, "streamed layout: too many sections or nonzeros"};
-  // 1. entries by warp section (stable: row-major inside)
+  // 1. entries by (warp section, owning lane, rotated gather bank)
   int* rowid = dalloc<int>(h, nz);
-  int* key = dalloc<int>(h, nz);
-  int* skey = dalloc<int>(h, nz);
+  unsigned long long* key = dalloc<unsigned long long>(h, nz);
+  unsigned long long* skey = dalloc<unsigned long long>(h, nz);
   int* perm_in = dalloc<int>(h, nz);
   int* perm = dalloc<int>(h, nz);
   k_expand_rows<<<elem_grid(h, rows * 32), kBlock, 0, h->st>>>(M.rp, rows, rowid);
@@ -1559,63 +1560,24 @@ void build_stream(scs_handle* h, int mat) {
   while ((1LL << bits) < nsec) ++bits;
   {
     size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const int*)key, skey, (const int*)perm_in, perm,
-                                       (int)nz, 0, bits, h->st));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned long long*)key, skey,
+                                       (const int*)perm_in, perm, (int)nz, 0, bits + 9, h->st));
     void* tmp = dalloc<char>(h, tb);
-    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, (const int*)key, skey, (const int*)perm_in, perm,
-                                       (int)nz, 0, bits, h->st));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, (const unsigned long long*)key, skey,
+                                       (const int*)perm_in, perm, (int)nz, 0, bits + 9, h->st));
     CK(cudaStreamSynchronize(h->st));
     dfree(h, tmp);
   }
   dfree(h, key);
-  // 2. row segments
-  int* flag = perm_in;
-  int* incl = dalloc<int>(h, nz);
-  k_seg_flags<<<elem_grid(h, nz), kBlock, 0, h->st>>>(skey, perm, rowid, nz, flag);
-  {
-    size_t tb = 0;
-    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flag, incl, (int)nz, h->st));
-    void* tmp = dalloc<char>(h, tb);
-    CK(cub::DeviceScan::InclusiveSum(tmp, tb, flag, incl, (int)nz, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    dfree(h, tmp);
-  }
-  const long long nseg = read_dev(h, incl + nz - 1);
-  long long* seg_start = dalloc<long long>(h, nseg);
-  k_seg_starts<<<elem_grid(h, nz), kBlock, 0, h->st>>>(flag, incl, nz, seg_start);
-  dfree(h, incl);
-  // 3. segments by (section, length desc)
-  unsigned long long* key2 = dalloc<unsigned long long>(h, nseg);
-  unsigned long long* key2s = dalloc<unsigned long long>(h, nseg);
-  int* sec_of = dalloc<int>(h, nseg);
-  int* sidx = dalloc<int>(h, nseg);
-  int* order = dalloc<int>(h, nseg);
-  k_seg_keys<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(seg_start, nseg, nz, skey, key2, sec_of);
-  k_iota<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(sidx, nseg);
-  {
-    size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned long long*)key2, key2s,
-                                       (const int*)sidx, order, (int)nseg, 0, 20 + bits, h->st));
-    void* tmp = dalloc<char>(h, tb);
-    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, (const unsigned long long*)key2, key2s,
-                                       (const int*)sidx, order, (int)nseg, 0, 20 + bits, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    dfree(h, tmp);
-  }
-  int* sec_sorted = sec_of;
-  k_key_hi<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(key2s, nseg, sec_sorted);
-  dfree(h, key2);
-  dfree(h, key2s);
-  dfree(h, sidx);
-  dfree(h, skey);
-  // 4. lanes: first-fit-decreasing per section
+  dfree(h, perm_in);
+  // 2. sections, slots (pinned / overflow) and depths
+  int* sec = dalloc<int>(h, nz);
+  k_stm_sec<<<elem_grid(h, nz), kBlock, 0, h->st>>>(skey, nz, sec);
   long long* sec_ptr = dalloc<long long>(h, nsec + 1);
-  k_rowptr<<<elem_grid(h, nsec + 1), kBlock, 0, h->st>>>(sec_sorted, nseg, nsec, sec_ptr);
-  int* seg_lane = dalloc<int>(h, nseg);
-  int* seg_k0 = dalloc<int>(h, nseg);
+  k_rowptr<<<elem_grid(h, nsec + 1), kBlock, 0, h->st>>>(sec, nz, nsec, sec_ptr);
+  int* slot = dalloc<int>(h, nz);
   unsigned short* depth = dalloc<unsigned short>(h, nsec);
-  k_stm_ffd<<<elem_grid(h, nsec), kBlock, 0, h->st>>>(sec_ptr, nsec, order, seg_start, nseg, nz,
-                                                      seg_lane, seg_k0, depth);
+  k_stm_pin<<<elem_grid(h, nsec), kBlock, 0, h->st>>>(sec_ptr, nsec, skey, slot, depth);
   CK(cudaGetLastError());
   std::vector<unsigned short> D(nsec);
   d2h(h, D.data(), depth, nsec);
@@ -1624,6 +1586,7 @@ void build_stream(scs_handle* h, int mat) {
   CK(cudaStreamSynchronize(h->st));
   dfree(h, depth);
   dfree(h, sec_ptr);
+  dfree(h, skey);
   // 5. host: tiled sub-blocks, pieces, blob offsets
   StmTiles T;
   T.NB = F.NB;
@@ -1638,15 +1601,20 @@ void build_stream(scs_handle* h, int mat) {
     const long long r0 = sb * kStmRS, r1 = std::min(rows, r0 + kStmRS);
     T.nnz_sb[sb] = rp_h[r1] - rp_h[r0];
     long long sl = 0, nt = 0;
+    bool bad = false;
     for (long long s = 0; s < F.S; ++s) {
       long long a = 0;
-      for (int w = 0; w < kStmWarps; ++w) a += 32LL * D[(sb * F.S + s) * kStmWarps + w];
+      for (int w = 0; w < kStmWarps; ++w) {
+        const unsigned short d = D[(sb * F.S + s) * kStmWarps + w];
+        if (d == 0xffff) bad = true;
+        else a += 32LL * d;
+      }
       T.slots[sb * F.S + s] = a;
       sl += a;
       nt += a > 0;
     }
     // CSR units only for short rows (the consumers run them at 4 lanes per row)
-    T.tiled[sb] = (nt == 0 || sl >= min_avg * nt || T.nnz_sb[sb] > 16 * (r1 - r0)) ? 1 : 0;
+    T.tiled[sb] = !bad && (nt == 0 || sl >= min_avg * nt || T.nnz_sb[sb] > 16 * (r1 - r0)) ? 1 : 0;
   }
   std::vector<unsigned short> tile_kp(ntile, 1), pwsec;
   long long npiece = 0;
@@ -1697,16 +1665,13 @@ void build_stream(scs_handle* h, int mat) {
   h2d(h, d_pwsec, pwsec.data(), pwsec.size());
   if (npiece) {
     k_stm_init<<<elem_grid(h, npiece * 32), kBlock, 0, h->st>>>(blob, d_poff, d_pslots, d_pwsec, npiece);
-    k_stm_scatter<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(sec_sorted, order, seg_start, nseg, nz,
-                                                            seg_lane, seg_k0, perm, rowid, M.ci, M.v,
-                                                            d_pf, d_kp, d_poff, d_pslots, d_pwsec,
-                                                            F.W, blob);
+    k_stm_scatter<<<elem_grid(h, nz), kBlock, 0, h->st>>>(sec, slot, nz, perm, rowid, M.ci, M.v, d_pf,
+                                                          d_kp, d_poff, d_pslots, d_pwsec, F.W, blob);
     CK(cudaGetLastError());
   }
   CK(cudaStreamSynchronize(h->st));
   for (void* p : {(void*)d_pf, (void*)d_kp, (void*)d_poff, (void*)d_pslots, (void*)d_pwsec,
-                  (void*)seg_lane, (void*)seg_k0, (void*)sec_sorted, (void*)order, (void*)seg_start,
-                  (void*)perm_in, (void*)perm, (void*)rowid})
+                  (void*)sec, (void*)slot, (void*)perm, (void*)rowid})
     dfree(h, p);
   F.blob = blob;
   long long ncsr = 0;

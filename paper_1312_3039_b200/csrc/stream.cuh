@@ -54,7 +54,8 @@ constexpr int kStmThreads = (kStmWarps + 1) * 32;
 constexpr int kStmHdr = 48;         // piece header bytes: u32 nslots, u16 wsec[17]
 constexpr int kStmAccBytes = 2 * kStmRS * 8;
 constexpr int kStmMaxStages = 4;
-constexpr unsigned kStmSentinel = 0xffff0000u;  // padding slot: no row
+constexpr int kStmPin = kStmSecRows / 32;  // rows pinned to each lane
+constexpr unsigned kStmSentinel = 2u << 24;   // padding slot (STM_PAD)
 
 enum : unsigned short { STM_END = 1, STM_CSR = 2, STM_PAIR = 4, STM_TILE = 8 };
 
@@ -122,26 +123,75 @@ __device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, unsig
       : "memory");
 }
 
-// Epilogue (or raw split partials) for rows [r0, r1) owned by this lane's
-// warp, reading and clearing the shared accumulator `a` (NV per row).
+// Epilogue (or raw split partials) for the rows of this warp's section,
+// reading and clearing the shared accumulator `a` (NV per row).
 template <int NV, class Epi>
 __device__ __forceinline__ void stm_rows(Epi& epi, double* a, long long r0, int cnt, int splits,
                                          int sp, long long rows, double* P, double* red) {
   const int lane = threadIdx.x & 31;
-  for (int i = lane; i < cnt; i += 32) {
-    const long long r = r0 + i;
+  for (int i = lane; i < kStmSecRows; i += 32) {
     double sv[NV];
 #pragma unroll
     for (int t = 0; t < NV; ++t) { sv[t] = a[i * NV + t]; a[i * NV + t] = 0.0; }
-    if (splits > 1) {
+    if (i < cnt) {
+      const long long row = r0 + i;
+      if (splits > 1) {
 #pragma unroll
-      for (int t = 0; t < NV; ++t) P[((long long)sp * rows + r) * NV + t] = sv[t];
-    } else {
-      typename Epi::Pre pre;
-      epi.pre(r, pre);
-      epi.row(r, sv, pre, red);
+        for (int t = 0; t < NV; ++t) P[((long long)sp * rows + row) * NV + t] = sv[t];
+      } else {
+        typename Epi::Pre pre;
+        epi.pre(row, pre);
+        epi.row(row, sv, pre, red);
+      }
     }
   }
+}
+
+// One warp section of a piece.  Slot word: column (16 bits) | local row
+// (8 bits) << 16 | overflow << 24 | padding << 25.  A pinned entry's row is
+// owned by its lane (local row = 32 j + lane), so the pinned read-modify-
+// writes of a step hit 32 distinct rows in the minimum number of shared-
+// memory wavefronts; overflow entries (in another lane's free slots) are
+// applied after them, as separate instructions of the same warp, so they
+// see the pinned update of the step, and all overflow entries of one owner
+// lane sit in one lane, so their rows are distinct within a step.
+template <int NV, int STRIDE, int U>
+__device__ __forceinline__ void stm_steps(const double* vals, const unsigned* idx, int k,
+                                          const double* xs, double* a) {
+  const int lane = threadIdx.x & 31;
+  double pr[U][NV];
+  unsigned rw[U], fl[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {  // every load of the batch before its stores
+    const double v = vals[(k + u) * 32 + lane];
+    const unsigned id = idx[(k + u) * 32 + lane];
+    rw[u] = (id >> 16) & 0xffu;
+    fl[u] = id >> 24;
+    const unsigned col = id & 0xffffu;
+#pragma unroll
+    for (int t = 0; t < NV; ++t) pr[u][t] = v * xs[col * STRIDE + t];
+  }
+  bool any_ovf = false;
+#pragma unroll
+  for (int u = 0; u < U; ++u) any_ovf |= fl[u] == 1u;
+  any_ovf = __any_sync(0xffffffffu, any_ovf);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (fl[u] == 0u)
+#pragma unroll
+      for (int t = 0; t < NV; ++t) a[rw[u] * NV + t] += pr[u][t];
+    if (any_ovf && fl[u] == 1u)
+#pragma unroll
+      for (int t = 0; t < NV; ++t) a[rw[u] * NV + t] += pr[u][t];
+  }
+}
+
+template <int NV, int STRIDE>
+__device__ __forceinline__ void stm_piece(const double* vals, const unsigned* idx, int k0, int k1,
+                                          const double* xs, double* a) {
+  int k = k0;
+  for (; k + 4 <= k1; k += 4) stm_steps<NV, STRIDE, 4>(vals, idx, k, xs, a);
+  for (; k < k1; ++k) stm_steps<NV, STRIDE, 1>(vals, idx, k, xs, a);
 }
 
 template <int NV, int STRIDE, class Epi>
@@ -276,49 +326,7 @@ __global__ void __launch_bounds__(kStmThreads, 1)
           const unsigned* idx = reinterpret_cast<const unsigned*>(blob + kStmHdr + 8 * (size_t)nslots);
           const double* xs = xbuf0 + (size_t)c.xbuf * (xbytes / 8);
           double* a = acc + ((size_t)c.half * kStmRS + (size_t)warp * kStmSecRows) * NV;
-          unsigned cur = 0xffffu;
-          double sum[NV];
-#pragma unroll
-          for (int t = 0; t < NV; ++t) sum[t] = 0.0;
-          int k = k0;
-          for (; k + 4 <= k1; k += 4) {
-            double v[4];
-            unsigned id[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) { v[u] = vals[(k + u) * 32 + lane]; id[u] = idx[(k + u) * 32 + lane]; }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const unsigned r = id[u] >> 16, col = id[u] & 0xffffu;
-              if (r != cur) {
-                if (cur != 0xffffu)
-#pragma unroll
-                  for (int t = 0; t < NV; ++t) a[cur * NV + t] += sum[t];
-                cur = r;
-#pragma unroll
-                for (int t = 0; t < NV; ++t) sum[t] = 0.0;
-              }
-#pragma unroll
-              for (int t = 0; t < NV; ++t) sum[t] = fma(v[u], xs[col * STRIDE + t], sum[t]);
-            }
-          }
-          for (; k < k1; ++k) {
-            const double v = vals[k * 32 + lane];
-            const unsigned id = idx[k * 32 + lane];
-            const unsigned r = id >> 16, col = id & 0xffffu;
-            if (r != cur) {
-              if (cur != 0xffffu)
-#pragma unroll
-                for (int t = 0; t < NV; ++t) a[cur * NV + t] += sum[t];
-              cur = r;
-#pragma unroll
-              for (int t = 0; t < NV; ++t) sum[t] = 0.0;
-            }
-#pragma unroll
-            for (int t = 0; t < NV; ++t) sum[t] = fma(v, xs[col * STRIDE + t], sum[t]);
-          }
-          if (cur != 0xffffu)
-#pragma unroll
-            for (int t = 0; t < NV; ++t) a[cur * NV + t] += sum[t];
+          stm_piece<NV, STRIDE>(vals, idx, k0, k1, xs, a);
         }
       }
       __syncwarp();
@@ -353,51 +361,77 @@ __global__ void __launch_bounds__(kStmThreads, 1)
 }
 
 // ---- format build (setup) ----------------------------------------------------
-// section key of every entry: (sub-block, slab) tile * 16 + warp section
-__global__ void k_stm_keys(const int* rowid, const int* ci, long long nnz, int W, int S, int* key) {
+// Sort key of every entry: warp section ((sub-block, slab) tile * 16 + warp),
+// then the lane that owns its row (local row mod 32), then the bank of its
+// gather word rotated by the lane -- so that in each step the 32 lanes tend
+// to read different shared-memory banks of the slab.
+__global__ void k_stm_keys(const int* rowid, const int* ci, long long nnz, int W, int S,
+                           unsigned long long* key) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long k = tid; k < nnz; k += nt) {
     const int r = rowid[k], c = ci[k];
-    key[k] = (int)((((long long)(r / kStmRS) * S + c / W) * kStmWarps) + (r % kStmRS) / kStmSecRows);
+    const long long sec = ((long long)(r / kStmRS) * S + c / W) * kStmWarps + (r % kStmRS) / kStmSecRows;
+    const unsigned ln = (unsigned)(r % kStmSecRows) & 31u;
+    const unsigned bank = ((unsigned)(c % W) - ln) & 15u;
+    key[k] = ((unsigned long long)sec << 9) | (ln << 4) | bank;
   }
 }
+__global__ void k_stm_sec(const unsigned long long* key, long long nnz, int* sec) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long k = tid; k < nnz; k += nt) sec[k] = (int)(key[k] >> 9);
+}
 
-// First-fit-decreasing of one section's row segments (sorted by length,
-// descending) onto 32 lanes of depth D = max(longest, ceil(E / 32)),
-// raising D until everything fits.  One thread per section.
-__global__ void k_stm_ffd(const long long* sec_ptr, long long nsec, const int* order,
-                          const long long* seg_start, long long nseg, long long nnz, int* seg_lane,
-                          int* seg_k0, unsigned short* depth) {
+// Slots of one section (one thread per section).  Depth D starts at
+// ceil(E / 32); the i-th entry of owner lane l sits at step i of lane l
+// while i < D (pinned); each lane's excess (its "overflow group") goes, as
+// one block of consecutive steps, into the free tail of a single other lane
+// (first-fit decreasing), so two overflow entries of one row never share a
+// step.  D grows until the groups fit; a section that would need more than
+// 2 D0 + 16 steps (a row far longer than its neighbours) is flagged 0xffff
+// and its sub-block becomes a CSR unit.  slot = step * 32 + lane, | 1 << 30
+// for overflow.
+__global__ void k_stm_pin(const long long* sec_ptr, long long nsec, const unsigned long long* key,
+                          int* slot, unsigned short* depth) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long s = tid; s < nsec; s += nt) {
     const long long p0 = sec_ptr[s], p1 = sec_ptr[s + 1];
-    if (p0 == p1) { depth[s] = 0; continue; }
-    auto len = [&](long long p) {
-      const long long q = order[p];
-      return (int)((q + 1 < nseg ? seg_start[q + 1] : nnz) - seg_start[q]);
-    };
-    long long E = 0;
-    for (long long p = p0; p < p1; ++p) E += len(p);
-    int D = (int)((E + 31) / 32);
-    const int l0 = len(p0);
-    if (l0 > D) D = l0;
-    int load[32];
-    for (;;) {
-      for (int l = 0; l < 32; ++l) load[l] = 0;
-      bool ok = true;
-      for (long long p = p0; p < p1 && ok; ++p) {
-        const int L = len(p);
-        int l = 0;
-        while (l < 32 && load[l] + L > D) ++l;
-        if (l == 32) { ok = false; break; }
-        seg_lane[p] = l;
-        seg_k0[p] = load[l];
-        load[l] += L;
+    const long long E = p1 - p0;
+    if (E == 0) { depth[s] = 0; continue; }
+    const int D0 = (int)((E + 31) / 32);
+    int cnt[32], dst[32], st[32], fill[32];
+    for (int l = 0; l < 32; ++l) cnt[l] = 0;
+    for (long long e = p0; e < p1; ++e) cnt[(key[e] >> 4) & 31u]++;
+    int D = D0;
+    bool ok = false;
+    for (; D <= 2 * D0 + 16 && D < 0xffff; ++D) {
+      for (int l = 0; l < 32; ++l) fill[l] = cnt[l] < D ? cnt[l] : D;  // next free step
+      ok = true;
+      unsigned done = 0;
+      for (int g = 0; g < 32 && ok; ++g) {  // groups by size, descending
+        int best = -1, bs = 0;
+        for (int l = 0; l < 32; ++l)
+          if (!(done >> l & 1u) && cnt[l] - D > bs) { bs = cnt[l] - D; best = l; }
+        if (best < 0) break;
+        done |= 1u << best;
+        int lane = -1;
+        for (int l = 0; l < 32; ++l)
+          if (l != best && D - fill[l] >= bs) { lane = l; break; }
+        if (lane < 0) { ok = false; break; }
+        dst[best] = lane;
+        st[best] = fill[lane];
+        fill[lane] += bs;
       }
       if (ok) break;
-      ++D;
+    }
+    if (!ok) { depth[s] = 0xffff; continue; }
+    for (int l = 0; l < 32; ++l) cnt[l] = 0;
+    for (long long e = p0; e < p1; ++e) {
+      const int l = (int)((key[e] >> 4) & 31u);
+      const int i = cnt[l]++;
+      slot[e] = i < D ? i * 32 + l : (((st[l] + i - D) * 32 + dst[l]) | (1 << 30));
     }
     depth[s] = (unsigned short)D;
   }
@@ -422,36 +456,33 @@ __global__ void k_stm_init(unsigned char* blob, const unsigned long long* poff, 
 }
 
 // scatter every entry of a tiled sub-block into its piece
-__global__ void k_stm_scatter(const int* sec_sorted, const int* order, const long long* seg_start,
-                              long long nseg, long long nnz, const int* seg_lane, const int* seg_k0,
-                              const int* perm, const int* rowid, const int* ci, const double* val,
+__global__ void k_stm_scatter(const int* sec, const int* slot, long long nnz, const int* perm,
+                              const int* rowid, const int* ci, const double* val,
                               const long long* tile_pf, const unsigned short* tile_kp,
                               const unsigned long long* poff, const unsigned* pslots,
                               const unsigned short* pwsec, int W, unsigned char* blob) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
-  for (long long p = tid; p < nseg; p += nt) {
-    const int sec = sec_sorted[p];
-    const long long tile = sec / kStmWarps;
-    const int w = sec % kStmWarps;
+  for (long long e = tid; e < nnz; e += nt) {
+    const int sc = sec[e];
+    const long long tile = sc / kStmWarps;
+    const int w = sc % kStmWarps;
     const long long pf = tile_pf[tile];
     if (pf < 0) continue;  // CSR sub-block
     const int kp = tile_kp[tile];
-    const long long q = order[p];
-    const long long a = seg_start[q], b = q + 1 < nseg ? seg_start[q + 1] : nnz;
-    const int lane = seg_lane[p], k0 = seg_k0[p];
-    const unsigned rl = (unsigned)(rowid[perm[a]] % kStmSecRows);
-    for (long long e = a; e < b; ++e) {
-      const int k = k0 + (int)(e - a);
-      const long long piece = pf + k / kp;
-      const int kk = k % kp;
-      unsigned char* bl = blob + poff[piece];
-      const unsigned ns = pslots[piece];
-      const long long slot = ((long long)pwsec[piece * (kStmWarps + 1) + w] + kk) * 32 + lane;
-      const int s = perm[e];
-      reinterpret_cast<double*>(bl + kStmHdr)[slot] = val[s];
-      reinterpret_cast<unsigned*>(bl + kStmHdr + 8 * (size_t)ns)[slot] = (rl << 16) | (unsigned)(ci[s] % W);
-    }
+    const int sl = slot[e];
+    const unsigned ovf = (unsigned)(sl >> 30) & 1u;
+    const int k = (sl & ((1 << 30) - 1)) >> 5, lane = sl & 31;
+    const long long piece = pf + k / kp;
+    const int kk = k % kp;
+    unsigned char* bl = blob + poff[piece];
+    const unsigned ns = pslots[piece];
+    const long long at = ((long long)pwsec[piece * (kStmWarps + 1) + w] + kk) * 32 + lane;
+    const int s = perm[e];
+    const unsigned rl = (unsigned)(rowid[s] % kStmSecRows);
+    reinterpret_cast<double*>(bl + kStmHdr)[at] = val[s];
+    reinterpret_cast<unsigned*>(bl + kStmHdr + 8 * (size_t)ns)[at] =
+        (unsigned)(ci[s] % W) | (rl << 16) | (ovf << 24);
   }
 }
 
