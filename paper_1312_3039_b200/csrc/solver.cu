@@ -1561,10 +1561,10 @@ void build_stream(scs_handle* h, int mat) {
   {
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned long long*)key, skey,
-                                       (const int*)perm_in, perm, (int)nz, 0, bits + 9, h->st));
+                                       (const int*)perm_in, perm, (int)nz, 0, bits + 12, h->st));
     void* tmp = dalloc<char>(h, tb);
     CK(cub::DeviceRadixSort::SortPairs(tmp, tb, (const unsigned long long*)key, skey,
-                                       (const int*)perm_in, perm, (int)nz, 0, bits + 9, h->st));
+                                       (const int*)perm_in, perm, (int)nz, 0, bits + 12, h->st));
     CK(cudaStreamSynchronize(h->st));
     dfree(h, tmp);
   }
@@ -1577,7 +1577,7 @@ void build_stream(scs_handle* h, int mat) {
   k_rowptr<<<elem_grid(h, nsec + 1), kBlock, 0, h->st>>>(sec, nz, nsec, sec_ptr);
   int* slot = dalloc<int>(h, nz);
   unsigned short* depth = dalloc<unsigned short>(h, nsec);
-  k_stm_pin<<<elem_grid(h, nsec), kBlock, 0, h->st>>>(sec_ptr, nsec, skey, slot, depth);
+  k_stm_pin<<<elem_grid(h, nsec), kBlock, 0, h->st>>>(sec_ptr, nsec, skey, perm, slot, depth);
   CK(cudaGetLastError());
   std::vector<unsigned short> D(nsec);
   d2h(h, D.data(), depth, nsec);

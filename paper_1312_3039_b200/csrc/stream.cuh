@@ -151,10 +151,10 @@ __device__ __forceinline__ void stm_rows(Epi& epi, double* a, long long r0, int 
 // (8 bits) << 16 | overflow << 24 | padding << 25.  A pinned entry's row is
 // owned by its lane (local row = 32 j + lane), so the pinned read-modify-
 // writes of a step hit 32 distinct rows in the minimum number of shared-
-// memory wavefronts; overflow entries (in another lane's free slots) are
-// applied after them, as separate instructions of the same warp, so they
-// see the pinned update of the step, and all overflow entries of one owner
-// lane sit in one lane, so their rows are distinct within a step.
+// memory wavefronts; overflow entries (in another lane's free slots) share
+// the same update: all overflow entries of one owner lane sit in one lane,
+// and k_stm_pin keeps them off the steps where the owner lane holds the
+// same row, so the rows of a step are always distinct.
 template <int NV, int STRIDE, int U>
 __device__ __forceinline__ void stm_steps(const double* vals, const unsigned* idx, int k,
                                           const double* xs, double* a) {
@@ -171,19 +171,11 @@ __device__ __forceinline__ void stm_steps(const double* vals, const unsigned* id
 #pragma unroll
     for (int t = 0; t < NV; ++t) pr[u][t] = v * xs[col * STRIDE + t];
   }
-  bool any_ovf = false;
 #pragma unroll
-  for (int u = 0; u < U; ++u) any_ovf |= fl[u] == 1u;
-  any_ovf = __any_sync(0xffffffffu, any_ovf);
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    if (fl[u] == 0u)
+  for (int u = 0; u < U; ++u)
+    if (fl[u] < 2u)  // pinned or overflow (padding: 2)
 #pragma unroll
       for (int t = 0; t < NV; ++t) a[rw[u] * NV + t] += pr[u][t];
-    if (any_ovf && fl[u] == 1u)
-#pragma unroll
-      for (int t = 0; t < NV; ++t) a[rw[u] * NV + t] += pr[u][t];
-  }
 }
 
 template <int NV, int STRIDE>
@@ -231,6 +223,8 @@ __global__ void __launch_bounds__(kStmThreads, 1)
     long long slab_cur = -1;
     int xb = 1;
     long long last0 = -1, last1 = -1;  // last stage that read slab buffer 0 / 1
+    int st = -1;
+    unsigned ph = 1;
     for (long long base = c0; base < c1; base += 32) {
       StmCmd mine{};
       if (base + lane < c1) mine = cmds[base + lane];
@@ -243,8 +237,9 @@ __global__ void __launch_bounds__(kStmThreads, 1)
         const unsigned fl = __shfl_sync(0xffffffffu, (unsigned)mine.flags | ((unsigned)mine.half << 16) |
                                                          ((unsigned)mine.sp << 24), j);
         const long long i = base - c0 + j;
-        const int st = (int)(i % NS);
-        if (i >= NS) mbar_wait(empty + st, (unsigned)((i / NS - 1) & 1));
+        if (++st == NS) st = 0;
+        if (st == 0) ph ^= 1u;
+        if (i >= NS) mbar_wait(empty + st, ph ^ 1u);
         const bool tile = bytes > 0 && !(fl & STM_CSR);
         unsigned slab_bytes = 0;
         long long cstart = 0;
@@ -284,9 +279,12 @@ __global__ void __launch_bounds__(kStmThreads, 1)
   } else {
     // ---------------- consumer warps ----------------
     const long long ncmd = c1 - c0;
+    int st = -1;
+    unsigned ph = 1;
     for (long long i = 0; i < ncmd; ++i) {
-      const int st = (int)(i % NS);
-      mbar_wait(full + st, (unsigned)((i / NS) & 1));
+      if (++st == NS) st = 0;
+      if (st == 0) ph ^= 1u;
+      mbar_wait(full + st, ph);
       const StmCtl c = sctl[st];
       if (c.flags & STM_CSR) {
         // sparse sub-block: L = 4 lanes per row straight from CSR
@@ -372,15 +370,15 @@ __global__ void k_stm_keys(const int* rowid, const int* ci, long long nnz, int W
   for (long long k = tid; k < nnz; k += nt) {
     const int r = rowid[k], c = ci[k];
     const long long sec = ((long long)(r / kStmRS) * S + c / W) * kStmWarps + (r % kStmRS) / kStmSecRows;
-    const unsigned ln = (unsigned)(r % kStmSecRows) & 31u;
+    const unsigned rl = (unsigned)(r % kStmSecRows), ln = rl & 31u;
     const unsigned bank = ((unsigned)(c % W) - ln) & 15u;
-    key[k] = ((unsigned long long)sec << 9) | (ln << 4) | bank;
+    key[k] = ((unsigned long long)sec << 12) | (ln << 7) | (bank << 3) | (rl >> 5);
   }
 }
 __global__ void k_stm_sec(const unsigned long long* key, long long nnz, int* sec) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
-  for (long long k = tid; k < nnz; k += nt) sec[k] = (int)(key[k] >> 9);
+  for (long long k = tid; k < nnz; k += nt) sec[k] = (int)(key[k] >> 12);
 }
 
 // Slots of one section (one thread per section).  Depth D starts at
@@ -392,8 +390,8 @@ __global__ void k_stm_sec(const unsigned long long* key, long long nnz, int* sec
 // 2 D0 + 16 steps (a row far longer than its neighbours) is flagged 0xffff
 // and its sub-block becomes a CSR unit.  slot = step * 32 + lane, | 1 << 30
 // for overflow.
-__global__ void k_stm_pin(const long long* sec_ptr, long long nsec, const unsigned long long* key,
-                          int* slot, unsigned short* depth) {
+__global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned long long* key,
+                          int* perm, int* slot, unsigned short* depth) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long s = tid; s < nsec; s += nt) {
@@ -403,14 +401,15 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, const unsign
     const int D0 = (int)((E + 31) / 32);
     int cnt[32], dst[32], st[32], fill[32];
     for (int l = 0; l < 32; ++l) cnt[l] = 0;
-    for (long long e = p0; e < p1; ++e) cnt[(key[e] >> 4) & 31u]++;
+    for (long long e = p0; e < p1; ++e) cnt[(key[e] >> 7) & 31u]++;
     int D = D0;
     bool ok = false;
-    for (; D <= 2 * D0 + 16 && D < 0xffff; ++D) {
+    for (; D <= 2 * D0 + 16 && D < 0xffff && !ok; ++D) {
+      // overflow groups: first-fit decreasing into the free tails
       for (int l = 0; l < 32; ++l) fill[l] = cnt[l] < D ? cnt[l] : D;  // next free step
       ok = true;
       unsigned done = 0;
-      for (int g = 0; g < 32 && ok; ++g) {  // groups by size, descending
+      for (int g = 0; g < 32 && ok; ++g) {
         int best = -1, bs = 0;
         for (int l = 0; l < 32; ++l)
           if (!(done >> l & 1u) && cnt[l] - D > bs) { bs = cnt[l] - D; best = l; }
@@ -424,12 +423,37 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, const unsign
         st[best] = fill[lane];
         fill[lane] += bs;
       }
-      if (ok) break;
+      // a step must not hold a pinned and an overflow entry of the same row:
+      // swap pinned entries (key and perm, inside the owner lane's run) away
+      // from the overflow window until every step of it is row-distinct
+      long long run = p0;
+      for (int l = 0; l < 32 && ok; ++l) {
+        const int o = cnt[l] - D;
+        for (int q = 0; q < o && ok; ++q) {
+          const long long a = run + st[l] + q, b = run + D + q;
+          const unsigned jb = (unsigned)(key[b] & 7u);
+          if ((unsigned)(key[a] & 7u) != jb) continue;
+          bool fixed = false;
+          for (int k2 = 0; k2 < D && !fixed; ++k2) {
+            const long long c2 = run + k2;
+            const unsigned j2 = (unsigned)(key[c2] & 7u);
+            if (j2 == jb) continue;
+            const int q2 = k2 - st[l];  // overflow entry sharing step k2, if any
+            if (q2 >= 0 && q2 < o && (unsigned)(key[run + D + q2] & 7u) == jb) continue;
+            const unsigned long long tk = key[a]; key[a] = key[c2]; key[c2] = tk;
+            const int tp = perm[a]; perm[a] = perm[c2]; perm[c2] = tp;
+            fixed = true;
+          }
+          ok = fixed;
+        }
+        run += cnt[l];
+      }
     }
+    --D;  // the loop stepped past the depth that worked
     if (!ok) { depth[s] = 0xffff; continue; }
     for (int l = 0; l < 32; ++l) cnt[l] = 0;
     for (long long e = p0; e < p1; ++e) {
-      const int l = (int)((key[e] >> 4) & 31u);
+      const int l = (int)((key[e] >> 7) & 31u);
       const int i = cnt[l]++;
       slot[e] = i < D ? i * 32 + l : (((st[l] + i - D) * 32 + dst[l]) | (1 << 30));
     }
