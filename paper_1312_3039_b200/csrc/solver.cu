@@ -1538,7 +1538,7 @@ void build_stream(scs_handle* h, int mat) {
   Stm& F = h->sF[mat];
   F.rows = rows;
   F.cols = cols;
-  F.W = (int)std::min<long long>(65536, std::max<long long>(8, env_ll("SCS_STREAM_W", 2048)));
+  F.W = (int)std::min<long long>(65536, std::max<long long>(32, env_ll("SCS_STREAM_W", 2048)));  // >= 32: padding gathers column = lane
   F.cap = (int)(env_ll("SCS_STREAM_CAP", 32768) & ~15LL);
   const int min_cap = kStmHdr + 12 * 32 * kStmWarps;
   if (F.cap < min_cap) F.cap = (min_cap + 15) & ~15;

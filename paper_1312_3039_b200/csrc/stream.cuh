@@ -475,7 +475,8 @@ __global__ void k_stm_init(unsigned char* blob, const unsigned long long* poff, 
       reinterpret_cast<unsigned short*>(b + 4)[lane] = pwsec[p * (kStmWarps + 1) + lane];
     double* v = reinterpret_cast<double*>(b + kStmHdr);
     unsigned* id = reinterpret_cast<unsigned*>(b + kStmHdr + 8 * (size_t)ns);
-    for (unsigned k = lane; k < ns; k += 32) { v[k] = 0.0; id[k] = kStmSentinel; }
+    // padding gathers column = lane: distinct banks, no conflict with the real entries
+    for (unsigned k = lane; k < ns; k += 32) { v[k] = 0.0; id[k] = kStmSentinel | (unsigned)lane; }
   }
 }
 
