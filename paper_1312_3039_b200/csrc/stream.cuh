@@ -383,13 +383,17 @@ __global__ void k_stm_sec(const unsigned long long* key, long long nnz, int* sec
 
 // Slots of one section (one thread per section).  Depth D starts at
 // ceil(E / 32); the i-th entry of owner lane l sits at step i of lane l
-// while i < D (pinned); each lane's excess (its "overflow group") goes, as
-// one block of consecutive steps, into the free tail of a single other lane
-// (first-fit decreasing), so two overflow entries of one row never share a
-// step.  D grows until the groups fit; a section that would need more than
-// 2 D0 + 16 steps (a row far longer than its neighbours) is flagged 0xffff
-// and its sub-block becomes a CSR unit.  slot = step * 32 + lane, | 1 << 30
-// for overflow.
+// while i < D (pinned; lanes that are not full start at step l mod D and
+// wrap, which spreads the free slots over all steps).  The excess of each owner lane (largest first)
+// takes free slots -- steps >= another lane's own count -- at pairwise
+// distinct steps, so two overflow entries of one row never share a step;
+// pinned entries of the owner are then swapped (key and perm, inside the
+// owner's run) so that no step holds a pinned and an overflow entry of the
+// same row.  D grows until this succeeds; sections deeper than kStmPinMax
+// steps or 2 D0 + 16 (rows far longer than their neighbours) are flagged
+// 0xffff and their sub-block becomes a CSR unit.
+// slot = step * 32 + lane, | 1 << 30 for overflow.
+constexpr int kStmPinMax = 64;
 __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned long long* key,
                           int* perm, int* slot, unsigned short* depth) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -399,65 +403,78 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
     const long long E = p1 - p0;
     if (E == 0) { depth[s] = 0; continue; }
     const int D0 = (int)((E + 31) / 32);
-    int cnt[32], dst[32], st[32], fill[32];
+    if (D0 > kStmPinMax) { depth[s] = 0xffff; continue; }
+    int cnt[32];
+    long long run0[32];
+    unsigned freem[kStmPinMax];
+    int ostep[kStmPinMax];
     for (int l = 0; l < 32; ++l) cnt[l] = 0;
     for (long long e = p0; e < p1; ++e) cnt[(key[e] >> 7) & 31u]++;
-    int D = D0;
+    {
+      long long r = p0;
+      for (int l = 0; l < 32; ++l) { run0[l] = r; r += cnt[l]; }
+    }
     bool ok = false;
-    for (; D <= 2 * D0 + 16 && D < 0xffff && !ok; ++D) {
-      // overflow groups: first-fit decreasing into the free tails
-      for (int l = 0; l < 32; ++l) fill[l] = cnt[l] < D ? cnt[l] : D;  // next free step
+    int D = D0;
+    for (; !ok && D <= 2 * D0 + 16 && D <= kStmPinMax; ++D) {
+      // lanes that are not full start their pinned entries at step
+      // rot(l) = l mod D (wrapping), so the free slots spread over all steps
+      for (int k = 0; k < D; ++k) {
+        unsigned m = 0;
+        for (int l = 0; l < 32; ++l) {
+          const int r = cnt[l] >= D ? 0 : l % D;
+          m |= (((k - r + D) % D) >= cnt[l] ? 1u : 0u) << l;
+        }
+        freem[k] = m;
+      }
       ok = true;
       unsigned done = 0;
-      for (int g = 0; g < 32 && ok; ++g) {
-        int best = -1, bs = 0;
-        for (int l = 0; l < 32; ++l)
-          if (!(done >> l & 1u) && cnt[l] - D > bs) { bs = cnt[l] - D; best = l; }
-        if (best < 0) break;
-        done |= 1u << best;
-        int lane = -1;
-        for (int l = 0; l < 32; ++l)
-          if (l != best && D - fill[l] >= bs) { lane = l; break; }
-        if (lane < 0) { ok = false; break; }
-        dst[best] = lane;
-        st[best] = fill[lane];
-        fill[lane] += bs;
-      }
-      // a step must not hold a pinned and an overflow entry of the same row:
-      // swap pinned entries (key and perm, inside the owner lane's run) away
-      // from the overflow window until every step of it is row-distinct
-      long long run = p0;
-      for (int l = 0; l < 32 && ok; ++l) {
-        const int o = cnt[l] - D;
-        for (int q = 0; q < o && ok; ++q) {
-          const long long a = run + st[l] + q, b = run + D + q;
+      for (int g = 0; g < 32 && ok; ++g) {  // owners by overflow size, descending
+        int l = -1, o = 0;
+        for (int c = 0; c < 32; ++c)
+          if (!(done >> c & 1u) && cnt[c] - D > o) { o = cnt[c] - D; l = c; }
+        if (l < 0) break;
+        done |= 1u << l;
+        int n = 0;
+        for (int k = D - 1; k >= 0 && n < o; --k)
+          if (freem[k] & ~(1u << l)) ostep[n++] = k;
+        if (n < o) { ok = false; break; }
+        const long long run = run0[l];
+        for (int q = 0; q < o && ok; ++q) {  // row-distinct steps: swap pinned entries
+          const long long a = run + ostep[q], b = run + D + q;
           const unsigned jb = (unsigned)(key[b] & 7u);
           if ((unsigned)(key[a] & 7u) != jb) continue;
           bool fixed = false;
           for (int k2 = 0; k2 < D && !fixed; ++k2) {
             const long long c2 = run + k2;
-            const unsigned j2 = (unsigned)(key[c2] & 7u);
-            if (j2 == jb) continue;
-            const int q2 = k2 - st[l];  // overflow entry sharing step k2, if any
-            if (q2 >= 0 && q2 < o && (unsigned)(key[run + D + q2] & 7u) == jb) continue;
+            if ((unsigned)(key[c2] & 7u) == jb) continue;
+            int q2 = -1;  // overflow entry of this owner at step k2, if any
+            for (int t = 0; t < o; ++t)
+              if (ostep[t] == k2) q2 = t;
+            if (q2 >= 0 && (unsigned)(key[run + D + q2] & 7u) == jb) continue;
             const unsigned long long tk = key[a]; key[a] = key[c2]; key[c2] = tk;
             const int tp = perm[a]; perm[a] = perm[c2]; perm[c2] = tp;
             fixed = true;
           }
           ok = fixed;
         }
-        run += cnt[l];
+        for (int q = 0; q < o && ok; ++q) {
+          const int k = ostep[q];
+          const unsigned m = freem[k] & ~(1u << l);
+          const int lane = __ffs(m) - 1;
+          freem[k] &= ~(1u << lane);
+          slot[run + D + q] = (k * 32 + lane) | (1 << 30);
+        }
+      }
+      if (ok) {
+        for (int l = 0; l < 32; ++l) {
+          const int r = cnt[l] >= D ? 0 : l % D;
+          for (int i = 0; i < cnt[l] && i < D; ++i) slot[run0[l] + i] = ((i + r) % D) * 32 + l;
+        }
       }
     }
-    --D;  // the loop stepped past the depth that worked
     if (!ok) { depth[s] = 0xffff; continue; }
-    for (int l = 0; l < 32; ++l) cnt[l] = 0;
-    for (long long e = p0; e < p1; ++e) {
-      const int l = (int)((key[e] >> 7) & 31u);
-      const int i = cnt[l]++;
-      slot[e] = i < D ? i * 32 + l : (((st[l] + i - D) * 32 + dst[l]) | (1 << 30));
-    }
-    depth[s] = (unsigned short)D;
+    depth[s] = (unsigned short)(D - 1);  // the loop stepped past the depth that worked
   }
 }
 
