@@ -435,9 +435,14 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
           if (!(done >> c & 1u) && cnt[c] - D > o) { o = cnt[c] - D; l = c; }
         if (l < 0) break;
         done |= 1u << l;
+        // steps where the partner lane l ^ 16 (same accumulator banks as l,
+        // other half-warp) is free first: hosting there adds no bank conflict
+        const unsigned partner = 1u << (l ^ 16);
         int n = 0;
         for (int k = D - 1; k >= 0 && n < o; --k)
-          if (freem[k] & ~(1u << l)) ostep[n++] = k;
+          if (freem[k] & partner) ostep[n++] = k;
+        for (int k = D - 1; k >= 0 && n < o; --k)
+          if ((freem[k] & ~(1u << l)) && !(freem[k] & partner)) ostep[n++] = k;
         if (n < o) { ok = false; break; }
         const long long run = run0[l];
         for (int q = 0; q < o && ok; ++q) {  // row-distinct steps: swap pinned entries
@@ -461,15 +466,55 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
         for (int q = 0; q < o && ok; ++q) {
           const int k = ostep[q];
           const unsigned m = freem[k] & ~(1u << l);
-          const int lane = __ffs(m) - 1;
+          const int lane = (m & partner) ? (l ^ 16) : __ffs(m) - 1;
           freem[k] &= ~(1u << lane);
           slot[run + D + q] = (k * 32 + lane) | (1 << 30);
         }
       }
       if (ok) {
+        // gather banks of a step, per half-warp (the shared-memory conflict
+        // unit of 8-byte loads): first the entries whose step is fixed
+        // (owner lanes' pinned entries, overflow entries), then every other
+        // lane picks, step by step, the remaining entry of its run whose
+        // bank is least used at that step in its half-warp
+        unsigned char use[kStmPinMax][2][16];
+        for (int k = 0; k < D; ++k)
+          for (int h = 0; h < 2; ++h)
+            for (int b = 0; b < 16; ++b) use[k][h][b] = 0;
+        auto bank = [&](long long e) {
+          return (unsigned)(((key[e] >> 3) + (key[e] >> 7)) & 15u);  // (col - lane) + lane
+        };
         for (int l = 0; l < 32; ++l) {
+          if (cnt[l] <= D) continue;
+          for (int i = 0; i < D; ++i) {
+            const long long e = run0[l] + i;
+            slot[e] = i * 32 + l;
+            use[i][l >> 4][bank(e)]++;
+          }
+          for (long long e = run0[l] + D; e < run0[l] + cnt[l]; ++e) {
+            const int sl = slot[e] & ((1 << 30) - 1);
+            use[sl >> 5][(sl & 31) >> 4][bank(e)]++;
+          }
+        }
+        for (int l = 0; l < 32; ++l) {
+          if (cnt[l] > D) continue;
           const int r = cnt[l] >= D ? 0 : l % D;
-          for (int i = 0; i < cnt[l] && i < D; ++i) slot[run0[l] + i] = ((i + r) % D) * 32 + l;
+          for (int i = 0; i < cnt[l]; ++i) {
+            const int k = (i + r) % D;
+            long long best = run0[l] + i;
+            int bu = 1 << 30;
+            for (long long e = run0[l] + i; e < run0[l] + cnt[l]; ++e) {
+              const int u = use[k][l >> 4][bank(e)];
+              if (u < bu) { bu = u; best = e; }
+            }
+            const long long a = run0[l] + i;
+            if (best != a) {
+              const unsigned long long tk = key[a]; key[a] = key[best]; key[best] = tk;
+              const int tp = perm[a]; perm[a] = perm[best]; perm[best] = tp;
+            }
+            use[k][l >> 4][bank(a)]++;
+            slot[a] = k * 32 + l;
+          }
         }
       }
     }
