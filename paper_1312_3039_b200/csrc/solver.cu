@@ -1489,6 +1489,7 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T) {
         StmCmd c{};
         c.row0 = u.sb0 * kStmRS;
         c.flags = STM_CSR | STM_END;
+        if (T.nnz_sb[u.sb0] > 16LL * kStmRS) c.flags |= STM_CSR32;  // long rows: warp per row
         cmds.push_back(c);
         continue;
       }
@@ -1538,21 +1539,30 @@ void build_stream(scs_handle* h, int mat) {
   Stm& F = h->sF[mat];
   F.rows = rows;
   F.cols = cols;
-  F.W = (int)std::min<long long>(65536, std::max<long long>(32, env_ll("SCS_STREAM_W", 2048)));  // >= 32: padding gathers column = lane
+  // slab width: 2048 columns, narrowed (/4, down to 256) when dense rows
+  // make warp sections deeper than k_stm_pin handles (> 0.1% flagged)
+  const bool wforced = getenv("SCS_STREAM_W") != nullptr;
+  long long W = std::min<long long>(65536, std::max<long long>(32, env_ll("SCS_STREAM_W", 2048)));  // >= 32: padding gathers column = lane
   F.cap = (int)(env_ll("SCS_STREAM_CAP", 32768) & ~15LL);
   const int min_cap = kStmHdr + 12 * 32 * kStmWarps;
   if (F.cap < min_cap) F.cap = (min_cap + 15) & ~15;
-  F.S = (int)((cols + F.W - 1) / F.W);
   F.NB = (int)((rows + kStmRS - 1) / kStmRS);
-  const long long ntile = (long long)F.NB * F.S, nsec = ntile * kStmWarps;
+  long long ntile = 0, nsec = 0;
+  int *rowid = nullptr, *perm = nullptr, *sec = nullptr, *slot = nullptr;
+  std::vector<unsigned short> D;
+  for (;;) {
+  F.W = (int)W;
+  F.S = (int)((cols + F.W - 1) / F.W);
+  ntile = (long long)F.NB * F.S;
+  nsec = ntile * kStmWarps;
   if (nsec >= (1LL << 31) - 1 || nz >= (1LL << 31) - 1 || nz == 0)
     throw Fail{SCS_EINVAL, "streamed layout: too many sections or nonzeros"};
   // 1. entries by (warp section, owning lane, rotated gather bank)
-  int* rowid = dalloc<int>(h, nz);
+  rowid = dalloc<int>(h, nz);
   unsigned long long* key = dalloc<unsigned long long>(h, nz);
   unsigned long long* skey = dalloc<unsigned long long>(h, nz);
   int* perm_in = dalloc<int>(h, nz);
-  int* perm = dalloc<int>(h, nz);
+  perm = dalloc<int>(h, nz);
   k_expand_rows<<<elem_grid(h, rows * 32), kBlock, 0, h->st>>>(M.rp, rows, rowid);
   k_stm_keys<<<elem_grid(h, nz), kBlock, 0, h->st>>>(rowid, M.ci, nz, F.W, F.S, key);
   k_iota<<<elem_grid(h, nz), kBlock, 0, h->st>>>(perm_in, nz);
@@ -1571,22 +1581,33 @@ void build_stream(scs_handle* h, int mat) {
   dfree(h, key);
   dfree(h, perm_in);
   // 2. sections, slots (pinned / overflow) and depths
-  int* sec = dalloc<int>(h, nz);
+  sec = dalloc<int>(h, nz);
   k_stm_sec<<<elem_grid(h, nz), kBlock, 0, h->st>>>(skey, nz, sec);
   long long* sec_ptr = dalloc<long long>(h, nsec + 1);
   k_rowptr<<<elem_grid(h, nsec + 1), kBlock, 0, h->st>>>(sec, nz, nsec, sec_ptr);
-  int* slot = dalloc<int>(h, nz);
+  slot = dalloc<int>(h, nz);
   unsigned short* depth = dalloc<unsigned short>(h, nsec);
   k_stm_pin<<<elem_grid(h, nsec), kBlock, 0, h->st>>>(sec_ptr, nsec, skey, perm, slot, depth);
   CK(cudaGetLastError());
-  std::vector<unsigned short> D(nsec);
+  D.assign(nsec, 0);
   d2h(h, D.data(), depth, nsec);
-  std::vector<long long> rp_h(rows + 1);
-  d2h(h, rp_h.data(), M.rp, rows + 1);
   CK(cudaStreamSynchronize(h->st));
   dfree(h, depth);
   dfree(h, sec_ptr);
   dfree(h, skey);
+  long long nbad = 0, nne = 0;
+  for (long long q = 0; q < nsec; ++q) {
+    nbad += D[q] == 0xffff;
+    nne += D[q] != 0;
+  }
+  dbg("stream pin mat=%d W=%d sections=%lld flagged=%lld", mat, F.W, nne, nbad);
+  if (wforced || W <= 256 || nbad * 1000 <= nne) break;
+  for (void* p : {(void*)rowid, (void*)perm, (void*)sec, (void*)slot}) dfree(h, p);
+  W /= 4;
+  }
+  std::vector<long long> rp_h(rows + 1);
+  d2h(h, rp_h.data(), M.rp, rows + 1);
+  CK(cudaStreamSynchronize(h->st));
   // 5. host: tiled sub-blocks, pieces, blob offsets
   StmTiles T;
   T.NB = F.NB;
@@ -1754,12 +1775,6 @@ void setup_stream(scs_handle* h) {
   if (force < 0 && h->nnz < 20000000LL) return;
   size_t need = 0;
   for (int mat = 0; mat < 2; ++mat) {
-    // where a row meets a 4096-column slab >= 3 times on average the slab-
-    // tiled SELL kernel (tiled.cuh) is faster (config 3); streamed tiles
-    // win on wide matrices with short row segments (config 5)
-    const double rows = mat == 0 ? h->m : h->n, cols = mat == 0 ? h->n : h->m;
-    const double seg = (double)h->nnz / std::max(rows, 1.0) * std::min(1.0, 4096.0 / std::max(cols, 1.0));
-    if (force < 0 && seg >= 3.0) continue;
     build_stream(h, mat);
     h->stm_m[mat] = true;
     for (int pair = 0; pair < 2; ++pair)

@@ -57,7 +57,7 @@ constexpr int kStmMaxStages = 4;
 constexpr int kStmPin = kStmSecRows / 32;  // rows pinned to each lane
 constexpr unsigned kStmSentinel = 2u << 24;   // padding slot (STM_PAD)
 
-enum : unsigned short { STM_END = 1, STM_CSR = 2, STM_PAIR = 4, STM_TILE = 8 };
+enum : unsigned short { STM_END = 1, STM_CSR = 2, STM_PAIR = 4, STM_TILE = 8, STM_CSR32 = 16 };
 
 struct StmCmd {
   unsigned long long off;  // blob byte offset
@@ -186,6 +186,33 @@ __device__ __forceinline__ void stm_piece(const double* vals, const unsigned* id
   for (; k < k1; ++k) stm_steps<NV, STRIDE, 1>(vals, idx, k, xs, a);
 }
 
+// CSR unit rows [r0, rend) of this warp, L lanes per row (warp-uniform loop)
+template <int L, int NV, int STRIDE, class Epi>
+__device__ __forceinline__ void stm_csr(Epi& epi, const Csr& M, long long r0, long long rend,
+                                        int splits, long long rows, double* P, double* red) {
+  constexpr int G = 32 / L;
+  const int lane = threadIdx.x & 31, gl = lane & (L - 1), gi = lane / L;
+  for (long long rb = r0; rb < rend; rb += G) {
+    const long long r = rb + gi;
+    const bool ok = r < rend;
+    long long k0 = 0, k1 = 0;
+    if (ok) { k0 = __ldg(M.rp + r); k1 = __ldg(M.rp + r + 1); }
+    double s[NV];
+    row_dot<L, NV, STRIDE>(M, k0, k1, gl, epi.xb, s);
+    if (ok && gl == 0) {
+      if (splits > 1) {
+        for (int q = 0; q < splits; ++q)
+#pragma unroll
+          for (int t = 0; t < NV; ++t) P[((long long)q * rows + r) * NV + t] = q == 0 ? s[t] : 0.0;
+      } else {
+        typename Epi::Pre pre;
+        epi.pre(r, pre);
+        epi.row(r, s, pre, red);
+      }
+    }
+  }
+}
+
 template <int NV, int STRIDE, class Epi>
 __global__ void __launch_bounds__(kStmThreads, 1)
     k_stream(Stm F, const StmCmd* __restrict__ cmds, const long long* __restrict__ coff, Csr M,
@@ -287,29 +314,14 @@ __global__ void __launch_bounds__(kStmThreads, 1)
       mbar_wait(full + st, ph);
       const StmCtl c = sctl[st];
       if (c.flags & STM_CSR) {
-        // sparse sub-block: L = 4 lanes per row straight from CSR
+        // sparse sub-block straight from CSR: 4 lanes per row, or a warp per
+        // row when its rows are long
         const long long r0 = c.row0 + (long long)warp * kStmSecRows;
         const long long rend = (r0 + kStmSecRows < F.rows) ? r0 + kStmSecRows : F.rows;
-        const int gl = lane & 3, gi = lane >> 2;
-        for (long long rb = r0; rb < rend; rb += 8) {
-          const long long r = rb + gi;
-          const bool ok = r < rend;
-          long long k0 = 0, k1 = 0;
-          if (ok) { k0 = __ldg(M.rp + r); k1 = __ldg(M.rp + r + 1); }
-          double s[NV];
-          row_dot<4, NV, STRIDE>(M, k0, k1, gl, epi.xb, s);
-          if (ok && gl == 0) {
-            if (splits > 1) {
-              for (int q = 0; q < splits; ++q)
-#pragma unroll
-                for (int t = 0; t < NV; ++t) P[((long long)q * F.rows + r) * NV + t] = q == 0 ? s[t] : 0.0;
-            } else {
-              typename Epi::Pre pre;
-              epi.pre(r, pre);
-              epi.row(r, s, pre, red);
-            }
-          }
-        }
+        if (c.flags & STM_CSR32)
+          stm_csr<32, NV, STRIDE>(epi, M, r0, rend, splits, F.rows, P, red);
+        else
+          stm_csr<4, NV, STRIDE>(epi, M, r0, rend, splits, F.rows, P, red);
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + st);
         continue;
@@ -393,7 +405,7 @@ __global__ void k_stm_sec(const unsigned long long* key, long long nnz, int* sec
 // steps or 2 D0 + 16 (rows far longer than their neighbours) are flagged
 // 0xffff and their sub-block becomes a CSR unit.
 // slot = step * 32 + lane, | 1 << 30 for overflow.
-constexpr int kStmPinMax = 64;
+constexpr int kStmPinMax = 128;
 __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned long long* key,
                           int* perm, int* slot, unsigned short* depth) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
