@@ -489,10 +489,15 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
         // (owner lanes' pinned entries, overflow entries), then every other
         // lane picks, step by step, the remaining entry of its run whose
         // bank is least used at that step in its half-warp
-        unsigned char use[kStmPinMax][2][16];
-        for (int k = 0; k < D; ++k)
+        // (16-byte gathers of NV = 2 passes conflict per quarter-warp over
+        // 8 bank quads: those counts weigh 4x in the choice)
+        unsigned char use[kStmPinMax][2][16], useq[kStmPinMax][4][8];
+        for (int k = 0; k < D; ++k) {
           for (int h = 0; h < 2; ++h)
             for (int b = 0; b < 16; ++b) use[k][h][b] = 0;
+          for (int h = 0; h < 4; ++h)
+            for (int b = 0; b < 8; ++b) useq[k][h][b] = 0;
+        }
         auto bank = [&](long long e) {
           return (unsigned)(((key[e] >> 3) + (key[e] >> 7)) & 15u);  // (col - lane) + lane
         };
@@ -502,10 +507,12 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
             const long long e = run0[l] + i;
             slot[e] = i * 32 + l;
             use[i][l >> 4][bank(e)]++;
+            useq[i][l >> 3][bank(e) & 7u]++;
           }
           for (long long e = run0[l] + D; e < run0[l] + cnt[l]; ++e) {
             const int sl = slot[e] & ((1 << 30) - 1);
             use[sl >> 5][(sl & 31) >> 4][bank(e)]++;
+            useq[sl >> 5][(sl & 31) >> 3][bank(e) & 7u]++;
           }
         }
         for (int l = 0; l < 32; ++l) {
@@ -516,7 +523,8 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
             long long best = run0[l] + i;
             int bu = 1 << 30;
             for (long long e = run0[l] + i; e < run0[l] + cnt[l]; ++e) {
-              const int u = use[k][l >> 4][bank(e)];
+              const unsigned b = bank(e);
+              const int u = 4 * useq[k][l >> 3][b & 7u] + use[k][l >> 4][b];
               if (u < bu) { bu = u; best = e; }
             }
             const long long a = run0[l] + i;
@@ -525,6 +533,7 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
               const int tp = perm[a]; perm[a] = perm[best]; perm[best] = tp;
             }
             use[k][l >> 4][bank(a)]++;
+            useq[k][l >> 3][bank(a) & 7u]++;
             slot[a] = k * 32 + l;
           }
         }

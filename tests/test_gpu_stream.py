@@ -71,7 +71,8 @@ def test_stream_products_match_dense(stream, shape):
 
 
 def test_stream_skewed_rows(stream):
-    """A dense row and a dense column among short ones (FFD depth > E/32)."""
+    """A dense row and a dense column among short ones (pinned depths far
+    above E / 32: deeper sections, narrower slabs or a CSR unit)."""
     m, n = 9000, 6000
     colptr, rows, vals = random_csc(m, n, 0.0005, 11)
     A = dense(colptr, rows, vals, m)
@@ -125,3 +126,22 @@ def test_stream_lasso_deterministic(monkeypatch):
                          P.ConeSpec.from_any(cone))
     runs = [P.Workspace(data, P.Settings(max_iters=40)).solve() for _ in range(2)]
     assert np.array_equal(runs[0].x, runs[1].x) and np.array_equal(runs[0].y, runs[1].y)
+
+
+@pytest.mark.parametrize("name", ["c1_lp_soc", "c2_lp_infeasible", "ref_lasso"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_stream_row_shards_match_reference(monkeypatch, name, world):
+    """Row shards (emulated all-reduce group) over streamed tiles: raw
+    partial products of the A^T passes (EpiRaw through the streamed kernel,
+    split partials), all-reduced, against the reference's first iterates."""
+    from test_gpu_sharded import fixture_prob, settings_from, sharded
+    monkeypatch.setenv("SCS_STREAM", "1")
+    monkeypatch.setenv("SCS_STREAM_W", "256")
+    prob, d = fixture_prob(name)
+    st = settings_from(d["settings"])
+    res, traj = sharded(prob, st, world)
+    kept = [int(k) for k in d["kept"]]
+    for i, k in enumerate(kept):
+        if k in traj:
+            assert rel(traj[k], d["us"][i]) < 1e-9, (name, world, k)
+    assert all(s.status.value == d["status"] for _, s in res)
