@@ -1418,9 +1418,18 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T) {
   }
   const int G0 = h->sms;
   int splits = 1;
-  // enough units for longest-processing-time balance (>= ~16 per CTA)
-  if (ntiled > 0 && ntiled < 16LL * G0)
-    splits = (int)std::min<long long>(std::min<long long>(32, T.S), (16LL * G0 + ntiled - 1) / ntiled);
+  // enough units for longest-processing-time balance (>= ~16 per CTA), as
+  // long as the split partial rows (written, then read by k_tiled_combine)
+  // stay within ~3% of the pass's bytes
+  const long long per_cta = env_ll("SCS_STREAM_UNITS", 16);
+  if (ntiled > 0 && ntiled < per_cta * G0) {
+    double bytes = 0.0;
+    for (long long t = 0; t < (long long)T.NB * T.S; ++t) bytes += 12.0 * (double)T.slots[t];
+    const double part = 16.0 * (pair ? 1 : 2) * (double)F.rows;
+    const long long cap = std::max<long long>(1, (long long)(0.03 * bytes / std::max(part, 1.0)));
+    splits = (int)std::min<long long>(std::min<long long>(std::min<long long>(32, T.S), cap),
+                                      (per_cta * G0 + ntiled - 1) / ntiled);
+  }
   splits = (int)env_ll("SCS_STREAM_SPLITS", splits);
   splits = std::max(1, std::min(splits, std::max(1, T.S)));
   if (splits > 255) splits = 255;
@@ -2588,6 +2597,26 @@ void do_begin(scs_handle* h, const double* wx, const double* wy, const double* w
   h->launches = 0;
 }
 
+// Row-sharded: a Jacobi non-convergence is detected on the rank that owns
+// the PSD block only; OR the error bits over all ranks at every batch end so
+// that every rank raises after the same batch (instead of the others
+// waiting in the next collective).
+__global__ void k_err_pack(Ctl* c, double* d) {
+  if (threadIdx.x < 4) d[threadIdx.x] = (c->err >> threadIdx.x) & 1 ? 1.0 : 0.0;
+}
+__global__ void k_err_unpack(Ctl* c, const double* d) {
+  if (threadIdx.x) return;
+  int e = 0;
+  for (int b = 0; b < 4; ++b) e |= d[b] > 0.0 ? 1 << b : 0;
+  if (e) { c->err |= e; c->stop = 1; }
+}
+void share_err(scs_handle* h) {
+  if (!h->sharded) return;
+  k_err_pack<<<1, 32, 0, h->st>>>(h->ctl, h->dscal);
+  allreduce(h, h->dscal, 4);
+  k_err_unpack<<<1, 32, 0, h->st>>>(h->ctl, h->dscal);
+}
+
 // run up to k iterations, stopping at termination or max_iters
 void do_steps(scs_handle* h, long long k) {
   Ctl* c = h->ctl_h;
@@ -2598,6 +2627,7 @@ void do_steps(scs_handle* h, long long k) {
     for (long long i = 0; i < b; ++i) run_iteration(h);
     h->launched_iters += b;
     todo -= b;
+    share_err(h);
     pull_ctl(h);
     dbg("steps: launched=%lld iter=%lld status=%d stop=%d err=%d cg_it=%d", h->launched_iters,
         c->iter, c->status, c->stop, c->err, c->cg_it);
