@@ -95,6 +95,7 @@ struct Cones {
   int n_psd;
   const long long* psd_off;
   const int* psd_side;
+  const long long* psd_goff;      // global scratch offset of blocks beyond the smem side (-1: smem)
   long long psd_lo, psd_hi;       // y range of all PSD blocks
   long long exp_lo;               // first exp row
   long long n_exp;

@@ -402,12 +402,19 @@ __global__ void __launch_bounds__(kBlock) k_cone_apply(Vec V, Cones K, double* p
     const long long o = K.psd_off[b];
     double* M;
     double* Vv;
+    double *pcs = cs, *psn = sn, *pdp = dpp, *pdq = dqq;
+    int *ppp = pp, *pqq = qq;
     if (k <= smem_side) { M = smem; Vv = smem + k * k; }
-    else {
-      M = psd_scratch + (size_t)2 * blockIdx.x * K.max_side * K.max_side;
+    else {  // matrices (and, beyond 128 rotation pairs, the pair arrays) in global scratch
+      M = psd_scratch + K.psd_goff[b];
       Vv = M + (size_t)k * k;
+      const int np = (k + 1) / 2;
+      if (np > 128) {
+        pcs = Vv + (size_t)k * k; psn = pcs + np; pdp = psn + np; pdq = pdp + np;
+        ppp = reinterpret_cast<int*>(pdq + np); pqq = ppp + np;
+      }
     }
-    psd_block<0>(CtaGroup{}, V, c, o, k, corr, al, M, Vv, cs, sn, pp, qq, dpp, dqq);
+    psd_block<0>(CtaGroup{}, V, c, o, k, corr, al, M, Vv, pcs, psn, ppp, pqq, pdp, pdq);
   }
 }
 
@@ -2157,7 +2164,6 @@ void build_cones(scs_handle* h, const scs_problem* P) {
   int side = 0;
   while ((size_t)2 * (side + 1) * (side + 1) * sizeof(double) <= budget) ++side;
   h->smem_side = std::min(side, 255);
-  if (max_side > 255) throw Fail{SCS_EINVAL, "PSD side > 255 is not supported by the device Jacobi kernel"};
   if (const char* e = getenv("SCS_PSD_WARP")) h->warp_side = atoi(e) ? kWarpPsd : 0;
   const int s_used = max_side > h->warp_side ? std::min(max_side, h->smem_side) : 0;
   // CTA-per-block region for large blocks; per-warp regions for small ones
@@ -2172,8 +2178,20 @@ void build_cones(scs_handle* h, const scs_problem* P) {
     h->n_psd_small = (int)small.size();
     if (!small.empty()) h->psd_small_list = up_i(small);
   }
-  if (max_side > h->smem_side)
-    h->psd_scratch = dalloc<double>(h, (size_t)2 * max_side * max_side * h->grid_full);
+  // blocks beyond the shared-memory side: M, V (and the rotation-pair
+  // arrays when > 128 pairs) in global scratch, one region per block
+  {
+    std::vector<long long> goff(psd_side.size(), -1);
+    long long tot = 0;
+    for (size_t b = 0; b < psd_side.size(); ++b) {
+      const long long k = psd_side[b];
+      if (k <= h->smem_side || k <= h->warp_side) continue;
+      goff[b] = tot;
+      tot += 2 * k * k + 5 * ((k + 1) / 2) + 8;
+    }
+    if (tot) h->psd_scratch = dalloc<double>(h, tot);
+    if (!goff.empty()) h->K.psd_goff = up_ll(goff);
+  }
   if (h->cone_smem > 48 * 1024)
     CK(cudaFuncSetAttribute(k_cone_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)h->cone_smem));

@@ -255,3 +255,24 @@ def test_north_star_signature_and_dict():
     doc = P.solution_to_dict(sol)
     assert set(doc) >= {"status", "x", "y", "s", "info"}
     assert abs(doc["x"][0] - float(d["x"][0])) < 1e-9
+
+
+@pytest.mark.parametrize("sides", [[300], [600, 2, 257]])
+def test_large_psd_sides_vs_eigh(sides):
+    """PSD blocks beyond the shared-memory side (and beyond 128 rotation
+    pairs): matrices and pair arrays in global scratch.  The projection is
+    unique, so numpy's eigh (not the pure-Python Jacobi restatement, too
+    slow at these sides) is the checker."""
+    rng = np.random.default_rng(sum(sides))
+    cone = {"s": sides}
+    oc = O.cone_from_spec(cone)
+    x = rng.standard_normal(oc.dim)
+    got = native.project_cone(x, cone, "dual")
+    off = 0
+    for k in sides:
+        d = k * (k + 1) // 2
+        m = O.svec_to_mat(x[off:off + d], k)
+        w, v = np.linalg.eigh(0.5 * (m + m.T))
+        exp = O.mat_to_svec((v * np.maximum(w, 0.0)) @ v.T)
+        np.testing.assert_allclose(got[off:off + d], exp, atol=1e-9 * (1 + np.abs(x).max()))
+        off += d
