@@ -1425,17 +1425,20 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T) {
   }
   const int G0 = h->sms;
   int splits = 1;
-  // enough units for longest-processing-time balance (>= ~16 per CTA), as
-  // long as the split partial rows (written, then read by k_tiled_combine)
-  // stay within ~3% of the pass's bytes
-  const long long per_cta = env_ll("SCS_STREAM_UNITS", 16);
-  if (ntiled > 0 && ntiled < per_cta * G0) {
+  // splits: the split count minimising (LPT makespan bound) + (split
+  // partial rows written and read back by k_tiled_combine, + a launch)
+  if (ntiled > 0) {
     double bytes = 0.0;
-    for (long long t = 0; t < (long long)T.NB * T.S; ++t) bytes += 12.0 * (double)T.slots[t];
+    for (long long t = 0; t < (long long)T.NB * T.S; ++t) bytes += 10.0 * (double)T.slots[t];
     const double part = 16.0 * (pair ? 1 : 2) * (double)F.rows;
-    const long long cap = std::max<long long>(1, (long long)(0.03 * bytes / std::max(part, 1.0)));
-    splits = (int)std::min<long long>(std::min<long long>(std::min<long long>(32, T.S), cap),
-                                      (per_cta * G0 + ntiled - 1) / ntiled);
+    double best = 1e300;
+    for (int sp = 1; sp <= std::min(32, std::max(1, T.S)); ++sp) {
+      // longest-processing-time makespan <= average + largest unit
+      const double U = (double)ntiled * sp;
+      const double t = (bytes / G0 + bytes / U) / (6.0e12 / G0) +
+                       (sp > 1 ? part * sp / 5.0e12 + 5e-6 : 0.0);
+      if (t < best * 0.99) { best = t; splits = sp; }
+    }
   }
   splits = (int)env_ll("SCS_STREAM_SPLITS", splits);
   splits = std::max(1, std::min(splits, std::max(1, T.S)));
@@ -1457,7 +1460,7 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T) {
       bool any = false;
       for (int q = 0; q < u.nsb; ++q) {
         const long long t = (u.sb0 + q) * T.S + s;
-        a += 12.0 * (double)T.slots[t] + 2048.0 * T.np[t];  // + per-stage overhead
+        a += 10.0 * (double)T.slots[t] + 2048.0 * T.np[t];  // + per-stage overhead
         any = any || T.np[t] > 0;
       }
       cum[s + 1] = cum[s] + a + (any ? slab_cost : 0.0);
@@ -1516,7 +1519,7 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T) {
             const long long p = T.pf[t] + j;
             StmCmd c{};
             c.off = T.poff[p];
-            c.bytes = (unsigned)(kStmHdr + 12ULL * T.pslots[p]);
+            c.bytes = (unsigned)stm_piece_bytes(T.pslots[p]);
             c.slab = (unsigned)s;
             c.row0 = u.sb0 * kStmRS;
             c.flags = pf;
@@ -1558,13 +1561,14 @@ void build_stream(scs_handle* h, int mat) {
   // slab width: 2048 columns, narrowed (/4, down to 256) when dense rows
   // make warp sections deeper than k_stm_pin handles (> 0.1% flagged)
   const bool wforced = getenv("SCS_STREAM_W") != nullptr;
-  long long W = std::min<long long>(65536, std::max<long long>(32, env_ll("SCS_STREAM_W", 2048)));  // >= 32: padding gathers column = lane
+  long long W = std::min<long long>(kStmMaxW, std::max<long long>(32, env_ll("SCS_STREAM_W", 2048)));  // >= 32: padding gathers column = lane
   F.cap = (int)(env_ll("SCS_STREAM_CAP", 32768) & ~15LL);
-  const int min_cap = kStmHdr + 12 * 32 * kStmWarps;
+  const int min_cap = (int)stm_piece_bytes(32 * kStmWarps);
   if (F.cap < min_cap) F.cap = (min_cap + 15) & ~15;
   F.NB = (int)((rows + kStmRS - 1) / kStmRS);
   long long ntile = 0, nsec = 0;
   int *rowid = nullptr, *perm = nullptr, *sec = nullptr, *slot = nullptr;
+  unsigned char* hown = nullptr;
   std::vector<unsigned short> D;
   for (;;) {
   F.W = (int)W;
@@ -1603,7 +1607,8 @@ void build_stream(scs_handle* h, int mat) {
   k_rowptr<<<elem_grid(h, nsec + 1), kBlock, 0, h->st>>>(sec, nz, nsec, sec_ptr);
   slot = dalloc<int>(h, nz);
   unsigned short* depth = dalloc<unsigned short>(h, nsec);
-  k_stm_pin<<<elem_grid(h, nsec), kBlock, 0, h->st>>>(sec_ptr, nsec, skey, perm, slot, depth);
+  hown = dalloc<unsigned char>(h, nsec * 32);
+  k_stm_pin<<<elem_grid(h, nsec), kBlock, 0, h->st>>>(sec_ptr, nsec, skey, perm, slot, depth, hown);
   CK(cudaGetLastError());
   D.assign(nsec, 0);
   d2h(h, D.data(), depth, nsec);
@@ -1618,7 +1623,7 @@ void build_stream(scs_handle* h, int mat) {
   }
   dbg("stream pin mat=%d W=%d sections=%lld flagged=%lld", mat, F.W, nne, nbad);
   if (wforced || W <= 256 || nbad * 1000 <= nne) break;
-  for (void* p : {(void*)rowid, (void*)perm, (void*)sec, (void*)slot}) dfree(h, p);
+  for (void* p : {(void*)rowid, (void*)perm, (void*)sec, (void*)slot, (void*)hown}) dfree(h, p);
   W /= 4;
   }
   std::vector<long long> rp_h(rows + 1);
@@ -1654,6 +1659,7 @@ void build_stream(scs_handle* h, int mat) {
     T.tiled[sb] = !bad && (nt == 0 || sl >= min_avg * nt || T.nnz_sb[sb] > 16 * (r1 - r0)) ? 1 : 0;
   }
   std::vector<unsigned short> tile_kp(ntile, 1), pwsec;
+  std::vector<long long> ptile;  // tile of every piece
   long long npiece = 0;
   unsigned long long bytes = 0;
   for (long long t = 0; t < ntile; ++t) {
@@ -1661,13 +1667,13 @@ void build_stream(scs_handle* h, int mat) {
     const unsigned short* d = &D[t * kStmWarps];
     int maxd = 0;
     for (int w = 0; w < kStmWarps; ++w) maxd = std::max<int>(maxd, d[w]);
-    int np = (int)std::max<long long>(1, (12 * T.slots[t] + (F.cap - kStmHdr) - 1) / (F.cap - kStmHdr));
+    int np = (int)std::max<long long>(1, (10 * T.slots[t] + (F.cap - kStmData) - 1) / (F.cap - kStmData));
     int kp = 0;
     for (;; ++np) {
       kp = (maxd + np - 1) / np;
       long long first = 0;  // piece 0 is the largest
       for (int w = 0; w < kStmWarps; ++w) first += std::min<int>(d[w], kp);
-      if (kStmHdr + 12LL * 32 * first <= F.cap) break;
+      if (stm_piece_bytes(32ULL * first) <= (unsigned long long)F.cap) break;
     }
     np = (maxd + kp - 1) / kp;
     tile_kp[t] = (unsigned short)kp;
@@ -1683,8 +1689,9 @@ void build_stream(scs_handle* h, int mat) {
       }
       const unsigned ns = 32u * acc;
       T.poff.push_back(bytes);
+      ptile.push_back(t);
       T.pslots.push_back(ns);
-      bytes += kStmHdr + 12ULL * ns;
+      bytes += stm_piece_bytes(ns);
       ++npiece;
     }
   }
@@ -1701,14 +1708,19 @@ void build_stream(scs_handle* h, int mat) {
   h2d(h, d_pslots, T.pslots.data(), npiece);
   h2d(h, d_pwsec, pwsec.data(), pwsec.size());
   if (npiece) {
-    k_stm_init<<<elem_grid(h, npiece * 32), kBlock, 0, h->st>>>(blob, d_poff, d_pslots, d_pwsec, npiece);
+    long long* d_ptile = dalloc<long long>(h, npiece);
+    h2d(h, d_ptile, ptile.data(), npiece);
+    k_stm_init<<<elem_grid(h, npiece * 32), kBlock, 0, h->st>>>(blob, d_poff, d_pslots, d_pwsec,
+                                                                d_ptile, hown, npiece);
     k_stm_scatter<<<elem_grid(h, nz), kBlock, 0, h->st>>>(sec, slot, nz, perm, rowid, M.ci, M.v, d_pf,
                                                           d_kp, d_poff, d_pslots, d_pwsec, F.W, blob);
     CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->st));
+    dfree(h, d_ptile);
   }
   CK(cudaStreamSynchronize(h->st));
   for (void* p : {(void*)d_pf, (void*)d_kp, (void*)d_poff, (void*)d_pslots, (void*)d_pwsec,
-                  (void*)sec, (void*)slot, (void*)perm, (void*)rowid})
+                  (void*)sec, (void*)slot, (void*)perm, (void*)rowid, (void*)hown})
     dfree(h, p);
   F.blob = blob;
   long long ncsr = 0;

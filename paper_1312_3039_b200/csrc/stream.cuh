@@ -52,10 +52,16 @@ constexpr int kStmSecRows = 256;    // rows per warp section
 constexpr int kStmWarps = kStmRS / kStmSecRows;  // 16 consumer warps
 constexpr int kStmThreads = (kStmWarps + 1) * 32;
 constexpr int kStmHdr = 48;         // piece header bytes: u32 nslots, u16 wsec[17]
+constexpr int kStmOwn = 32 * 16;    // + per warp section, per lane: owner lane of its overflow slots
+constexpr int kStmData = kStmHdr + kStmOwn;  // values start here; then u16 slot words
+constexpr int kStmMaxW = 2048;      // slot word column field: 11 bits
+__host__ __device__ constexpr unsigned long long stm_piece_bytes(unsigned long long ns) {
+  return kStmData + 10ULL * ns;
+}
 constexpr int kStmAccBytes = 2 * kStmRS * 8;
 constexpr int kStmMaxStages = 4;
 constexpr int kStmPin = kStmSecRows / 32;  // rows pinned to each lane
-constexpr unsigned kStmSentinel = 2u << 24;   // padding slot (STM_PAD)
+constexpr unsigned kStmSentinel = 2u << 14;   // padding slot word (flags 2)
 
 enum : unsigned short { STM_END = 1, STM_CSR = 2, STM_PAIR = 4, STM_TILE = 8, STM_CSR32 = 16 };
 
@@ -156,8 +162,8 @@ __device__ __forceinline__ void stm_rows(Epi& epi, double* a, long long r0, int 
 // and k_stm_pin keeps them off the steps where the owner lane holds the
 // same row, so the rows of a step are always distinct.
 template <int NV, int STRIDE, int U>
-__device__ __forceinline__ void stm_steps(const double* vals, const unsigned* idx, int k,
-                                          const double* xs, double* a) {
+__device__ __forceinline__ void stm_steps(const double* vals, const unsigned short* idx, int k,
+                                          const double* xs, double* a, unsigned own) {
   const int lane = threadIdx.x & 31;
   double pr[U][NV];
   unsigned rw[U], fl[U];
@@ -165,9 +171,9 @@ __device__ __forceinline__ void stm_steps(const double* vals, const unsigned* id
   for (int u = 0; u < U; ++u) {  // every load of the batch before its stores
     const double v = vals[(k + u) * 32 + lane];
     const unsigned id = idx[(k + u) * 32 + lane];
-    rw[u] = (id >> 16) & 0xffu;
-    fl[u] = id >> 24;
-    const unsigned col = id & 0xffffu;
+    fl[u] = id >> 14;
+    rw[u] = ((id >> 11) & 7u) << 5 | (fl[u] == 1u ? own : (unsigned)lane);
+    const unsigned col = id & 0x7ffu;
 #pragma unroll
     for (int t = 0; t < NV; ++t) pr[u][t] = v * xs[col * STRIDE + t];
   }
@@ -179,11 +185,11 @@ __device__ __forceinline__ void stm_steps(const double* vals, const unsigned* id
 }
 
 template <int NV, int STRIDE>
-__device__ __forceinline__ void stm_piece(const double* vals, const unsigned* idx, int k0, int k1,
-                                          const double* xs, double* a) {
+__device__ __forceinline__ void stm_piece(const double* vals, const unsigned short* idx, int k0,
+                                          int k1, const double* xs, double* a, unsigned own) {
   int k = k0;
-  for (; k + 4 <= k1; k += 4) stm_steps<NV, STRIDE, 4>(vals, idx, k, xs, a);
-  for (; k < k1; ++k) stm_steps<NV, STRIDE, 1>(vals, idx, k, xs, a);
+  for (; k + 4 <= k1; k += 4) stm_steps<NV, STRIDE, 4>(vals, idx, k, xs, a, own);
+  for (; k < k1; ++k) stm_steps<NV, STRIDE, 1>(vals, idx, k, xs, a, own);
 }
 
 // CSR unit rows [r0, rend) of this warp, L lanes per row (warp-uniform loop)
@@ -332,11 +338,13 @@ __global__ void __launch_bounds__(kStmThreads, 1)
         if (nslots) {
           const unsigned short* wsec = reinterpret_cast<const unsigned short*>(blob + 4);
           const int k0 = wsec[warp], k1 = wsec[warp + 1];
-          const double* vals = reinterpret_cast<const double*>(blob + kStmHdr);
-          const unsigned* idx = reinterpret_cast<const unsigned*>(blob + kStmHdr + 8 * (size_t)nslots);
+          const unsigned own = blob[kStmHdr + warp * 32 + lane];
+          const double* vals = reinterpret_cast<const double*>(blob + kStmData);
+          const unsigned short* idx =
+              reinterpret_cast<const unsigned short*>(blob + kStmData + 8 * (size_t)nslots);
           const double* xs = xbuf0 + (size_t)c.xbuf * (xbytes / 8);
           double* a = acc + ((size_t)c.half * kStmRS + (size_t)warp * kStmSecRows) * NV;
-          stm_piece<NV, STRIDE>(vals, idx, k0, k1, xs, a);
+          stm_piece<NV, STRIDE>(vals, idx, k0, k1, xs, a, own);
         }
       }
       __syncwarp();
@@ -401,22 +409,25 @@ __global__ void k_stm_sec(const unsigned long long* key, long long nnz, int* sec
 // distinct steps, so two overflow entries of one row never share a step;
 // pinned entries of the owner are then swapped (key and perm, inside the
 // owner's run) so that no step holds a pinned and an overflow entry of the
-// same row.  D grows until this succeeds; sections deeper than kStmPinMax
+// same row.  A lane hosts the overflow of at most one owner (hown: the
+// owner of each lane's overflow slots, so a slot word needs only the row's
+// j = row >> 5).  D grows until this succeeds; sections deeper than kStmPinMax
 // steps or 2 D0 + 16 (rows far longer than their neighbours) are flagged
 // 0xffff and their sub-block becomes a CSR unit.
 // slot = step * 32 + lane, | 1 << 30 for overflow.
 constexpr int kStmPinMax = 128;
 __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned long long* key,
-                          int* perm, int* slot, unsigned short* depth) {
+                          int* perm, int* slot, unsigned short* depth, unsigned char* hown) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long s = tid; s < nsec; s += nt) {
     const long long p0 = sec_ptr[s], p1 = sec_ptr[s + 1];
     const long long E = p1 - p0;
+    for (int l = 0; l < 32; ++l) hown[s * 32 + l] = 0xff;
     if (E == 0) { depth[s] = 0; continue; }
     const int D0 = (int)((E + 31) / 32);
     if (D0 > kStmPinMax) { depth[s] = 0xffff; continue; }
-    int cnt[32];
+    int cnt[32], host[32];
     long long run0[32];
     unsigned freem[kStmPinMax];
     int ostep[kStmPinMax];
@@ -441,6 +452,7 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
       }
       ok = true;
       unsigned done = 0;
+      for (int l = 0; l < 32; ++l) host[l] = -1;  // a lane hosts the overflow of one owner
       for (int g = 0; g < 32 && ok; ++g) {  // owners by overflow size, descending
         int l = -1, o = 0;
         for (int c = 0; c < 32; ++c)
@@ -449,12 +461,15 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
         done |= 1u << l;
         // steps where the partner lane l ^ 16 (same accumulator banks as l,
         // other half-warp) is free first: hosting there adds no bank conflict
-        const unsigned partner = 1u << (l ^ 16);
+        unsigned allow = 0;
+        for (int c = 0; c < 32; ++c)
+          if (c != l && (host[c] < 0 || host[c] == l)) allow |= 1u << c;
+        const unsigned partner = (1u << (l ^ 16)) & allow;
         int n = 0;
         for (int k = D - 1; k >= 0 && n < o; --k)
           if (freem[k] & partner) ostep[n++] = k;
         for (int k = D - 1; k >= 0 && n < o; --k)
-          if ((freem[k] & ~(1u << l)) && !(freem[k] & partner)) ostep[n++] = k;
+          if ((freem[k] & allow) && !(freem[k] & partner)) ostep[n++] = k;
         if (n < o) { ok = false; break; }
         const long long run = run0[l];
         for (int q = 0; q < o && ok; ++q) {  // row-distinct steps: swap pinned entries
@@ -477,8 +492,13 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
         }
         for (int q = 0; q < o && ok; ++q) {
           const int k = ostep[q];
-          const unsigned m = freem[k] & ~(1u << l);
-          const int lane = (m & partner) ? (l ^ 16) : __ffs(m) - 1;
+          const unsigned m = freem[k] & allow;
+          int lane = -1;  // prefer the partner, then a lane already hosting l
+          if (m & partner) lane = l ^ 16;
+          for (int c = 0; c < 32 && lane < 0; ++c)
+            if ((m >> c & 1u) && host[c] == l) lane = c;
+          if (lane < 0) lane = __ffs(m) - 1;
+          host[lane] = l;
           freem[k] &= ~(1u << lane);
           slot[run + D + q] = (k * 32 + lane) | (1 << 30);
         }
@@ -540,13 +560,16 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
       }
     }
     if (!ok) { depth[s] = 0xffff; continue; }
+    for (int l = 0; l < 32; ++l) hown[s * 32 + l] = host[l] < 0 ? 0xff : (unsigned char)host[l];
     depth[s] = (unsigned short)(D - 1);  // the loop stepped past the depth that worked
   }
 }
 
-// piece headers + padding (values 0, sentinel rows): one warp per piece
+// piece headers, owner tables, padding (values 0, padding words): one warp
+// per piece
 __global__ void k_stm_init(unsigned char* blob, const unsigned long long* poff, const unsigned* pslots,
-                           const unsigned short* pwsec, long long npiece) {
+                           const unsigned short* pwsec, const long long* ptile,
+                           const unsigned char* hown, long long npiece) {
   const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -556,10 +579,15 @@ __global__ void k_stm_init(unsigned char* blob, const unsigned long long* poff, 
     if (lane == 0) *reinterpret_cast<unsigned*>(b) = ns;
     if (lane < kStmWarps + 1)
       reinterpret_cast<unsigned short*>(b + 4)[lane] = pwsec[p * (kStmWarps + 1) + lane];
-    double* v = reinterpret_cast<double*>(b + kStmHdr);
-    unsigned* id = reinterpret_cast<unsigned*>(b + kStmHdr + 8 * (size_t)ns);
+    const long long sec0 = ptile[p] * kStmWarps;
+    for (int q = lane; q < kStmWarps * 32; q += 32) b[kStmHdr + q] = hown[sec0 * 32 + q];
+    double* v = reinterpret_cast<double*>(b + kStmData);
+    unsigned short* id = reinterpret_cast<unsigned short*>(b + kStmData + 8 * (size_t)ns);
     // padding gathers column = lane: distinct banks, no conflict with the real entries
-    for (unsigned k = lane; k < ns; k += 32) { v[k] = 0.0; id[k] = kStmSentinel | (unsigned)lane; }
+    for (unsigned k = lane; k < ns; k += 32) {
+      v[k] = 0.0;
+      id[k] = (unsigned short)(kStmSentinel | (unsigned)lane);
+    }
   }
 }
 
@@ -588,9 +616,9 @@ __global__ void k_stm_scatter(const int* sec, const int* slot, long long nnz, co
     const long long at = ((long long)pwsec[piece * (kStmWarps + 1) + w] + kk) * 32 + lane;
     const int s = perm[e];
     const unsigned rl = (unsigned)(rowid[s] % kStmSecRows);
-    reinterpret_cast<double*>(bl + kStmHdr)[at] = val[s];
-    reinterpret_cast<unsigned*>(bl + kStmHdr + 8 * (size_t)ns)[at] =
-        (unsigned)(ci[s] % W) | (rl << 16) | (ovf << 24);
+    reinterpret_cast<double*>(bl + kStmData)[at] = val[s];
+    reinterpret_cast<unsigned short*>(bl + kStmData + 8 * (size_t)ns)[at] =
+        (unsigned short)((unsigned)(ci[s] % W) | ((rl >> 5) << 11) | (ovf << 14));
   }
 }
 
