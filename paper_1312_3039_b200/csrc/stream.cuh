@@ -542,7 +542,9 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
             const int k = (i + r) % D;
             long long best = run0[l] + i;
             int bu = 1 << 30;
-            for (long long e = run0[l] + i; e < run0[l] + cnt[l]; ++e) {
+            // candidates: the next 8 entries of the run (keeps deep sections linear)
+            const long long e_end = run0[l] + (cnt[l] < i + 8 ? cnt[l] : i + 8);
+            for (long long e = run0[l] + i; e < e_end; ++e) {
               const unsigned b = bank(e);
               const int u = 4 * useq[k][l >> 3][b & 7u] + use[k][l >> 4][b];
               if (u < bu) { bu = u; best = e; }
