@@ -26,4 +26,15 @@ from .api import (  # noqa: F401
     validate_problem,
 )
 
+from .problem_io import (  # noqa: F401
+    FileFormatError,
+    problem_from_dict,
+    problem_to_dict,
+    read_problem,
+    read_solution,
+    solution_from_dict,
+    write_problem,
+    write_solution,
+)
+
 __version__ = "0.1.0"

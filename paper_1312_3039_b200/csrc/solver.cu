@@ -4,6 +4,7 @@
 // the C-ABI declared in include/scs_b200.h.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -372,7 +373,8 @@ __device__ void psd_block(const G& g, const Vec& V, Ctl* c, long long o, int k_r
 }
 
 __global__ void __launch_bounds__(kBlock) k_cone_apply(Vec V, Cones K, double* psd_scratch,
-                                                       int smem_side, int warp_side) {
+                                                       int smem_side, int warp_side,
+                                                       int grid_max) {
   Ctl* c = V.ctl;
   if (c->stop) return;
   const double corr = c->corr, al = c->alpha;
@@ -399,6 +401,7 @@ __global__ void __launch_bounds__(kBlock) k_cone_apply(Vec V, Cones K, double* p
   for (int b = blockIdx.x; b < K.n_psd; b += gridDim.x) {
     const int k = K.psd_side[b];
     if (k <= warp_side) continue;
+    if (k > smem_side && k <= grid_max) continue;  // k_psd_grid
     const long long o = K.psd_off[b];
     double* M;
     double* Vv;
@@ -440,6 +443,243 @@ __global__ void __launch_bounds__(kBlock) k_psd_small(Vec V, Cones K, const int*
     const int k = K.psd_side[b];
     psd_block<0>(WarpGroup{}, V, c, K.psd_off[b], k, corr, al, M, M + k * k, wcs[wi], wsn[wi],
                  wpp[wi], wqq[wi], wdp[wi], wdq[wi]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Large PSD blocks (side > the shared-memory side; RPCA's 2p x 2p block,
+// generators.py:197-286): the whole cooperative grid works on one block at a
+// time, M and V in global scratch (row-major, L2-resident up to side ~2500),
+// two grid barriers per Jacobi round.  Same parallel (round-robin) order,
+// tiny-entry rule and stopping test as group_jacobi (cones.cuh), which
+// follows _kernels.py:137-191.  A round applies M <- J^T M J as independent
+// 2x2-block updates: thread item (pi, pj) reads rows {p_i, q_i} x columns
+// {p_j, q_j}, applies the column then the row rotation and writes them back
+// in place (no other item touches those four entries), and item (i, pj)
+// rotates columns p_j, q_j of row i of V.  Items whose two rotations are
+// both the identity are skipped (most of them in the late sweeps).  Every
+// CTA computes the round's rotation parameters for all pairs redundantly
+// into shared memory from the diagonal blocks (a barrier then separates
+// those reads from the diagonal-block writes).  Loads and stores go through L2 (__ldcg / __stcg): another SM
+// wrote the data in the previous round.  The reconstruction
+// X = V diag(max(lambda, 0)) V^T is a tiled fp64 product over the lower
+// triangle of 64 x 64 tiles, written straight into svec order.
+// ---------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+constexpr int kPsdTile = 64, kPsdTk = 32;
+constexpr size_t kPsdTileSmem = (size_t)2 * kPsdTk * (kPsdTile + 1) * sizeof(double);
+__host__ __device__ constexpr size_t psd_grid_pair_bytes(int k) {
+  return (size_t)((k + 1) / 2) * (4 * sizeof(double) + 2 * sizeof(int));
+}
+
+// deterministic grid sum: per-CTA partials, barrier, every thread adds them
+// in CTA order; a trailing barrier frees `part` for the next use
+__device__ double psd_grid_sum(const cg::grid_group& grid, double v, double* part) {
+  double a[1] = {v};
+  block_sum<1>(a);
+  if (threadIdx.x == 0) __stcg(part + blockIdx.x, a[0]);
+  grid.sync();
+  double t = 0.0;
+  for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(part + b);
+  grid.sync();
+  return t;
+}
+
+__device__ __forceinline__ long long svec_index(int r, int col, int k) {
+  // element (r, col), r >= col, of the column-major packed lower triangle
+  return (long long)col * k - (long long)col * (col - 1) / 2 + (r - col);
+}
+
+__global__ void __launch_bounds__(kBlock) k_psd_grid(Vec V, Cones K, double* psd_scratch,
+                                                     const int* list, int count, double* part) {
+  cg::grid_group grid = cg::this_grid();
+  Ctl* c = V.ctl;
+  if (c->stop) return;
+  const double corr = c->corr, al = c->alpha;
+  extern __shared__ double smem[];
+  const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long gsz = (long long)gridDim.x * blockDim.x;
+  for (int bi = 0; bi < count; ++bi) {
+    const int b = list[bi];
+    const int k = K.psd_side[b];
+    const long long o = K.psd_off[b];
+    double* M = psd_scratch + K.psd_goff[b];
+    double* Vv = M + (size_t)k * k;
+    double* lam = Vv + (size_t)k * k;
+    // unpack the relaxed point (off-diagonals / sqrt 2) and V = I
+    double fro = 0.0;
+    for (long long w = gtid; w < (long long)k * k; w += gsz) {
+      const int i = (int)(w / k), j = (int)(w % k);
+      const long long e = i >= j ? svec_index(i, j, k) : svec_index(j, i, k);
+      const double t = relax_y(V, o + e, corr, al).t;
+      const double val = i == j ? t : t / 1.4142135623730951;
+      __stcg(M + w, val);
+      __stcg(Vv + w, i == j ? 1.0 : 0.0);
+      fro += val * val;
+    }
+    fro = psd_grid_sum(grid, fro, part);
+    if (!isfinite(fro)) {
+      if (gtid == 0) atomicOr(&c->err, ERR_CONE_NONFINITE);
+      continue;
+    }
+    const double thresh = 1e-12 * sqrt(fro);
+    const double tiny = thresh / (2.0 * k);
+    const int kk = k + (k & 1);
+    const int np = kk / 2;
+    double* cs = smem;
+    double* sn = cs + np;
+    double* dp = sn + np;
+    double* dq = dp + np;
+    int* pp = reinterpret_cast<int*>(dq + np);
+    int* qq = pp + np;
+    bool ok = k == 1;
+    for (int sweep = 0; sweep <= 100 && !ok; ++sweep) {
+      double off = 0.0;
+      for (long long w = gtid; w < (long long)k * k; w += gsz) {
+        const int i = (int)(w / k), j = (int)(w % k);
+        if (j > i) { const double x = __ldcg(M + w); off += 2.0 * x * x; }
+      }
+      off = psd_grid_sum(grid, off, part);
+      if (sqrt(off) <= thresh) { ok = true; break; }
+      if (sweep == 100) break;
+      for (int step = 0; step < kk - 1; ++step) {
+        for (int pi = threadIdx.x; pi < np; pi += blockDim.x) {
+          const int a = rr_player(pi, step, kk), bb = rr_player(kk - 1 - pi, step, kk);
+          const int p = a < bb ? a : bb, q = a < bb ? bb : a;
+          double cc = 1.0, ss = 0.0, vp = 0.0, vq = 0.0;
+          if (q < k) {
+            const double apq = __ldcg(M + (size_t)p * k + q);
+            const double app = __ldcg(M + (size_t)p * k + p), aqq = __ldcg(M + (size_t)q * k + q);
+            vp = app; vq = aqq;
+            if (fabs(apq) > tiny) {
+              const double tau = (aqq - app) / (2.0 * apq);
+              const double root = sqrt(1.0 + tau * tau);
+              const double t = tau >= 0.0 ? 1.0 / (tau + root) : 1.0 / (tau - root);
+              cc = 1.0 / sqrt(1.0 + t * t);
+              ss = t * cc;
+              vp = app - t * apq;
+              vq = aqq + t * apq;
+            }
+          }
+          pp[pi] = p; qq[pi] = q; cs[pi] = cc; sn[pi] = ss; dp[pi] = vp; dq[pi] = vq;
+        }
+        // the diagonal-block items below overwrite the entries the other
+        // CTAs read for these parameters
+        grid.sync();
+        const long long nm = (long long)np * np, nitem = nm + (long long)k * np;
+        for (long long w = gtid; w < nitem; w += gsz) {
+          if (w < nm) {
+            const int pi = (int)(w / np), pj = (int)(w % np);
+            const int p = pp[pi], q = qq[pi];
+            if (pi == pj) {  // diagonal block: eigenvalue estimates, zero coupling
+              if (q < k) {
+                if (sn[pi] != 0.0) {
+                  __stcg(M + (size_t)p * k + p, dp[pi]);
+                  __stcg(M + (size_t)q * k + q, dq[pi]);
+                }
+                __stcg(M + (size_t)p * k + q, 0.0);
+                __stcg(M + (size_t)q * k + p, 0.0);
+              }
+              continue;
+            }
+            const double si = sn[pi], sj = sn[pj];
+            if (si == 0.0 && sj == 0.0) continue;
+            const double ci = cs[pi], cj = cs[pj];
+            const int r = pp[pj], s = qq[pj];
+            const bool qv = q < k, sv = s < k;
+            double* Mp = M + (size_t)p * k;
+            double* Mq = M + (size_t)q * k;
+            double b00 = __ldcg(Mp + r), b01 = sv ? __ldcg(Mp + s) : 0.0;
+            double b10 = qv ? __ldcg(Mq + r) : 0.0, b11 = (qv && sv) ? __ldcg(Mq + s) : 0.0;
+            if (sj != 0.0) {  // columns r, s
+              const double t00 = cj * b00 - sj * b01, t01 = sj * b00 + cj * b01;
+              const double t10 = cj * b10 - sj * b11, t11 = sj * b10 + cj * b11;
+              b00 = t00; b01 = t01; b10 = t10; b11 = t11;
+            }
+            if (si != 0.0) {  // rows p, q
+              const double t00 = ci * b00 - si * b10, t10 = si * b00 + ci * b10;
+              const double t01 = ci * b01 - si * b11, t11 = si * b01 + ci * b11;
+              b00 = t00; b01 = t01; b10 = t10; b11 = t11;
+            }
+            __stcg(Mp + r, b00);
+            if (sv) __stcg(Mp + s, b01);
+            if (qv) {
+              __stcg(Mq + r, b10);
+              if (sv) __stcg(Mq + s, b11);
+            }
+          } else {
+            const long long u = w - nm;
+            const int i = (int)(u / np), pj = (int)(u % np);
+            const double sj = sn[pj];
+            if (sj == 0.0) continue;
+            const double cj = cs[pj];
+            double* row = Vv + (size_t)i * k;
+            const int r = pp[pj], s = qq[pj];
+            const double va = __ldcg(row + r), vb = __ldcg(row + s);
+            __stcg(row + r, cj * va - sj * vb);
+            __stcg(row + s, sj * va + cj * vb);
+          }
+        }
+        grid.sync();
+      }
+    }
+    if (!ok) {
+      if (gtid == 0) atomicOr(&c->err, ERR_JACOBI);
+      continue;
+    }
+    for (long long t = gtid; t < k; t += gsz) {
+      const double x = __ldcg(M + (size_t)t * k + t);
+      __stcg(lam + t, x > 0.0 ? x : 0.0);
+    }
+    grid.sync();
+    // X = V diag(lam+) V^T over lower-triangle tiles: As = (V lam) rows of
+    // tile ti, Bs = V rows of tile tj, k-chunks of kPsdTk
+    const int nt = (k + kPsdTile - 1) / kPsdTile;
+    const long long ntiles = (long long)nt * (nt + 1) / 2;
+    double (*As)[kPsdTile + 1] = reinterpret_cast<double (*)[kPsdTile + 1]>(smem);
+    double (*Bs)[kPsdTile + 1] = As + kPsdTk;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4 x 4 each
+    for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+      int ti = (int)((sqrt(8.0 * (double)tl + 1.0) - 1.0) / 2.0);
+      while ((long long)(ti + 1) * (ti + 2) / 2 <= tl) ++ti;
+      while ((long long)ti * (ti + 1) / 2 > tl) --ti;
+      const int tj = (int)(tl - (long long)ti * (ti + 1) / 2);
+      const int r0 = ti * kPsdTile, c0 = tj * kPsdTile;
+      double acc[4][4] = {};
+      for (int t0 = 0; t0 < k; t0 += kPsdTk) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPsdTk * kPsdTile; e += blockDim.x) {
+          const int rr = e / kPsdTk, tt = e % kPsdTk;
+          const int t = t0 + tt;
+          const bool tin = t < k;
+          const int gi = r0 + rr, gj = c0 + rr;
+          As[tt][rr] = (tin && gi < k) ? __ldcg(Vv + (size_t)gi * k + t) * __ldcg(lam + t) : 0.0;
+          Bs[tt][rr] = (tin && gj < k) ? __ldcg(Vv + (size_t)gj * k + t) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int tt = 0; tt < kPsdTk; ++tt) {
+          double a[4], bv[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) { a[x] = As[tt][ty + 16 * x]; bv[x] = Bs[tt][tx + 16 * x]; }
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], bv[y], acc[x][y]);
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int i = r0 + ty + 16 * x, j = c0 + tx + 16 * y;
+          if (i >= k || j >= k || i < j) continue;
+          const long long e = o + svec_index(i, j, k);
+          const Relax r = relax_y(V, e, corr, al);
+          store_y(V, e, r.ub, i == j ? acc[x][y] : acc[x][y] * 1.4142135623730951);
+        }
+    }
+    grid.sync();
   }
 }
 
@@ -953,6 +1193,12 @@ struct scs_handle {
   int warp_side = kWarpPsd;  // PSD blocks up to this side: warp per block (SCS_PSD_WARP=0: off)
   int n_psd_small = 0;
   const int* psd_small_list = nullptr;  // their block indices, largest side first
+  int n_psd_grid = 0;                   // blocks beyond smem_side: cooperative grid each
+  const int* psd_grid_list = nullptr;
+  int psd_grid_ctas = 0;
+  int psd_grid_max = 0;                 // largest side k_psd_grid takes (0: off)
+  size_t psd_grid_smem = 0;
+  double* psd_grid_part = nullptr;
   size_t cone_smem = 0;
   int cone_red_len = 3;
   // vectors
@@ -2204,6 +2450,43 @@ void build_cones(scs_handle* h, const scs_problem* P) {
     if (tot) h->psd_scratch = dalloc<double>(h, tot);
     if (!goff.empty()) h->K.psd_goff = up_ll(goff);
   }
+  // those blocks go to the cooperative-grid Jacobi (SCS_PSD_GRID=0: one CTA
+  // each in k_cone_apply, the r01 path) while its pair table fits in smem
+  {
+    bool use = true;
+    if (const char* e = getenv("SCS_PSD_GRID")) use = atoi(e) != 0;
+    std::vector<int> big;
+    int kmax = 0;
+    if (use) {
+      h->psd_grid_max = h->smem_side;
+      while (psd_grid_pair_bytes(h->psd_grid_max + 1) <= budget) ++h->psd_grid_max;
+    }
+    for (size_t b = 0; b < psd_side.size() && use; ++b) {
+      const int k = psd_side[b];
+      if (k <= h->smem_side || k <= h->warp_side || k > h->psd_grid_max) continue;
+      big.push_back((int)b);
+      kmax = std::max(kmax, k);
+    }
+    if (!big.empty()) {
+      h->n_psd_grid = (int)big.size();
+      h->psd_grid_list = up_i(big);
+      h->psd_grid_smem = std::max(kPsdTileSmem, psd_grid_pair_bytes(kmax));
+      if (h->psd_grid_smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(k_psd_grid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)h->psd_grid_smem));
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_psd_grid, kBlock,
+                                                       h->psd_grid_smem));
+      if (occ < 1) throw Fail{SCS_ECUDA, "k_psd_grid: no resident CTA"};
+      int per_sm = std::min(occ, 2);
+      if (const char* e = getenv("SCS_PSD_GRID_PER_SM")) per_sm = std::max(1, std::min(occ, atoi(e)));
+      // small sides: fewer CTAs (cheaper barriers), ~16 items per thread
+      const long long items = (long long)kmax * kmax * 3 / 4;
+      const long long want = (items + 16LL * kBlock - 1) / (16LL * kBlock);
+      h->psd_grid_ctas = (int)std::max<long long>(1, std::min<long long>(want, (long long)h->sms * per_sm));
+      h->psd_grid_part = dalloc<double>(h, h->psd_grid_ctas);
+    }
+  }
   if (h->cone_smem > 48 * 1024)
     CK(cudaFuncSetAttribute(k_cone_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)h->cone_smem));
@@ -2528,11 +2811,11 @@ void enqueue_iteration(scs_handle* h) {
 
 // big SOCs and large PSD blocks (CTA each), then small PSD blocks (warp each)
 void launch_cone_apply(scs_handle* h, const Vec& V) {
-  const int n_big = h->K.n_psd - h->n_psd_small;
+  const int n_big = h->K.n_psd - h->n_psd_small - h->n_psd_grid;
   if (h->K.n_chunk > 0 || n_big > 0) {
     const int g = std::max(1, std::min(std::max(h->K.n_chunk, n_big), h->grid_full));
     k_cone_apply<<<g, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side,
-                                                      h->warp_side);
+                                                      h->warp_side, h->psd_grid_max);
     h->launches++;
   }
   if (h->n_psd_small > 0) {
@@ -2540,6 +2823,21 @@ void launch_cone_apply(scs_handle* h, const Vec& V) {
                                             (long long)h->sms * 32);
     k_psd_small<<<(int)g, kBlock, kPsdSmallSmem, h->st>>>(V, h->K, h->psd_small_list,
                                                           h->n_psd_small);
+    h->launches++;
+  }
+  if (h->n_psd_grid > 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(h->psd_grid_ctas);
+    cfg.blockDim = dim3(kBlock);
+    cfg.dynamicSmemBytes = h->psd_grid_smem;
+    cfg.stream = h->st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_psd_grid, V, h->K, h->psd_scratch, h->psd_grid_list,
+                          h->n_psd_grid, h->psd_grid_part));
     h->launches++;
   }
 }

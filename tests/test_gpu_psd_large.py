@@ -1,0 +1,116 @@
+"""GPU parity of the cooperative-grid Jacobi for large PSD blocks
+(`k_psd_grid`, sides beyond the shared-memory side; the
+RPCA block of generators.py:197-286).
+
+The PSD projection is unique, so at these sides numpy's eigh (the pure-Python
+Jacobi restatement is too slow) and the r01 one-CTA path (SCS_PSD_GRID=0,
+itself checked against eigh) are the checkers.  The reference's stopping
+rule (_kernels.py:137-191) is kept, so results agree to rounding.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1312_3039_b200 as P
+from paper_1312_3039_b200 import native
+from oracle import scs_oracle as O
+
+from _fixtures import rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _eigh_proj(x, k):
+    m = O.svec_to_mat(x, k)
+    w, v = np.linalg.eigh(0.5 * (m + m.T))
+    return O.mat_to_svec((v * np.maximum(w, 0.0)) @ v.T)
+
+
+@pytest.mark.parametrize("sides", [[130], [1000], [2000, 3, 501], [117, 116, 20, 300]])
+def test_grid_psd_vs_eigh(sides):
+    rng = np.random.default_rng(7 + sum(sides))
+    cone = {"s": sides}
+    x = rng.standard_normal(O.cone_from_spec(cone).dim)
+    got = native.project_cone(x, cone, "dual")
+    off = 0
+    for k in sides:
+        d = k * (k + 1) // 2
+        exp = _eigh_proj(x[off:off + d], k)
+        np.testing.assert_allclose(got[off:off + d], exp, atol=1e-9 * (1 + np.abs(x).max()))
+        off += d
+
+
+def test_grid_psd_low_rank_and_clustered():
+    """Clustered spectra (many equal eigenvalues: the tiny-entry rule) and a
+    rank-deficient input, primal and dual projections."""
+    rng = np.random.default_rng(3)
+    k = 400
+    q, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    w = np.concatenate([np.full(150, 2.0), np.full(150, -1.0), rng.standard_normal(100)])
+    m = (q * w) @ q.T
+    x = O.mat_to_svec(m)
+    for kind in ("dual", "primal"):
+        got = native.project_cone(x, {"s": [k]}, kind)
+        exp = _eigh_proj(x, k) if kind == "dual" else x + _eigh_proj(-x, k)
+        np.testing.assert_allclose(got, exp, atol=1e-9 * (1 + np.abs(x).max()))
+
+
+def test_grid_matches_cta_path(monkeypatch):
+    rng = np.random.default_rng(11)
+    cone = {"l": 5, "q": [4], "s": [200, 9, 160]}
+    x = rng.standard_normal(O.cone_from_spec(cone).dim)
+    got = native.project_cone(x, cone, "dual")
+    monkeypatch.setenv("SCS_PSD_GRID", "0")
+    old = native.project_cone(x, cone, "dual")
+    np.testing.assert_allclose(got, old, atol=1e-10 * (1 + np.abs(x).max()))
+
+
+def _min_eig_sdp(k, seed):
+    """min tr(C X) s.t. tr(X) = 1, X PSD (optimum: lambda_min(C)), in the
+    reference's standard form: one zero-cone row, then s = x in the PSD cone."""
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((k, k))
+    C = 0.5 * (g + g.T) / np.sqrt(k)
+    d = k * (k + 1) // 2
+    diag = O.mat_to_svec(np.eye(k))
+    dense = np.zeros((1 + d, d))
+    dense[0] = diag
+    dense[1:] = -np.eye(d)
+    b = np.zeros(1 + d)
+    b[0] = 1.0
+    c = O.mat_to_svec(C)
+    colptr, rowidx, vals = [0], [], []
+    for j in range(d):
+        nz = np.nonzero(dense[:, j])[0]
+        rowidx.extend(nz)
+        vals.extend(dense[nz, j])
+        colptr.append(len(rowidx))
+    A = P.SparseMatrix(1 + d, d, np.array(colptr, np.int64), np.array(rowidx, np.int64),
+                       np.array(vals, np.float64))
+    return P.ProblemData(A, b, c, P.ConeSpec.from_any({"z": 1, "s": [k]})), C
+
+
+def test_sdp_solve_grid_vs_cta_path(monkeypatch):
+    """Full solves through the graph-captured iteration (the cooperative
+    launch inside the CUDA graph): same iterates as the one-CTA path to 1e-9
+    for 50 iterations, same status and iteration count, optimum = lambda_min."""
+    prob, C = _min_eig_sdp(150, 5)
+    st = P.Settings(eps_pri=1e-5, eps_dual=1e-5, eps_gap=1e-5, max_iters=5000)
+
+    def run():
+        traj = {}
+        P.Workspace(prob, P.Settings(max_iters=50)).solve(
+            on_iteration=lambda s: traj.__setitem__(s.iter, s.u.copy()))
+        return P.Workspace(prob, st).solve(), traj
+
+    sol, traj = run()
+    monkeypatch.setenv("SCS_PSD_GRID", "0")
+    sol0, traj0 = run()
+    assert len(traj0) == 50
+    for it in traj0:
+        assert rel(traj[it], traj0[it]) < 1e-9, it
+    assert sol.status is P.Status.SOLVED and sol0.status is P.Status.SOLVED
+    assert abs(sol.info.iterations - sol0.info.iterations) <= 1
+    lam = np.linalg.eigvalsh(C)[0]
+    assert abs(sol.objective - lam) <= 1e-3 * (1 + abs(lam))
+    assert abs(sol.objective - sol0.objective) <= 1e-8 * (1 + abs(lam))
