@@ -490,7 +490,7 @@ __device__ __forceinline__ long long svec_index(int r, int col, int k) {
   return (long long)col * k - (long long)col * (col - 1) / 2 + (r - col);
 }
 
-__global__ void __launch_bounds__(kBlock) k_psd_grid(Vec V, Cones K, double* psd_scratch,
+__global__ void __launch_bounds__(kBlock, 2) k_psd_grid(Vec V, Cones K, double* psd_scratch,
                                                      const int* list, int count, double* part) {
   cg::grid_group grid = cg::this_grid();
   Ctl* c = V.ctl;
@@ -499,6 +499,8 @@ __global__ void __launch_bounds__(kBlock) k_psd_grid(Vec V, Cones K, double* psd
   extern __shared__ double smem[];
   const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long gsz = (long long)gridDim.x * blockDim.x;
+  const int gtid32 = (int)gtid, gsz32 = (int)gsz;
+  constexpr int kU = 4;
   for (int bi = 0; bi < count; ++bi) {
     const int b = list[bi];
     const int k = K.psd_side[b];
@@ -543,81 +545,116 @@ __global__ void __launch_bounds__(kBlock) k_psd_grid(Vec V, Cones K, double* psd
       if (sqrt(off) <= thresh) { ok = true; break; }
       if (sweep == 100) break;
       for (int step = 0; step < kk - 1; ++step) {
-        for (int pi = threadIdx.x; pi < np; pi += blockDim.x) {
-          const int a = rr_player(pi, step, kk), bb = rr_player(kk - 1 - pi, step, kk);
-          const int p = a < bb ? a : bb, q = a < bb ? bb : a;
-          double cc = 1.0, ss = 0.0, vp = 0.0, vq = 0.0;
-          if (q < k) {
-            const double apq = __ldcg(M + (size_t)p * k + q);
-            const double app = __ldcg(M + (size_t)p * k + p), aqq = __ldcg(M + (size_t)q * k + q);
-            vp = app; vq = aqq;
-            if (fabs(apq) > tiny) {
-              const double tau = (aqq - app) / (2.0 * apq);
+        // rotation parameters of every pair (loads of kU pairs in flight)
+        for (int p0 = threadIdx.x; p0 < np; p0 += kU * blockDim.x) {
+          int pv[kU], qv[kU];
+          double apq[kU], app[kU], aqq[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int pi = p0 + u * blockDim.x;
+            pv[u] = 0; qv[u] = k;
+            apq[u] = app[u] = aqq[u] = 0.0;
+            if (pi < np) {
+              const int a = rr_player(pi, step, kk), bb = rr_player(kk - 1 - pi, step, kk);
+              pv[u] = a < bb ? a : bb; qv[u] = a < bb ? bb : a;
+              if (qv[u] < k) {
+                apq[u] = __ldcg(M + (size_t)pv[u] * k + qv[u]);
+                app[u] = __ldcg(M + (size_t)pv[u] * k + pv[u]);
+                aqq[u] = __ldcg(M + (size_t)qv[u] * k + qv[u]);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int pi = p0 + u * blockDim.x;
+            if (pi >= np) continue;
+            double cc = 1.0, ss = 0.0, vp = app[u], vq = aqq[u];
+            if (qv[u] < k && fabs(apq[u]) > tiny) {
+              const double tau = (aqq[u] - app[u]) / (2.0 * apq[u]);
               const double root = sqrt(1.0 + tau * tau);
               const double t = tau >= 0.0 ? 1.0 / (tau + root) : 1.0 / (tau - root);
               cc = 1.0 / sqrt(1.0 + t * t);
               ss = t * cc;
-              vp = app - t * apq;
-              vq = aqq + t * apq;
+              vp = app[u] - t * apq[u];
+              vq = aqq[u] + t * apq[u];
             }
+            pp[pi] = pv[u]; qq[pi] = qv[u]; cs[pi] = cc; sn[pi] = ss; dp[pi] = vp; dq[pi] = vq;
           }
-          pp[pi] = p; qq[pi] = q; cs[pi] = cc; sn[pi] = ss; dp[pi] = vp; dq[pi] = vq;
         }
         // the diagonal-block items below overwrite the entries the other
         // CTAs read for these parameters
         grid.sync();
-        const long long nm = (long long)np * np, nitem = nm + (long long)k * np;
-        for (long long w = gtid; w < nitem; w += gsz) {
-          if (w < nm) {
-            const int pi = (int)(w / np), pj = (int)(w % np);
-            const int p = pp[pi], q = qq[pi];
-            if (pi == pj) {  // diagonal block: eigenvalue estimates, zero coupling
-              if (q < k) {
-                if (sn[pi] != 0.0) {
-                  __stcg(M + (size_t)p * k + p, dp[pi]);
-                  __stcg(M + (size_t)q * k + q, dq[pi]);
+        // items: M blocks (pi, pj), then V (row i, pair pj); kU items per
+        // thread have their loads issued before any store (items are disjoint)
+        const int nm = np * np, nitem = nm + k * np;
+        for (int w0 = gtid32; w0 < nitem; w0 += kU * gsz32) {
+          int kind[kU], off[kU][4];
+          double x[kU][4], ci[kU], si[kU], cj[kU], sj[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int w = w0 + u * gsz32;
+            kind[u] = 0;
+            if (w < nm) {
+              const int pi = w / np, pj = w - (w / np) * np;
+              const int p = pp[pi], q = qq[pi];
+              if (pi == pj) {  // diagonal block: eigenvalue estimates, zero coupling
+                if (q < k) {
+                  if (sn[pi] != 0.0) {
+                    __stcg(M + (size_t)p * k + p, dp[pi]);
+                    __stcg(M + (size_t)q * k + q, dq[pi]);
+                  }
+                  __stcg(M + (size_t)p * k + q, 0.0);
+                  __stcg(M + (size_t)q * k + p, 0.0);
                 }
-                __stcg(M + (size_t)p * k + q, 0.0);
-                __stcg(M + (size_t)q * k + p, 0.0);
+                continue;
               }
-              continue;
+              si[u] = sn[pi]; sj[u] = sn[pj];
+              if (si[u] == 0.0 && sj[u] == 0.0) continue;
+              ci[u] = cs[pi]; cj[u] = cs[pj];
+              const int r = pp[pj], sc = qq[pj];
+              const bool qok = q < k, sok = sc < k;
+              kind[u] = 1;
+              off[u][0] = p * k + r;
+              off[u][1] = sok ? p * k + sc : -1;
+              off[u][2] = qok ? q * k + r : -1;
+              off[u][3] = (qok && sok) ? q * k + sc : -1;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) x[u][e] = off[u][e] >= 0 ? __ldcg(M + off[u][e]) : 0.0;
+            } else if (w < nitem) {
+              const int v = w - nm;
+              const int i = v / np, pj = v - (v / np) * np;
+              sj[u] = sn[pj];
+              if (sj[u] == 0.0) continue;
+              cj[u] = cs[pj];
+              si[u] = 0.0; ci[u] = 1.0;
+              kind[u] = 2;
+              off[u][0] = i * k + pp[pj];
+              off[u][1] = i * k + qq[pj];
+              off[u][2] = off[u][3] = -1;
+              x[u][0] = __ldcg(Vv + off[u][0]);
+              x[u][1] = __ldcg(Vv + off[u][1]);
+              x[u][2] = x[u][3] = 0.0;
             }
-            const double si = sn[pi], sj = sn[pj];
-            if (si == 0.0 && sj == 0.0) continue;
-            const double ci = cs[pi], cj = cs[pj];
-            const int r = pp[pj], s = qq[pj];
-            const bool qv = q < k, sv = s < k;
-            double* Mp = M + (size_t)p * k;
-            double* Mq = M + (size_t)q * k;
-            double b00 = __ldcg(Mp + r), b01 = sv ? __ldcg(Mp + s) : 0.0;
-            double b10 = qv ? __ldcg(Mq + r) : 0.0, b11 = (qv && sv) ? __ldcg(Mq + s) : 0.0;
-            if (sj != 0.0) {  // columns r, s
-              const double t00 = cj * b00 - sj * b01, t01 = sj * b00 + cj * b01;
-              const double t10 = cj * b10 - sj * b11, t11 = sj * b10 + cj * b11;
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            if (kind[u] == 0) continue;
+            double b00 = x[u][0], b01 = x[u][1], b10 = x[u][2], b11 = x[u][3];
+            if (sj[u] != 0.0) {  // columns r, s
+              const double t00 = cj[u] * b00 - sj[u] * b01, t01 = sj[u] * b00 + cj[u] * b01;
+              const double t10 = cj[u] * b10 - sj[u] * b11, t11 = sj[u] * b10 + cj[u] * b11;
               b00 = t00; b01 = t01; b10 = t10; b11 = t11;
             }
-            if (si != 0.0) {  // rows p, q
-              const double t00 = ci * b00 - si * b10, t10 = si * b00 + ci * b10;
-              const double t01 = ci * b01 - si * b11, t11 = si * b01 + ci * b11;
+            if (si[u] != 0.0) {  // rows p, q
+              const double t00 = ci[u] * b00 - si[u] * b10, t10 = si[u] * b00 + ci[u] * b10;
+              const double t01 = ci[u] * b01 - si[u] * b11, t11 = si[u] * b01 + ci[u] * b11;
               b00 = t00; b01 = t01; b10 = t10; b11 = t11;
             }
-            __stcg(Mp + r, b00);
-            if (sv) __stcg(Mp + s, b01);
-            if (qv) {
-              __stcg(Mq + r, b10);
-              if (sv) __stcg(Mq + s, b11);
-            }
-          } else {
-            const long long u = w - nm;
-            const int i = (int)(u / np), pj = (int)(u % np);
-            const double sj = sn[pj];
-            if (sj == 0.0) continue;
-            const double cj = cs[pj];
-            double* row = Vv + (size_t)i * k;
-            const int r = pp[pj], s = qq[pj];
-            const double va = __ldcg(row + r), vb = __ldcg(row + s);
-            __stcg(row + r, cj * va - sj * vb);
-            __stcg(row + s, sj * va + cj * vb);
+            double* base = kind[u] == 1 ? M : Vv;
+            __stcg(base + off[u][0], b00);
+            if (off[u][1] >= 0) __stcg(base + off[u][1], b01);
+            if (off[u][2] >= 0) __stcg(base + off[u][2], b10);
+            if (off[u][3] >= 0) __stcg(base + off[u][3], b11);
           }
         }
         grid.sync();
