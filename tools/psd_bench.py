@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1312_3039_b200 import native  # noqa: E402
 
 sides = [int(a) for a in sys.argv[1:]] or [256, 500, 1000, 2000]
-old_max = int(os.environ.get("PSD_BENCH_OLD_MAX", "1000"))
+old_max = int(os.environ.get("PSD_BENCH_OLD_MAX", "0"))
 for k in sides:
     rng = np.random.default_rng(k)
     x = rng.standard_normal(k * (k + 1) // 2)
