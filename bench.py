@@ -312,7 +312,7 @@ def run_ours(args, cfg):
     e2e_s = time.perf_counter() - t0
     e2e_iters = sol.info.iterations
     h2d = 8 * (n + 2 * m)
-    d2h = 8 * 2 * (n + m + 1) + 8 * (n + 2 * m)
+    d2h = 8 * (n + 2 * m)  # x, y, s (extracted on the device, scs_extract_point)
     line = {
         "metric": "ADMM iterations/s (indirect SCS, LASSO-as-SOCP)", "value": ips,
         "unit": "iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -325,7 +325,7 @@ def run_ours(args, cfg):
                 "d2h_bytes_per_step": d2h / max(e2e_iters, 1),
                 "iterations": e2e_iters, "seconds": e2e_s,
                 "note": "Workspace.solve(warm_start=host arrays) incl. H2D of the warm start, "
-                        "D2H of (u, v), extraction and point residuals"},
+                        "device extraction, D2H of (x, y, s) and point residuals"},
         "gpu_launches": int(launches_per_iter * args.steps),
         "launches_per_step": int(launches_per_iter),
         "clocks": clk.summary(),
@@ -442,7 +442,7 @@ def run_sharded(args, cfg, rank, world):
                                        "frac": b_iter(m, n, nnz) * ips / 1e9 / (peak * world)}},
             "e2e": {"value": sol.info.iterations / e2e.item(), "unit": "iters/s",
                     "h2d_bytes_per_step": 8 * (n + 2 * (hi - lo)) / max(sol.info.iterations, 1),
-                    "d2h_bytes_per_step": 8 * 3 * (n + hi - lo) / max(sol.info.iterations, 1),
+                    "d2h_bytes_per_step": 8 * (n + 2 * (hi - lo)) / max(sol.info.iterations, 1),
                     "iterations": sol.info.iterations, "seconds": e2e.item()},
             "gpu_launches": int(info.launches), "clocks": clk.summary(),
             "setup_s": setup_s, "generate_s": gen_s, "status_after_timed": int(info.status),

@@ -182,6 +182,14 @@ int scs_update_vectors(scs_handle* h, const double* b, const double* c);
 int scs_point_residuals(scs_handle* h, const double* x, const double* y,
                         const double* s, double* out3);
 
+/* extract_solution for status solved / max_iters_reached (solver.py:251-270,
+ * unscale_solution scaling.py:140-145, _point_residuals solver.py:237-248)
+ * on the device: x (n), y, s (m_local) in original units, copied into the
+ * caller's buffers (each nullable); out5 = {pri, dual, gap, c'x, b'y}
+ * (b'y all-reduced over row shards), so primal_obj = c'x and
+ * dual_obj = -b'y without a second upload of the point. */
+int scs_extract_point(scs_handle* h, double* x, double* y, double* s, double* out5);
+
 /* spmv / spmv_t (sparse_linalg.py:318-335) on the device copy of the
  * ORIGINAL (unscaled) A is not kept; these apply the equilibrated A_hat:
  * which = 0: y = A_hat x; which = 1: x = A_hat^T y. */

@@ -373,7 +373,8 @@ class Workspace:
         self._create()
         self.setup_time = time.perf_counter() - t0
         self.last_setup_time = self.setup_time
-        self.final_state = None
+        self._final = None
+        self._final_iter = None
         self._scal = None
 
     @property
@@ -530,17 +531,47 @@ class Workspace:
                         info.iterations == prev:
                     break
             self._call(self._lib.scs_finish(self._h, native.C.byref(info)))
-        u, v = self.state()
         status = _STATUS_BY_CODE[int(info.status)]
         res = Residuals(*[float(x) for x in info.res])
-        sol = self._extract(u, v, status)
+        self._final = None
+        self._final_iter = int(info.iterations)
+        if status in (Status.SOLVED, Status.MAX_ITERS_REACHED):
+            sol = self._extract_point(status)
+        else:
+            u, v = self.state()
+            self._final = SolverState(u=u, v=v, iter=self._final_iter)
+            sol = self._extract(u, v, status)
         sol.info.iterations = int(info.iterations)
         sol.info.residuals = res
         sol.info.setup_time = self.last_setup_time
         sol.info.solve_time = time.perf_counter() - t0
         sol.info.cg_iters = int(info.cg_iters)
         self.launches = int(info.launches)
-        self.final_state = SolverState(u=u, v=v, iter=int(info.iterations))
+        return sol
+
+    @property
+    def final_state(self):
+        """(u, v, iter) after the last solve (solver.py:374), fetched from the
+        device on first access."""
+        if self._final is None and self._final_iter is not None:
+            u, v = self.state()
+            self._final = SolverState(u=u, v=v, iter=self._final_iter)
+        return self._final
+
+    def _extract_point(self, status):
+        """extract_solution (solver.py:251-270) for solved / max_iters_reached,
+        on the device (scs_extract_point): x, y, s, objectives and point
+        residuals without copying u, v out and the point back in."""
+        d = self.data
+        sol = Solution(status=status)
+        x, y, s = np.empty(d.n), np.empty(d.m), np.empty(d.m)
+        out = np.empty(5)
+        self._call(self._lib.scs_extract_point(self._h, native.ptr(x), native.ptr(y),
+                                               native.ptr(s), native.ptr(out)))
+        sol.x, sol.y, sol.s = x, y, s  # y, s: this shard's rows when sharded
+        sol.primal_obj = float(out[3])
+        sol.dual_obj = float(-out[4])
+        sol.info.pri_res, sol.info.dual_res, sol.info.gap = (float(t) for t in out[:3])
         return sol
 
     def point_residuals(self, x, y, s):

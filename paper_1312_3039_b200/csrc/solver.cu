@@ -1245,6 +1245,7 @@ struct scs_handle {
   double *tmp_n = nullptr, *tmp_m = nullptr, *tmp_m2 = nullptr, *zero_m = nullptr;
   double* Traw = nullptr;   // raw A^T partial products (sharded)
   double* dscal = nullptr;  // device scratch scalars
+  double* ext_y = nullptr;  // y of extract_point / point_residuals (m)
   Ctl* ctl = nullptr;
   Ctl* ctl_h = nullptr;     // pinned mirror
   double sigma = 1.0, rho = 1.0, mean_col = 1.0, mean_row = 1.0;
@@ -3365,39 +3366,93 @@ int scs_apply_a(scs_handle* h, int which, const double* in, double* out) {
   });
 }
 
+// _point_residuals (solver.py:237-248) of a device-resident point (dx: n,
+// dy, ds: m; dx is also read after the passes).  out = {pri, dual, gap,
+// c'x, b'y} (m-length sums all-reduced over row shards).
+void point_residuals_dev(scs_handle* h, const double* dx, const double* dy, const double* ds,
+                         double* out5) {
+  const long long n = h->n, m = h->m;
+  // A x = D^-1 A_hat E^-1 x ; A^T y = E^-1 A_hat^T D^-1 y  (rows may be sharded:
+  // m-length sums are all-reduced, A^T products go through at_pass)
+  k_div<<<elem_grid(h, n), kBlock, 0, h->st>>>(dx, h->E, n, h->V.r);
+  EpiPlain e{};
+  e.V = h->V;
+  e.xb = h->V.r;
+  e.out = h->tmp_m2;
+  a_pass(h, e);
+  k_point_pri<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->tmp_m2, h->D, ds, h->b0, m, h->V.q);
+  const double pri = sqrt(norm2_dev(h, h->V.q, h->V.q, m, 2, true));
+  const double bn = sqrt(norm2_dev(h, h->b0, h->b0, m, 2, true));
+  k_div<<<elem_grid(h, m), kBlock, 0, h->st>>>(dy, h->D, m, h->tmp_m2);
+  EpiPlain f{};
+  f.V = h->V;
+  f.xb = h->tmp_m2;
+  f.out = h->V.Gp;
+  at_pass(h, f);
+  k_point_dual<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->V.Gp, h->E, h->c0, n, h->V.r);
+  const double dual = sqrt(norm2_dev(h, h->V.r, h->V.r, n, 2));
+  const double cn = sqrt(norm2_dev(h, h->c0, h->c0, n, 2));
+  const double ctx = norm2_dev(h, h->c0, dx, n, 2);
+  const double bty = norm2_dev(h, h->b0, dy, m, 2, true);
+  out5[0] = pri / (1.0 + bn);
+  out5[1] = dual / (1.0 + cn);
+  out5[2] = fabs(ctx + bty) / (1.0 + fabs(ctx) + fabs(bty));
+  out5[3] = ctx;
+  out5[4] = bty;
+}
+
+double* ext_y(scs_handle* h) {
+  if (!h->ext_y) h->ext_y = dalloc<double>(h, std::max<long long>(h->m, 1));
+  return h->ext_y;
+}
+
 int scs_point_residuals(scs_handle* h, const double* x, const double* y, const double* s,
                         double* out3) {
   if (!h) return SCS_EINVAL;
   return guard(h, [&] {
-    const long long n = h->n, m = h->m;
-    // A x = D^-1 A_hat E^-1 x ; A^T y = E^-1 A_hat^T D^-1 y  (rows may be sharded:
-    // m-length sums are all-reduced, A^T products go through at_pass)
-    h2d(h, h->tmp_n, x, n);
-    k_div<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->tmp_n, h->E, n, h->V.r);
-    EpiPlain e{};
-    e.V = h->V;
-    e.xb = h->V.r;
-    e.out = h->tmp_m2;
-    a_pass(h, e);
-    h2d(h, h->tmp_m, s, m);
-    k_point_pri<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->tmp_m2, h->D, h->tmp_m, h->b0, m, h->V.q);
-    const double pri = sqrt(norm2_dev(h, h->V.q, h->V.q, m, 2, true));
-    const double bn = sqrt(norm2_dev(h, h->b0, h->b0, m, 2, true));
-    h2d(h, h->tmp_m, y, m);
-    k_div<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->tmp_m, h->D, m, h->tmp_m2);
-    EpiPlain f{};
-    f.V = h->V;
-    f.xb = h->tmp_m2;
-    f.out = h->V.Gp;
-    at_pass(h, f);
-    k_point_dual<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->V.Gp, h->E, h->c0, n, h->V.r);
-    const double dual = sqrt(norm2_dev(h, h->V.r, h->V.r, n, 2));
-    const double cn = sqrt(norm2_dev(h, h->c0, h->c0, n, 2));
-    const double ctx = norm2_dev(h, h->c0, h->tmp_n, n, 2);
-    const double bty = norm2_dev(h, h->b0, h->tmp_m, m, 2, true);
-    out3[0] = pri / (1.0 + bn);
-    out3[1] = dual / (1.0 + cn);
-    out3[2] = fabs(ctx + bty) / (1.0 + fabs(ctx) + fabs(bty));
+    double* dy = ext_y(h);
+    h2d(h, h->tmp_n, x, h->n);
+    h2d(h, h->tmp_m, s, h->m);
+    h2d(h, dy, y, h->m);
+    double out5[5];
+    point_residuals_dev(h, h->tmp_n, dy, h->tmp_m, out5);
+    std::copy(out5, out5 + 3, out3);
+  });
+}
+
+// extract_solution for a solved / max-iterations state (solver.py:251-270,
+// scaling.py:140-145): x = E (u_x / tau) / sigma, y = D (u_y / tau) / rho,
+// s = (v_s / tau) / (D sigma) formed on the device in the reference's
+// operation order, copied out, and their point residuals computed from the
+// device copies (no re-upload).
+__global__ void k_extract(Vec V, const double* D, const double* E, double sigma, double rho,
+                          double* x, double* y, double* s) {
+  const long long n = V.n, m = V.m;
+  const double ut = V.u[n + m];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n + m; i += nt) {
+    if (i < n) {
+      x[i] = E[i] * (V.u[i] / ut) / sigma;
+    } else {
+      const long long j = i - n;
+      y[j] = D[j] * (V.u[i] / ut) / rho;
+      s[j] = (V.v[i] / ut) / (D[j] * sigma);
+    }
+  }
+}
+
+int scs_extract_point(scs_handle* h, double* x, double* y, double* s, double* out5) {
+  if (!h || !out5) return SCS_EINVAL;
+  return guard(h, [&] {
+    double* dy = ext_y(h);
+    k_extract<<<elem_grid(h, h->n + h->m), kBlock, 0, h->st>>>(h->V, h->D, h->E, h->sigma,
+                                                                h->rho, h->tmp_n, dy, h->tmp_m);
+    if (x) d2h(h, x, h->tmp_n, h->n);
+    if (y) d2h(h, y, dy, h->m);
+    if (s) d2h(h, s, h->tmp_m, h->m);
+    point_residuals_dev(h, h->tmp_n, dy, h->tmp_m, out5);
+    CK(cudaStreamSynchronize(h->st));
   });
 }
 

@@ -29,7 +29,7 @@ f64p = C.POINTER(C.c_double)
 EXPORTS = (
     "scs_create", "scs_solve", "scs_begin", "scs_step", "scs_finish",
     "scs_get_state", "scs_get_scaling", "scs_update_vectors",
-    "scs_point_residuals", "scs_apply_a", "scs_project_cone", "scs_destroy",
+    "scs_point_residuals", "scs_extract_point", "scs_apply_a", "scs_project_cone", "scs_destroy",
     "scs_last_error", "scs_abi_version", "scs_nccl_unique_id",
     "scs_partition_rows", "scs_gen_lasso", "scs_bench_iters", "scs_bench_kernel",
     "scs_emu_group_create", "scs_emu_group_destroy", "scs_allreduce",
@@ -96,6 +96,7 @@ def load():
         "scs_get_scaling": (C.c_int, [hp, f64p, f64p, f64p, f64p]),
         "scs_update_vectors": (C.c_int, [hp, f64p, f64p]),
         "scs_point_residuals": (C.c_int, [hp, f64p, f64p, f64p, f64p]),
+        "scs_extract_point": (C.c_int, [hp, f64p, f64p, f64p, f64p]),
         "scs_apply_a": (C.c_int, [hp, C.c_int, f64p, f64p]),
         "scs_project_cone": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, i64p, C.c_int64, i64p,
                                        C.c_int64, C.c_int, C.c_int64, f64p, f64p, C.c_int]),
