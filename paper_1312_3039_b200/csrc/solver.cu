@@ -2493,6 +2493,9 @@ void build_cones(scs_handle* h, const scs_problem* P) {
   {
     bool use = true;
     if (const char* e = getenv("SCS_PSD_GRID")) use = atoi(e) != 0;
+    // emulated group: several shards share this GPU, and two partly resident
+    // cooperative grids could wait on each other's SMs -- one CTA per block
+    if (h->comm && dynamic_cast<EmuComm*>(h->comm)) use = false;
     std::vector<int> big;
     int kmax = 0;
     if (use) {

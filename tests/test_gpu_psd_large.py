@@ -113,3 +113,41 @@ def test_sdp_solve_grid_vs_cta_path(monkeypatch):
     assert sol.status is P.Status.SOLVED
     lam = np.linalg.eigvalsh(C)[0]
     assert abs(sol.objective - lam) <= 1e-2 * (1 + abs(lam))
+
+
+def _tuple(prob):
+    A = prob.A
+    sp = prob.spec
+    return (A.colptr, A.rowidx, A.vals, prob.b, prob.c,
+            {"z": sp.zero_dim, "l": sp.nonneg_dim, "q": list(sp.soc_dims), "s": list(sp.psd_sides)})
+
+
+def test_sdp_sharded_paths_match_single():
+    """Row-sharded code paths with a large PSD block: the NCCL communicator
+    (one rank, sharded path forced on: the cooperative launch captured in one
+    graph with the all-reduces, and the device extraction's all-reduced b'y),
+    and the emulated 2-shard group (which keeps one CTA per block)."""
+    from paper_1312_3039_b200 import parallel
+    prob, _ = _min_eig_sdp(130, 9)
+    st = P.Settings(max_iters=60)
+    t1 = {}
+    sol1 = P.Workspace(prob, st).solve(
+        on_iteration=lambda s: t1.__setitem__(s.iter, s.u.copy()))
+    lib = native.load()
+    buf = (native.C.c_uint8 * 128)()
+    native.check(lib.scs_nccl_unique_id(buf))
+    colptr, rowidx, vals, b, c, cone = _tuple(prob)
+    m = b.size
+    spec = parallel.ShardSpec(0, 1, np.array([0, m], np.int64), nccl_id=bytes(buf), force=True)
+    shard = parallel.shard_problem(colptr, rowidx, vals, b, c, cone, spec.bounds, 0)
+    ws = P.Workspace(shard, st, dist=spec)
+    t2 = {}
+    ws.solve(on_iteration=lambda s: t2.__setitem__(s.iter, s.u.copy()))
+    for k in t1:
+        assert rel(t2[k], t1[k]) < 1e-9, k
+    sol2 = ws.solve()  # graph-launched loop
+    assert sol2.status == sol1.status and sol2.info.iterations == sol1.info.iterations
+    assert abs(sol2.objective - sol1.objective) <= 1e-9 * (1 + abs(sol1.objective))
+    res = parallel.emulated_solve(_tuple(prob), st, 2, bounds=np.array([0, 1, m], np.int64))
+    for _, s in res:
+        assert s.status == sol1.status and s.info.iterations == sol1.info.iterations
