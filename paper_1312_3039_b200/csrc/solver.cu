@@ -499,7 +499,6 @@ __global__ void __launch_bounds__(kBlock, 2) k_psd_grid(Vec V, Cones K, double* 
   extern __shared__ double smem[];
   const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long gsz = (long long)gridDim.x * blockDim.x;
-  const int gtid32 = (int)gtid, gsz32 = (int)gsz;
   constexpr int kU = 4;
   for (int bi = 0; bi < count; ++bi) {
     const int b = list[bi];
@@ -534,6 +533,13 @@ __global__ void __launch_bounds__(kBlock, 2) k_psd_grid(Vec V, Cones K, double* 
     double* dq = dp + np;
     int* pp = reinterpret_cast<int*>(dq + np);
     int* qq = pp + np;
+    // item geometry: rpi row-items per thread pass when the pair count is
+    // below the CTA size, else one row-item and a column loop
+    const int rpi = np >= (int)blockDim.x ? 1 : (int)blockDim.x / np;
+    const int rsub = rpi > 1 ? (int)threadIdx.x / np : 0;
+    const int col0 = rpi > 1 ? (int)threadIdx.x - rsub * np : (int)threadIdx.x;
+    const int cstep = rpi > 1 ? np : (int)blockDim.x;
+    const int ngroup = (np + k + rpi - 1) / rpi;
     bool ok = k == 1;
     for (int sweep = 0; sweep <= 100 && !ok; ++sweep) {
       double off = 0.0;
@@ -584,77 +590,82 @@ __global__ void __launch_bounds__(kBlock, 2) k_psd_grid(Vec V, Cones K, double* 
         // the diagonal-block items below overwrite the entries the other
         // CTAs read for these parameters
         grid.sync();
-        // items: M blocks (pi, pj), then V (row i, pair pj); kU items per
-        // thread have their loads issued before any store (items are disjoint)
-        const int nm = np * np, nitem = nm + k * np;
-        for (int w0 = gtid32; w0 < nitem; w0 += kU * gsz32) {
-          int kind[kU], off[kU][4];
-          double x[kU][4], ci[kU], si[kU], cj[kU], sj[kU];
+        // items: row-items ri < np are M block-rows pi = ri, the rest V rows
+        // i = ri - np; a thread keeps one pair column pj and takes kU
+        // row-items of its CTA's interleaved row groups at a time, all loads
+        // of the batch before any store (items are disjoint)
+        for (int pj = col0; rsub < rpi && pj < np; pj += cstep) {
+          const double sj = sn[pj], cj = cs[pj];
+          const int r = pp[pj], sc = qq[pj];
+          const bool sok = sc < k;
+          for (int g0 = blockIdx.x; g0 < ngroup; g0 += kU * (int)gridDim.x) {
+            int kind[kU], off[kU][4];
+            double x[kU][4], ci[kU], si[kU];
 #pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int w = w0 + u * gsz32;
-            kind[u] = 0;
-            if (w < nm) {
-              const int pi = w / np, pj = w - (w / np) * np;
-              const int p = pp[pi], q = qq[pi];
-              if (pi == pj) {  // diagonal block: eigenvalue estimates, zero coupling
-                if (q < k) {
-                  if (sn[pi] != 0.0) {
-                    __stcg(M + (size_t)p * k + p, dp[pi]);
-                    __stcg(M + (size_t)q * k + q, dq[pi]);
+            for (int u = 0; u < kU; ++u) {
+              const int g = g0 + u * (int)gridDim.x;
+              const int ri = g * rpi + rsub;
+              kind[u] = 0;
+              if (g >= ngroup || ri >= np + k) continue;
+              if (ri < np) {
+                const int pi = ri;
+                const int p = pp[pi], q = qq[pi];
+                if (pi == pj) {  // diagonal block: eigenvalue estimates, zero coupling
+                  if (q < k) {
+                    if (sn[pi] != 0.0) {
+                      __stcg(M + (size_t)p * k + p, dp[pi]);
+                      __stcg(M + (size_t)q * k + q, dq[pi]);
+                    }
+                    __stcg(M + (size_t)p * k + q, 0.0);
+                    __stcg(M + (size_t)q * k + p, 0.0);
                   }
-                  __stcg(M + (size_t)p * k + q, 0.0);
-                  __stcg(M + (size_t)q * k + p, 0.0);
+                  continue;
                 }
-                continue;
+                si[u] = sn[pi];
+                if (si[u] == 0.0 && sj == 0.0) continue;
+                ci[u] = cs[pi];
+                const bool qok = q < k;
+                kind[u] = 1;
+                off[u][0] = p * k + r;
+                off[u][1] = sok ? p * k + sc : -1;
+                off[u][2] = qok ? q * k + r : -1;
+                off[u][3] = (qok && sok) ? q * k + sc : -1;
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  x[u][e] = off[u][e] >= 0 ? __ldcg(M + off[u][e]) : 0.0;
+              } else {
+                if (sj == 0.0) continue;
+                const int i = ri - np;
+                si[u] = 0.0; ci[u] = 1.0;
+                kind[u] = 2;
+                off[u][0] = i * k + r;
+                off[u][1] = i * k + sc;
+                off[u][2] = off[u][3] = -1;
+                x[u][0] = __ldcg(Vv + off[u][0]);
+                x[u][1] = __ldcg(Vv + off[u][1]);
+                x[u][2] = x[u][3] = 0.0;
               }
-              si[u] = sn[pi]; sj[u] = sn[pj];
-              if (si[u] == 0.0 && sj[u] == 0.0) continue;
-              ci[u] = cs[pi]; cj[u] = cs[pj];
-              const int r = pp[pj], sc = qq[pj];
-              const bool qok = q < k, sok = sc < k;
-              kind[u] = 1;
-              off[u][0] = p * k + r;
-              off[u][1] = sok ? p * k + sc : -1;
-              off[u][2] = qok ? q * k + r : -1;
-              off[u][3] = (qok && sok) ? q * k + sc : -1;
+            }
 #pragma unroll
-              for (int e = 0; e < 4; ++e) x[u][e] = off[u][e] >= 0 ? __ldcg(M + off[u][e]) : 0.0;
-            } else if (w < nitem) {
-              const int v = w - nm;
-              const int i = v / np, pj = v - (v / np) * np;
-              sj[u] = sn[pj];
-              if (sj[u] == 0.0) continue;
-              cj[u] = cs[pj];
-              si[u] = 0.0; ci[u] = 1.0;
-              kind[u] = 2;
-              off[u][0] = i * k + pp[pj];
-              off[u][1] = i * k + qq[pj];
-              off[u][2] = off[u][3] = -1;
-              x[u][0] = __ldcg(Vv + off[u][0]);
-              x[u][1] = __ldcg(Vv + off[u][1]);
-              x[u][2] = x[u][3] = 0.0;
+            for (int u = 0; u < kU; ++u) {
+              if (kind[u] == 0) continue;
+              double b00 = x[u][0], b01 = x[u][1], b10 = x[u][2], b11 = x[u][3];
+              if (sj != 0.0) {  // columns r, s
+                const double t00 = cj * b00 - sj * b01, t01 = sj * b00 + cj * b01;
+                const double t10 = cj * b10 - sj * b11, t11 = sj * b10 + cj * b11;
+                b00 = t00; b01 = t01; b10 = t10; b11 = t11;
+              }
+              if (si[u] != 0.0) {  // rows p, q
+                const double t00 = ci[u] * b00 - si[u] * b10, t10 = si[u] * b00 + ci[u] * b10;
+                const double t01 = ci[u] * b01 - si[u] * b11, t11 = si[u] * b01 + ci[u] * b11;
+                b00 = t00; b01 = t01; b10 = t10; b11 = t11;
+              }
+              double* base = kind[u] == 1 ? M : Vv;
+              __stcg(base + off[u][0], b00);
+              if (off[u][1] >= 0) __stcg(base + off[u][1], b01);
+              if (off[u][2] >= 0) __stcg(base + off[u][2], b10);
+              if (off[u][3] >= 0) __stcg(base + off[u][3], b11);
             }
-          }
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            if (kind[u] == 0) continue;
-            double b00 = x[u][0], b01 = x[u][1], b10 = x[u][2], b11 = x[u][3];
-            if (sj[u] != 0.0) {  // columns r, s
-              const double t00 = cj[u] * b00 - sj[u] * b01, t01 = sj[u] * b00 + cj[u] * b01;
-              const double t10 = cj[u] * b10 - sj[u] * b11, t11 = sj[u] * b10 + cj[u] * b11;
-              b00 = t00; b01 = t01; b10 = t10; b11 = t11;
-            }
-            if (si[u] != 0.0) {  // rows p, q
-              const double t00 = ci[u] * b00 - si[u] * b10, t10 = si[u] * b00 + ci[u] * b10;
-              const double t01 = ci[u] * b01 - si[u] * b11, t11 = si[u] * b01 + ci[u] * b11;
-              b00 = t00; b01 = t01; b10 = t10; b11 = t11;
-            }
-            double* base = kind[u] == 1 ? M : Vv;
-            __stcg(base + off[u][0], b00);
-            if (off[u][1] >= 0) __stcg(base + off[u][1], b01);
-            if (off[u][2] >= 0) __stcg(base + off[u][2], b10);
-            if (off[u][3] >= 0) __stcg(base + off[u][3], b11);
           }
         }
         grid.sync();
