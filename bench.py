@@ -307,6 +307,7 @@ def run_ours(args, cfg):
                           "frac": b_iter(m, n, nnz) * ips / 1e9 / peak}}
     # end-to-end through the public API with host buffers
     x0, y0, s0 = np.zeros(n), np.zeros(m), np.zeros(m)
+    ws.solve(warm_start=(x0, y0, s0))  # untimed warm-up (lazy module loading of the extraction kernels)
     t0 = time.perf_counter()
     sol = ws.solve(warm_start=(x0, y0, s0))
     e2e_s = time.perf_counter() - t0
@@ -419,6 +420,7 @@ def run_sharded(args, cfg, rank, world):
     dom = max(kern, key=lambda k: kern[k]["ms"])
     nnz = cfg["nnz"]
     x0, y0, s0 = np.zeros(n), np.zeros(hi - lo), np.zeros(hi - lo)
+    ws.solve(warm_start=(x0, y0, s0))  # untimed warm-up
     dist.barrier()
     t0 = time.perf_counter()
     sol = ws.solve(warm_start=(x0, y0, s0))

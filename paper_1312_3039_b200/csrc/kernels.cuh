@@ -63,6 +63,7 @@ struct Vec {
   double *P1;                 // compact copy of p = X2[2j] (stride-1 gathers of the later CG A passes)
   double *Axw;                // A cg_warm (m), from the previous EpiAFinal
   double *Aux;                // A u_x (m) for the split residual epilogue
+  double *Agx;                // A g_x (m): residual recurrence on (nullptr: off)
   double *q;                  // A p (m)
   double *zy;                 // z_y = rhs_y + A x (m)
   double *part;               // kMaxRed * kMaxGrid partials
@@ -327,7 +328,17 @@ struct EpiBase {
   const double* xb;  // gather base
   int pend;          // residual check of the previous iteration rides along
   int defer;         // row-sharded: totals go to V.dred for an all-reduce
+  // residual recurrence (first CG pass): +R = run on refresh iterations
+  // (k_sched = 1, 1 + R, ...), -R = run on the others, 0 = always
+  int rgate;
+  int waux;          // refresh pass: always store A u_x into Aux
   static constexpr int MINB = 1;  // min resident CTAs per SM (register cap)
+  __device__ __forceinline__ bool gate_ok() const {
+    if (!rgate) return true;
+    const int R = rgate > 0 ? rgate : -rgate;
+    const bool refresh = (V.ctl->k_sched - 1) % R == 0;
+    return refresh == (rgate > 0);
+  }
   struct Pre {};
   __device__ void pre(long long, Pre&) const {}
   __device__ void extra(double*) const {}
@@ -396,7 +407,8 @@ struct EpiAp : EpiBase {
   __device__ bool load() {
     const Ctl* c = V.ctl;
     pend = MERGED ? c->check_pending : 0;
-    return !c->stop && (!c->cg_done || pend);
+    if (!gate_ok()) return false;
+    return !c->stop && (!c->cg_done || pend || waux);
   }
   struct Pre { double vs, d, b, uy, ut; };
   __device__ void pre(long long i, Pre& p) const {
@@ -409,6 +421,7 @@ struct EpiAp : EpiBase {
   __device__ void row(long long i, const double (&s)[NV], const Pre& p, double* red) const {
     V.q[i] = s[0];
     if constexpr (MERGED) {
+      if (waux) V.Aux[i] = s[1];
       if (pend) {
         const double t = s[1] + p.vs;
         const double di = p.d;
@@ -553,11 +566,12 @@ struct EpiApPlain2 : EpiBase {
   __device__ bool load() {
     const Ctl* c = V.ctl;
     pend = c->check_pending;
-    return !c->stop && (!c->cg_done || pend);
+    if (!gate_ok()) return false;
+    return !c->stop && (!c->cg_done || pend || waux);
   }
   __device__ void row(long long i, const double (&s)[2], const Pre&, double*) const {
     V.q[i] = s[0];
-    if (pend) V.Aux[i] = s[1];
+    if (pend || waux) V.Aux[i] = s[1];
   }
   __device__ void finish(const double*) const {}
 };
@@ -568,7 +582,7 @@ struct EpiResY : EpiBase {
   __device__ bool load() {
     const Ctl* c = V.ctl;
     pend = c->check_pending;
-    return !c->stop && pend;
+    return gate_ok() && !c->stop && pend;
   }
   struct Pre { double vs, d, b, uy, ut; };
   __device__ void pre(long long i, Pre& p) const {

@@ -223,6 +223,13 @@ __global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K, int defer)
     V.X2[2 * j + 1] = t;
     V.v[j] = (vj - ub) + t;
   }
+  // residual recurrence: v_x == 0, so u+_x = al (x - corr g_x) + (1 - al) u_x
+  // and A u+_x = al (A x - corr A g_x) + (1 - al) A u_x (all terms on hand:
+  // A x from the final CG pass, A g_x from setup); refreshed directly every
+  // R iterations by the merged first CG pass
+  if (V.Agx)
+    for (long long i = tid; i < m; i += nt)
+      V.Aux[i] = al * (V.Axw[i] - corr * V.Agx[i]) + (1.0 - al) * V.Aux[i];
   // zero (free in K*) and nonnegative rows
   const long long zl = K.z + K.l;
   for (long long i = tid; i < zl; i += nt) {
@@ -1215,6 +1222,7 @@ struct scs_handle {
   // row-banded CSR(A^T) (setup_bands): S*n rows, raw band partials
   int nband = 1, LAb = 32;
   int recur_refresh = 20;  // opt-in recurrence: direct A x every k iterations
+  int res_rec = 32;        // A u_x of the residual check by recurrence, direct every k (0: always direct)
   // long rows split into pieces (setup_split): [A, A^T]
   bool split_m[2] = {false, false};
   Csr Asp[2] = {};
@@ -2751,20 +2759,40 @@ void check_err(scs_handle* h) {
 // one CG step (A p, A^T, update, p update); the first step of an ADMM
 // iteration also closes the previous iteration's termination check
 void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p, bool merged, bool recur) {
+  // residual recurrence (V.Agx set): the merged pass runs on refresh
+  // iterations only (and stores A u_x); the others check from Aux and run
+  // a plain A p pass
+  const int R = (merged && V.Agx) ? h->res_rec : 0;
   if (merged && !(h->tiled_m[0] || h->stm_m[0])) {  // CSR: plain SpMV + elementwise residual pass
     EpiApPlain2 ea{};
     ea.V = V;
     ea.xb = V.X2;
+    ea.rgate = R;
+    ea.waux = R > 0;
     launch_mat(h, 0, ea);
     EpiResY ry{};
     ry.V = V;
+    ry.rgate = R;
     y_rows(h, V.Aux, ry);
   } else if (merged) {
     EpiAp<true> ea{};
     ea.V = V;
     ea.xb = V.X2;
+    ea.rgate = R;
+    ea.waux = R > 0;
     a_pass(h, ea);
-  } else {
+  }
+  if (merged && R > 0) {
+    EpiResY ry{};
+    ry.V = V;
+    ry.rgate = -R;
+    y_rows(h, V.Aux, ry);
+    EpiAp<false> ea{};
+    ea.V = V;
+    ea.xb = V.P1;
+    ea.rgate = -R;
+    a_pass(h, ea);
+  } else if (!merged) {
     EpiAp<false> ea{};
     ea.V = V;
     ea.xb = V.P1;
@@ -2821,6 +2849,13 @@ void solve_g(scs_handle* h) {
     done_steps += batch;
   }
   a_final(h, G, h->V.gy, 1);
+  if (h->V.Agx) {  // A g_x for the residual recurrence
+    EpiPlain e{};
+    e.V = h->V;
+    e.xb = h->V.gx;
+    e.out = h->V.Agx;
+    launch_mat(h, 0, e);
+  }
   pull_ctl(h);
   check_err(h);
   if (c->denom < 1.0 - 1e-9)
@@ -3133,6 +3168,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     dbg("validated");
     h->set = *S;
     if (const char* e = getenv("SCS_RECUR_REFRESH")) h->recur_refresh = std::max(1, atoi(e));
+    if (const char* e = getenv("SCS_RES_RECUR")) h->res_rec = std::max(0, atoi(e));
     h->dev = S->device;
     CK(cudaSetDevice(h->dev));
     CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev));
@@ -3239,6 +3275,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     V.rhs_y = dalloc<double>(h, m);
     V.Axw = dalloc<double>(h, m);
     V.Aux = dalloc<double>(h, m);
+    V.Agx = h->res_rec > 0 ? dalloc<double>(h, m) : nullptr;
     V.q = dalloc<double>(h, m);
     V.zy = dalloc<double>(h, m);
     V.Dinv = dalloc<double>(h, m);
