@@ -9,7 +9,9 @@
 //   SpMV A^T  [EpiAtFirst]  cg_rhs = rhs_x - A^T rhs_y, r0 = cg_rhs - G x0   embedding.py:109, sparse_linalg.py:461-469
 //                           (+ A^T u_y of the previous iterate, see below)
 //   cg_max x { SpMV A [EpiAp]; SpMV A^T [EpiAtGp]; k_cg_update; k_cg_p }    sparse_linalg.py:470-485
-//                           (the first A pass also carries A u_x, below)
+//                           (the first A pass also carries A u_x, below --
+//                           every R-th iteration; the others carry A u_x by
+//                           recurrence in k_cone_tail, SCS_RES_RECUR)
 //   SpMV A    [EpiAFinal]   z_y = rhs_y + A x, corr = h'p / denom          embedding.py:113, 192
 //   k_cone_tail    u~, relaxation, cone projection (elementwise / SOC / exp),
 //                  tau update                                               embedding.py:193-196, solver.py:163-165
