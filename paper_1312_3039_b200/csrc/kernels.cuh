@@ -66,6 +66,13 @@ struct Vec {
   double *Axw;                // A cg_warm (m), from the previous EpiAFinal
   double *Aux;                // A u_x (m) for the split residual epilogue
   double *Agx;                // A g_x (m): residual recurrence on (nullptr: off)
+  // A^T side of the residual recurrence (n each; T == nullptr: off):
+  double *T;                  // A^T A x of the CG iterate (carried through the Gp products)
+  double *Sv;                 // A^T rhs_y of this iteration
+  double *Uy;                 // A^T u_y of the current state
+  double *Dd;                 // A^T (v_y - u_y) of the current state
+  double *Atb, *Atgy;         // A^T b^, A^T g_y (setup)
+  double *Yc;                 // compact rhs_y + A cg_warm (m), gather of the NV = 1 first pass
   double *q;                  // A p (m)
   double *zy;                 // z_y = rhs_y + A x (m)
   double *part;               // kMaxRed * kMaxGrid partials
@@ -356,7 +363,7 @@ struct EpiAtFirst : EpiBase {
   static constexpr int NV = 2, STRIDE = 2, NR = 5;
   __device__ bool load() {
     pend = V.ctl->check_pending;
-    return !V.ctl->stop;
+    return gate_ok() && !V.ctl->stop;
   }
   struct Pre { double rx, x, mi, ei, c, ux, ut; };
   __device__ void pre(long long j, Pre& p) const {
@@ -385,6 +392,12 @@ struct EpiAtFirst : EpiBase {
       red[2] += inf * inf;
       red[3] += p.c * p.ux;
     }
+    if (rgate > 0) {  // refresh of the A^T-side recurrence (T just computed directly)
+      const double sv = s[0] - V.T[j];
+      V.Sv[j] = sv;
+      V.Uy[j] = s[1];
+      V.Dd[j] = (sv + (V.u[V.n + V.m] + V.v[V.n + V.m]) * V.Atb[j]) - 2.0 * s[1];
+    }
   }
   __device__ void finish(const double* tot) const {
     if (threadIdx.x) return;
@@ -397,6 +410,73 @@ struct EpiAtFirst : EpiBase {
     c->cg_done = 0;
     c->rs = V.Minv ? tot[4] : res * res;
   }
+};
+
+// First A^T pass with the A^T-side residual recurrence (non-refresh
+// iterations): one product F = A^T (rhs_y + A x0) from the compact gather Yc.
+// With T = A^T A x0 carried by the CG updates, A^T rhs_y = F - T, and since
+// rhs_y = u_y + v_y - w_tau b^ (embedding.py:177-178),
+//   A^T u_y = ((F - T) + w_tau A^T b^ - Dd) / 2,   Dd = A^T (v_y - u_y)
+// (Dd from k_cone_tail: v+ - u+ = v - u_bar, solver.py:165).
+struct EpiAtFirst1 : EpiBase {
+  static constexpr int NV = 1, STRIDE = 1, NR = 5;
+  __device__ bool load() {
+    pend = V.ctl->check_pending;
+    return gate_ok() && !V.ctl->stop;
+  }
+  struct Pre { double rx, x, mi, ei, c, ux, ut, wt; };
+  __device__ void pre(long long j, Pre& p) const {
+    p.rx = V.rhs_x[j];
+    p.x = V.x[j];
+    if (V.Minv) p.mi = V.Minv[j];
+    p.ut = utau();
+    p.wt = p.ut + V.v[V.n + V.m];
+    if (pend) { p.ei = V.Einv[j]; p.c = V.c[j]; p.ux = V.X2[2 * j + 1]; }
+  }
+  __device__ void row(long long j, const double (&s)[1], const Pre& p, double* red) const {
+    const double r = (p.rx - p.x) - s[0];
+    V.r[j] = r;
+    red[0] += r * r;
+    if (V.Minv) {
+      const double z = p.mi * r;
+      V.X2[2 * j] = z;
+      V.P1[j] = z;
+      red[4] += r * z;
+    } else {
+      V.X2[2 * j] = r;
+      V.P1[j] = r;
+    }
+    const double sv = s[0] - V.T[j];
+    const double uy = 0.5 * ((sv + p.wt * V.Atb[j]) - V.Dd[j]);
+    V.Sv[j] = sv;
+    V.Uy[j] = uy;
+    if (pend) {
+      const double du = p.ei * (uy / p.ut + p.c);
+      const double inf = p.ei * uy;
+      red[1] += du * du;
+      red[2] += inf * inf;
+      red[3] += p.c * p.ux;
+    }
+  }
+  __device__ void finish(const double* tot) const {
+    if (threadIdx.x) return;
+    Ctl* c = V.ctl;
+    if (pend) { c->sums[3] = tot[1]; c->sums[4] = tot[2]; c->sums[5] = tot[3]; }
+    const double res = sqrt(tot[0]);
+    c->cg_it = 0;
+    if (!isfinite(res)) { c->err |= ERR_CG_NONFINITE; c->stop = 1; c->cg_done = 1; return; }
+    if (res <= c->tol) { c->cg_done = 1; return; }
+    c->cg_done = 0;
+    c->rs = V.Minv ? tot[4] : res * res;
+  }
+};
+
+// Refresh of T = A^T (A x0) (A x0 = Axw, stored by the previous final pass).
+struct EpiTRef : EpiBase {
+  static constexpr int NV = 1, STRIDE = 1, NR = 0;
+  __device__ bool load() { return gate_ok() && !V.ctl->stop; }
+  __device__ void row(long long j, const double (&s)[1], const Pre&, double*) const { V.T[j] = s[0]; }
+  __device__ void finish(const double*) const {}
 };
 
 // q = A p.  MERGED: the first CG pass also carries A u_x of the previous

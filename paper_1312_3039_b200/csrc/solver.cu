@@ -67,7 +67,9 @@ __global__ void __launch_bounds__(kBlock) k_prep(Vec V, int defer) {
     } else {
       r = w - wt * V.b[i - n];
       V.rhs_y[i - n] = r;
-      V.Y2[2 * (i - n)] = r + V.Axw[i - n];
+      const double yv = r + V.Axw[i - n];
+      V.Y2[2 * (i - n)] = yv;
+      if (V.Yc) V.Yc[i - n] = yv;
       red[0] += r * r;
     }
   }
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(Vec V, long long cap, int 
   const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
   const long long nt = (long long)gridDim.x * kBlock;
   for (long long j = tid; j < V.n; j += nt) {
+    if (V.T) V.T[j] += a * (V.Gp[j] - V.X2[2 * j]);  // A^T A x += alpha A^T A p
     V.x[j] += a * V.X2[2 * j];
     const double r = V.r[j] - a * V.Gp[j];
     V.r[j] = r;
@@ -222,6 +225,11 @@ __global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K, int defer)
     V.u[j] = t;
     V.X2[2 * j + 1] = t;
     V.v[j] = (vj - ub) + t;
+    if (V.T) {  // A^T (v+_y - u+_y) = A^T v_y - A^T u_bar_y, u~_y = z_y - corr g_y
+      const double aut = (V.Sv[j] + V.T[j]) - corr * V.Atgy[j];
+      const double uyj = V.Uy[j];
+      V.Dd[j] = (V.Dd[j] + uyj) - (al * aut + (1.0 - al) * uyj);
+    }
   }
   // residual recurrence: v_x == 0, so u+_x = al (x - corr g_x) + (1 - al) u_x
   // and A u+_x = al (A x - corr A g_x) + (1 - al) A u_x (all terms on hand:
@@ -1223,6 +1231,7 @@ struct scs_handle {
   int nband = 1, LAb = 32;
   int recur_refresh = 20;  // opt-in recurrence: direct A x every k iterations
   int res_rec = 32;        // A u_x of the residual check by recurrence, direct every k (0: always direct)
+  bool res_rec_at = true;  // ... and A^T u_y (SCS_RES_RECUR_AT=0: only A u_x)
   // long rows split into pieces (setup_split): [A, A^T]
   bool split_m[2] = {false, false};
   Csr Asp[2] = {};
@@ -2815,6 +2824,7 @@ void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p, bool merge
 void solve_g(scs_handle* h) {
   const long long n = h->n, m = h->m;
   Vec G = h->V;
+  G.T = nullptr;  // the g solve's CG must not touch the iteration's A^T A x
   G.rhs_x = h->ch;
   G.x = h->V.gx;
   G.rhs_y = h->bh;
@@ -2856,6 +2866,16 @@ void solve_g(scs_handle* h) {
     e.out = h->V.Agx;
     launch_mat(h, 0, e);
   }
+  if (h->V.T) {  // A^T b^ and A^T g_y for the A^T-side recurrence
+    EpiPlain e{};
+    e.V = h->V;
+    e.xb = h->bh;
+    e.out = h->V.Atb;
+    at_pass(h, e);
+    e.xb = h->V.gy;
+    e.out = h->V.Atgy;
+    at_pass(h, e);
+  }
   pull_ctl(h);
   check_err(h);
   if (c->denom < 1.0 - 1e-9)
@@ -2875,10 +2895,26 @@ void enqueue_iteration(scs_handle* h) {
     k_prep_finish<<<1, 32, 0, h->st>>>(V);
     h->launches++;
   }
+  const int RA = V.T ? h->res_rec : 0;  // A^T-side residual recurrence
+  if (RA) {
+    EpiTRef et{};
+    et.V = V;
+    et.xb = V.Axw;
+    et.rgate = RA;
+    at_pass(h, et);
+  }
   EpiAtFirst e0{};
   e0.V = V;
   e0.xb = V.Y2;
+  e0.rgate = RA;
   at_pass(h, e0);
+  if (RA) {
+    EpiAtFirst1 e1{};
+    e1.V = V;
+    e1.xb = V.Yc;
+    e1.rgate = -RA;
+    at_pass(h, e1);
+  }
   const long long cgm = h->set.cg_max;
   const bool recur = (h->set.fast & SCS_FAST_RECURRENCE) != 0;
   for (long long i = 0; i < cgm; ++i) cg_step(h, V, cgm, i + 1 < cgm, i == 0, recur);
@@ -3169,6 +3205,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     h->set = *S;
     if (const char* e = getenv("SCS_RECUR_REFRESH")) h->recur_refresh = std::max(1, atoi(e));
     if (const char* e = getenv("SCS_RES_RECUR")) h->res_rec = std::max(0, atoi(e));
+    if (const char* e = getenv("SCS_RES_RECUR_AT")) h->res_rec_at = atoi(e) != 0;
     h->dev = S->device;
     CK(cudaSetDevice(h->dev));
     CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev));
@@ -3276,6 +3313,15 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     V.Axw = dalloc<double>(h, m);
     V.Aux = dalloc<double>(h, m);
     V.Agx = h->res_rec > 0 ? dalloc<double>(h, m) : nullptr;
+    if (h->res_rec > 0 && h->res_rec_at) {
+      V.T = dalloc<double>(h, n);
+      V.Sv = dalloc<double>(h, n);
+      V.Uy = dalloc<double>(h, n);
+      V.Dd = dalloc<double>(h, n);
+      V.Atb = dalloc<double>(h, n);
+      V.Atgy = dalloc<double>(h, n);
+      V.Yc = dalloc<double>(h, m);
+    }
     V.q = dalloc<double>(h, m);
     V.zy = dalloc<double>(h, m);
     V.Dinv = dalloc<double>(h, m);

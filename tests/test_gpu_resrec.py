@@ -1,4 +1,5 @@
-"""GPU tests of the residual recurrence (SCS_RES_RECUR, default R = 32).
+"""GPU tests of the residual recurrence (SCS_RES_RECUR, default R = 32;
+SCS_RES_RECUR_AT=0 keeps A^T u_y direct).
 
 The termination check needs A u_x of the previous iterate (scaling.py:466).
 Because v_x is exactly 0 after every iteration (the x-part cone is free),
@@ -8,6 +9,12 @@ computes it directly only every R iterations, in the merged first CG pass;
 the other iterations run that pass on p alone (NV = 1).  The iterates never
 read A u_x, so they must be bit-identical to the direct mode (R = 0); only
 the residual values move, at rounding level.
+
+A^T side (SCS_RES_RECUR_AT, default on): A^T A x is carried through the CG
+Gp products (refreshed directly every R iterations), A^T rhs_y = F - A^T A x0
+from the first pass's single product F, and A^T (v_y - u_y) follows
+v+ - u+ = v - u_bar; A^T u_y = (A^T (u_y + v_y) - A^T (v_y - u_y)) / 2, so
+the first A^T pass also runs with NV = 1.
 """
 
 import numpy as np
@@ -52,13 +59,15 @@ def _close(a, b, tol):
     return abs(a - b) <= tol * max(abs(a), abs(b), 1e-300)
 
 
+@pytest.mark.parametrize("at", ["0", "1"])
 @pytest.mark.parametrize("path", ["csr", "stream"])
 @pytest.mark.parametrize("rec", [1, 3, 32])
 @pytest.mark.parametrize("name", NAMES)
-def test_recurrence_matches_direct(monkeypatch, name, rec, path):
+def test_recurrence_matches_direct(monkeypatch, name, rec, path, at):
     d = load(name)
     data, settings = fixture_data(d)
     env = [("SCS_STREAM", "1"), ("SCS_STREAM_W", "256")] if path == "stream" else []
+    env.append(("SCS_RES_RECUR_AT", at))
     ref, tref = run(monkeypatch, data, settings, 0, env)
     got, tgot = run(monkeypatch, data, settings, rec, env)
     assert got.status == ref.status and got.info.iterations == ref.info.iterations
