@@ -7,7 +7,9 @@
 //
 //   k_prep         w = u+v, rhs = w[:-1] - w_tau h, ||rhs|| -> CG tol       embedding.py:177-185
 //   SpMV A^T  [EpiAtFirst]  cg_rhs = rhs_x - A^T rhs_y, r0 = cg_rhs - G x0   embedding.py:109, sparse_linalg.py:461-469
-//                           (+ A^T u_y of the previous iterate, see below)
+//                           (+ A^T u_y of the previous iterate, see below --
+//                           every R-th iteration; the others run EpiAtFirst1,
+//                           NV = 1, with A^T u_y from recurrences)
 //   cg_max x { SpMV A [EpiAp]; SpMV A^T [EpiAtGp]; k_cg_update; k_cg_p }    sparse_linalg.py:470-485
 //                           (the first A pass also carries A u_x, below --
 //                           every R-th iteration; the others carry A u_x by
