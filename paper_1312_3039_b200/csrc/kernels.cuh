@@ -473,6 +473,16 @@ struct EpiAtFirst1 : EpiBase {
   }
 };
 
+// EpiAtFirst1, split (one GPU, no bands): the pass only stores F into Sv,
+// then k_rows runs EpiAtFirst1 over it (a heavy per-row epilogue inside the
+// streamed kernel cost ~0.55 ms at config 5; coalesced, it is ~20 us).
+struct EpiStoreF : EpiBase {
+  static constexpr int NV = 1, STRIDE = 1, NR = 0;
+  __device__ bool load() { return gate_ok() && !V.ctl->stop; }
+  __device__ void row(long long j, const double (&s)[1], const Pre&, double*) const { V.Sv[j] = s[0]; }
+  __device__ void finish(const double*) const {}
+};
+
 // Refresh of T = A^T (A x0) (A x0 = Axw, stored by the previous final pass).
 struct EpiTRef : EpiBase {
   static constexpr int NV = 1, STRIDE = 1, NR = 0;

@@ -2913,7 +2913,17 @@ void enqueue_iteration(scs_handle* h) {
     e1.V = V;
     e1.xb = V.Yc;
     e1.rgate = -RA;
-    at_pass(h, e1);
+    if (!h->sharded && h->nband <= 1) {  // products into Sv, then the epilogue coalesced
+      EpiStoreF sf{};
+      sf.V = V;
+      sf.xb = V.Yc;
+      sf.rgate = -RA;
+      launch_mat(h, 1, sf);
+      k_rows<EpiAtFirst1><<<elem_grid(h, h->n), kBlock, 0, h->st>>>(V.Sv, h->n, 1, e1);
+      h->launches++;
+    } else {
+      at_pass(h, e1);
+    }
   }
   const long long cgm = h->set.cg_max;
   const bool recur = (h->set.fast & SCS_FAST_RECURRENCE) != 0;

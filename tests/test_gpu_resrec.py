@@ -72,19 +72,25 @@ def test_recurrence_matches_direct(monkeypatch, name, rec, path, at):
     got, tgot = run(monkeypatch, data, settings, rec, env)
     assert got.status == ref.status and got.info.iterations == ref.info.iterations
     assert len(tgot) == len(tref)
-    # the iterates do not read A u_x: bit-identical on the CSR path; on the
-    # streamed path the plain A p pass (NV = 1) runs on another tile
-    # schedule than the merged NV = 2 pass (other split sums), a
-    # reduction-order change: first 50 iterates to 1e-12
+    # the iterates do not read A u_x: bit-identical on the CSR path with the
+    # A side alone; on the streamed path the plain A p pass (NV = 1) runs on
+    # another tile schedule than the merged NV = 2 pass (other split sums),
+    # and with the A^T side the first pass's epilogue (and its ||r0||^2 sum)
+    # runs in k_rows on another grid -- reduction-order changes: first 50
+    # iterates to 1e-12
     for k, ((u0, v0), (u1, v1)) in enumerate(zip(tref, tgot)):
-        if path == "csr":
+        if path == "csr" and at == "0":
             assert np.array_equal(u0, u1) and np.array_equal(v0, v1), k
         elif k < 50:
             assert rel(u1, u0) < 1e-12 and rel(v1, v0) < 1e-12, (k, rel(u1, u0))
+    # residuals at the same final iterate (bit-identical runs): rounding level;
+    # after a reduction-order change the final iterates themselves differ by
+    # the trajectory's own drift (~1e-9 after thousands of iterations)
+    tol = 1e-9 if (path == "csr" and at == "0") else 1e-6
     for key in ("pri_res", "dual_res", "gap"):
-        assert _close(getattr(got.info, key), getattr(ref.info, key), 1e-9), key
+        assert _close(getattr(got.info, key), getattr(ref.info, key), tol), key
     for key in ("unbdd_measure", "infeas_measure"):
-        assert _close(getattr(got.info.residuals, key), getattr(ref.info.residuals, key), 1e-9), key
+        assert _close(getattr(got.info.residuals, key), getattr(ref.info.residuals, key), tol), key
     assert got.status.value == d["status"]
 
 
@@ -97,11 +103,17 @@ def test_recurrence_lasso_long_run(monkeypatch):
                          P.ConeSpec.from_any(cone))
     st = P.Settings(max_iters=600, eps_pri=1e-9, eps_dual=1e-9, eps_gap=1e-9)
     ref, _ = run(monkeypatch, data, st, 0)
-    got, _ = run(monkeypatch, data, st, 1000)
+    got, _ = run(monkeypatch, data, st, 1000, [("SCS_RES_RECUR_AT", "0")])
     assert got.info.iterations == ref.info.iterations and got.status == ref.status
     assert np.array_equal(got.x, ref.x)
     for key in ("pri_res", "dual_res", "gap"):
         assert _close(getattr(got.info, key), getattr(ref.info, key), 1e-8), key
+    # both sides: the A^T side's split epilogue changes the ||r0||^2 sum order
+    got, _ = run(monkeypatch, data, st, 1000, [("SCS_RES_RECUR_AT", "1")])
+    assert got.info.iterations == ref.info.iterations and got.status == ref.status
+    assert rel(got.x, ref.x) < 1e-8
+    for key in ("pri_res", "dual_res", "gap"):
+        assert _close(getattr(got.info, key), getattr(ref.info, key), 1e-6), key
 
 
 @pytest.mark.parametrize("world", [2, 3])
