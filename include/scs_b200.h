@@ -230,6 +230,21 @@ int scs_bench_iters(scs_handle* h, int64_t k, double* ms);
 int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms_per_launch,
                      double* bytes_per_launch);
 
+/* Introspection of the device layout chosen at setup (no reference
+ * counterpart; tests use it to assert which SpMV format ran):
+ *   SCS_Q_FORMAT_A / SCS_Q_FORMAT_AT: 0 CSR kernel, 1 TMA-streamed tiles;
+ *   SCS_Q_LAUNCHES_PER_ITER: kernel launches of one captured iteration;
+ *   SCS_Q_STREAM_BYTES_A / _AT: bytes of the streamed format (0 if CSR);
+ *   SCS_Q_CG_ITERS_TOTAL: EmbeddingCache.cg_iters_total (embedding.py:43,
+ *   112): CG iterations of the setup solve of g plus every solve since. */
+#define SCS_Q_FORMAT_A 0
+#define SCS_Q_FORMAT_AT 1
+#define SCS_Q_LAUNCHES_PER_ITER 2
+#define SCS_Q_STREAM_BYTES_A 3
+#define SCS_Q_STREAM_BYTES_AT 4
+#define SCS_Q_CG_ITERS_TOTAL 5
+int scs_query(scs_handle* h, int32_t key, int64_t* out);
+
 void scs_destroy(scs_handle* h);
 const char* scs_last_error(const scs_handle* h);
 int scs_abi_version(void);

@@ -345,6 +345,13 @@ def _raise(exc: native.NativeError, setup=False):
     raise RuntimeError(exc.msg) from None
 
 
+class _CacheView:
+    """The one EmbeddingCache field a caller reads (embedding.py:43)."""
+
+    def __init__(self, cg_iters_total):
+        self.cg_iters_total = cg_iters_total
+
+
 class Workspace:
     """Reusable device-resident solver handle (solver.py:291-378).
 
@@ -371,6 +378,11 @@ class Workspace:
         self._h = None
         t0 = time.perf_counter()
         self._create()
+        # mirror of EmbeddingCache.cg_iters_total (embedding.py:43,112): the
+        # setup solve of g, then every solve's CG iterations; updated after
+        # every step, so an on_iteration callback reads it like the reference's
+        # ws.cache.cg_iters_total
+        self.cache = _CacheView(native.query(self._h, native.Q_CG_ITERS_TOTAL))
         self.setup_time = time.perf_counter() - t0
         self.last_setup_time = self.setup_time
         self._final = None
@@ -497,6 +509,7 @@ class Workspace:
                 self.data.c = nc
         self._scal = None
         self._call(self._lib.scs_update_vectors(self._h, native.ptr(nb), native.ptr(nc)))
+        self.cache.cg_iters_total = native.query(self._h, native.Q_CG_ITERS_TOTAL)
         self.last_setup_time = time.perf_counter() - t0
         return self.last_setup_time
 
@@ -524,6 +537,7 @@ class Workspace:
             while True:
                 prev = int(info.iterations)
                 self._call(self._lib.scs_step(self._h, 1, native.C.byref(info)))
+                self.cache.cg_iters_total = int(info.cg_iters)
                 if info.iterations > prev:
                     u, v = self.state()
                     on_iteration(SolverState(u=u, v=v, iter=int(info.iterations)))
@@ -531,6 +545,7 @@ class Workspace:
                         info.iterations == prev:
                     break
             self._call(self._lib.scs_finish(self._h, native.C.byref(info)))
+        self.cache.cg_iters_total = int(info.cg_iters)
         status = _STATUS_BY_CODE[int(info.status)]
         res = Residuals(*[float(x) for x in info.res])
         self._final = None

@@ -60,7 +60,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             cmd += ["-Xptxas", "-v"] if verbose else []
             cmd += [f for f in nccl if f.startswith("-D")]
         else:
-            cmd += ["-Xcompiler", "-pthread"]
+            cmd += ["-Xcompiler", "-pthread", "-Xcompiler", "-ffp-contract=off"]
         _run(cmd, verbose)
         objs.append(obj)
     link = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs,

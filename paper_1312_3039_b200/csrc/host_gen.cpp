@@ -5,7 +5,10 @@
 //     pure-Python generator cannot reach these sizes);
 //   * scs_partition_rows: contiguous row shards for multi-GPU runs.
 // Both are deterministic functions of their arguments, independent of the
-// thread count (counter-based random streams per column / per row).
+// thread count (counter-based random streams per column / per row), and the
+// generator is reproduced bit for bit by the pure-numpy
+// generators.gen_lasso_hashed.  Compiled with -ffp-contract=off: every
+// floating-point operation is a separately rounded IEEE +, * or sqrt.
 #include <stdint.h>
 
 #include <algorithm>
@@ -19,45 +22,35 @@
 
 namespace {
 
-inline uint64_t splitmix(uint64_t& s) {
-  uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+// Counter-based streams: every random number is fmix64 of (stream base +
+// counter), so the whole instance is a pure function of (seed, p, q, nnz_f)
+// that numpy reproduces bit for bit (generators.gen_lasso_hashed: uint64
+// wrap-around arithmetic, IEEE +,* only -- no libm -- so the CPU reference
+// arm builds the same instance without this library).
+inline uint64_t fmix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
-
-// xoshiro256** seeded by splitmix64 (the family of reference rng.py:16-50;
-// not bit-compatible with it, which the reference does not promise either)
-struct Rng {
-  uint64_t s[4];
-  bool has_spare = false;
-  double spare = 0.0;
-  explicit Rng(uint64_t seed) {
-    for (auto& w : s) w = splitmix(seed);
-  }
-  static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
-  uint64_t next() {
-    const uint64_t r = rotl(s[1] * 5, 7) * 9, t = s[1] << 17;
-    s[2] ^= s[0]; s[3] ^= s[1]; s[1] ^= s[2]; s[0] ^= s[3]; s[2] ^= t; s[3] = rotl(s[3], 45);
-    return r;
-  }
-  double uniform() { return (next() >> 11) * 0x1.0p-53; }
-  double normal() {  // Box-Muller (rng.py:59-70)
-    if (has_spare) { has_spare = false; return spare; }
-    const double u1 = 1.0 - uniform(), u2 = uniform();
-    const double r = std::sqrt(-2.0 * std::log(u1)), th = 6.283185307179586 * u2;
-    spare = r * std::sin(th);
-    has_spare = true;
-    return r * std::cos(th);
-  }
-  uint64_t below(uint64_t n) {  // unbiased (rng.py:75-83)
-    const uint64_t lim = UINT64_MAX - (UINT64_MAX % n);
-    for (;;) {
-      const uint64_t u = next();
-      if (u < lim) return u % n;
-    }
-  }
-};
+constexpr uint64_t kGold = 0x9E3779B97F4A7C15ull;
+// stream base of object `j` in domain `dom` (0: F column rows, 1: F column
+// values, 2: planted support keys, 3: planted values, 4: noise)
+inline uint64_t base_of(uint64_t seed, uint64_t dom, uint64_t j) {
+  return fmix64(seed * 0xD1B54A32D192ED03ull + dom * 0xA24BAED4963EE407ull + (j + 1) * kGold);
+}
+inline uint64_t draw(uint64_t base, uint64_t ctr) { return fmix64(base + (ctr + 1) * kGold); }
+// Approximately N(0,1): Irwin-Hall sum of four 32-bit uniforms from two
+// draws, centred and scaled to unit variance (exact IEEE operations in a
+// fixed order).
+inline double normal4(uint64_t base, uint64_t i) {
+  const uint64_t a = draw(base, 2 * i), b = draw(base, 2 * i + 1);
+  const double u1 = (double)(a >> 32) * 0x1p-32, u2 = (double)(a & 0xffffffffull) * 0x1p-32;
+  const double u3 = (double)(b >> 32) * 0x1p-32, u4 = (double)(b & 0xffffffffull) * 0x1p-32;
+  double s = u1 + u2;
+  s = s + u3;
+  s = s + u4;
+  return (s - 2.0) * 1.7320508075688772;
+}
 
 template <class F>
 void parallel_for(int64_t n, int threads, F&& fn) {
@@ -79,28 +72,36 @@ void parallel_for(int64_t n, int threads, F&& fn) {
   for (auto& th : pool) th.join();
 }
 
-// Column j of F: k sorted distinct rows of [0, q) with N(0,1) values.
+// Column j of F: k sorted distinct rows of [0, q) with values normal4.
+// Sparse columns (2k <= q): row_i = draw(i) mod q, sorted; every row equal
+// to its predecessor is redrawn from counter (round << 32 | position) and
+// the column re-sorted, until no duplicate is left.  Dense columns: the k
+// rows with the smallest (key, row), key = draw(2^40 + row).
 void f_column(uint64_t seed, int64_t j, int64_t k, int64_t q, std::vector<int64_t>& rows,
               std::vector<double>& vals) {
-  Rng rng(seed ^ (0xA24BAED4963EE407ull * (uint64_t)(j + 1)));
+  const uint64_t br = base_of(seed, 0, (uint64_t)j), bv = base_of(seed, 1, (uint64_t)j);
   rows.resize(k);
-  if (2 * k > q) {  // selection sampling (Knuth S)
-    int64_t need = k, t = 0;
-    for (int64_t r = 0; r < q && need; ++r)
-      if ((double)(q - r) * rng.uniform() < (double)need) { rows[t++] = r; --need; }
-  } else {
-    for (int64_t i = 0; i < k; ++i) rows[i] = (int64_t)rng.below(q);
+  if (2 * k > q) {
+    std::vector<std::pair<uint64_t, int64_t>> key(q);
+    for (int64_t r = 0; r < q; ++r) key[r] = {draw(br, (1ull << 40) + (uint64_t)r), r};
+    std::partial_sort(key.begin(), key.begin() + k, key.end());
+    for (int64_t i = 0; i < k; ++i) rows[i] = key[i].second;
     std::sort(rows.begin(), rows.end());
-    for (int round = 0; round < 64; ++round) {
-      int64_t dup = 0;
+  } else {
+    for (int64_t i = 0; i < k; ++i) rows[i] = (int64_t)(draw(br, (uint64_t)i) % (uint64_t)q);
+    std::sort(rows.begin(), rows.end());
+    std::vector<int64_t> dup;
+    for (uint64_t round = 1;; ++round) {
+      dup.clear();  // positions equal to their predecessor, all found before any redraw
       for (int64_t i = 1; i < k; ++i)
-        if (rows[i] == rows[i - 1]) { rows[i] = (int64_t)rng.below(q); ++dup; }
-      if (!dup) break;
+        if (rows[i] == rows[i - 1]) dup.push_back(i);
+      if (dup.empty()) break;
+      for (int64_t i : dup) rows[i] = (int64_t)(draw(br, (round << 32) | (uint64_t)i) % (uint64_t)q);
       std::sort(rows.begin(), rows.end());
     }
   }
   vals.resize(k);
-  for (int64_t i = 0; i < k; ++i) vals[i] = rng.normal();
+  for (int64_t i = 0; i < k; ++i) vals[i] = normal4(bv, (uint64_t)i);
 }
 
 }  // namespace
@@ -142,17 +143,21 @@ extern "C" int scs_gen_lasso(int64_t p, int64_t q, int64_t nnz_f, uint64_t seed,
   if (!colptr) return SCS_OK;
   colptr[0] = 0;
   for (int64_t j = 0; j < n; ++j) colptr[j + 1] = colptr[j] + cnt[j];
-  // planted coefficients (generators.py:72-75): p/10 support, N(0,1)
-  Rng grng(seed * 0x9E3779B97F4A7C15ull + 17);
+  // planted coefficients (generators.py:72-75): p/10 support (the columns
+  // with the smallest (key, column)), values normal4
   const int64_t ks = std::max<int64_t>(1, p / 10);
-  std::vector<int64_t> pool(p);
-  for (int64_t i = 0; i < p; ++i) pool[i] = i;
-  for (int64_t i = 0; i < ks; ++i) std::swap(pool[i], pool[i + (int64_t)grng.below(p - i)]);
-  std::vector<int64_t> support(pool.begin(), pool.begin() + ks);
-  std::sort(support.begin(), support.end());
+  std::vector<int64_t> support(ks);
   std::vector<double> zhat(ks);
-  for (int64_t i = 0; i < ks; ++i) zhat[i] = grng.normal();
-  std::vector<int64_t>().swap(pool);
+  {
+    std::vector<std::pair<uint64_t, int64_t>> key(p);
+    const uint64_t bk = base_of(seed, 2, 0);
+    for (int64_t j = 0; j < p; ++j) key[j] = {draw(bk, (uint64_t)j), j};
+    std::partial_sort(key.begin(), key.begin() + ks, key.end());
+    for (int64_t i = 0; i < ks; ++i) support[i] = key[i].second;
+    std::sort(support.begin(), support.end());
+    const uint64_t bz = base_of(seed, 3, 0);
+    for (int64_t i = 0; i < ks; ++i) zhat[i] = normal4(bz, (uint64_t)i);
+  }
   // g = F zhat + sqrt(0.1) noise (generators.py:76-77); deterministic by
   // accumulating each row block over the support columns in order
   std::vector<double> g(q, 0.0);
@@ -171,10 +176,8 @@ extern "C" int scs_gen_lasso(int64_t p, int64_t q, int64_t nnz_f, uint64_t seed,
         for (int64_t e = it - R.begin(); e < (int64_t)R.size() && R[e] < hi; ++e)
           g[R[e]] += svals[i][e] * zhat[i];
       }
-      for (int64_t r = lo; r < hi; ++r) {
-        Rng nr(seed ^ (0xD1B54A32D192ED03ull * (uint64_t)(r + 1)));
-        g[r] += nr.normal() * std::sqrt(0.1);
-      }
+      const uint64_t bn = base_of(seed, 4, 0);
+      for (int64_t r = lo; r < hi; ++r) g[r] += normal4(bn, (uint64_t)r) * std::sqrt(0.1);
     });
   }
   // mu = 0.1 ||F^T g||_inf (generators.py:78-79)

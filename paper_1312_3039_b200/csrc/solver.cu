@@ -1227,6 +1227,7 @@ struct scs_handle {
     long long ncmd = 0;
   } ssch[2][2];
   double* Pstm = nullptr;
+  unsigned long long stm_bytes[2] = {0, 0};
   // row-banded CSR(A^T) (setup_bands): S*n rows, raw band partials
   int nband = 1, LAb = 32;
   int recur_refresh = 20;  // opt-in recurrence: direct A x every k iterations
@@ -2035,6 +2036,7 @@ void build_stream(scs_handle* h, int mat) {
                   (void*)sec, (void*)slot, (void*)perm, (void*)rowid, (void*)hown})
     dfree(h, p);
   F.blob = blob;
+  h->stm_bytes[mat] = bytes;
   long long ncsr = 0;
   for (long long sb = 0; sb < F.NB; ++sb) ncsr += !T.tiled[sb];
   dbg("stream layout mat=%d rows=%lld cols=%lld nnz=%lld W=%d S=%d NB=%d csr_sb=%lld pieces=%lld "
@@ -3708,6 +3710,23 @@ int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms, double* 
     *h->ctl_h = saved;
     push_ctl(h);
   });
+}
+
+int scs_query(scs_handle* h, int32_t key, int64_t* out) {
+  if (!h || !out) return SCS_EINVAL;
+  switch (key) {
+    case SCS_Q_FORMAT_A: *out = h->stm_m[0] ? 1 : 0; return SCS_OK;
+    case SCS_Q_FORMAT_AT: *out = h->stm_m[1] ? 1 : 0; return SCS_OK;
+    case SCS_Q_LAUNCHES_PER_ITER: *out = h->launches_per_iter; return SCS_OK;
+    case SCS_Q_STREAM_BYTES_A: *out = (int64_t)h->stm_bytes[0]; return SCS_OK;
+    case SCS_Q_STREAM_BYTES_AT: *out = (int64_t)h->stm_bytes[1]; return SCS_OK;
+    case SCS_Q_CG_ITERS_TOTAL:
+      return guard(h, [&] {
+        pull_ctl(h);
+        *out = h->ctl_h->cg_iters_total;
+      });
+    default: return SCS_EINVAL;
+  }
 }
 
 int scs_allreduce(scs_handle* h, double* vals, int64_t n) {

@@ -11,7 +11,9 @@ rows strictly increasing per column) and ``cone`` a dict
 ``{"z","l","q","s","ep"}`` (fileio.py:68-73 plus the exp-cone count).
 
 Huge LASSO instances (1e8-1e9 nnz) come from the multithreaded C generator
-``scs_gen_lasso`` in the native library (see ``paper_1312_3039_b200.native``).
+``scs_gen_lasso`` in the native library (see ``paper_1312_3039_b200.native``);
+``gen_lasso_hashed`` is its bit-identical pure-numpy twin (counter-based
+streams), for callers that must not load the native library.
 """
 
 from __future__ import annotations
@@ -242,6 +244,146 @@ def gen_lasso(p, q, nnz_f, seed, mu=None):
     c = np.concatenate([np.zeros(p), mu * np.ones(p), [0.5]])
     colptr, ri, va = _csc_from_triplets(m, n, rows, cols, vals)
     return colptr, ri, va, b, c, {"z": 0, "l": 2 * p, "q": [q + 2], "s": [], "ep": 0}
+
+
+_M64 = (1 << 64) - 1
+_GOLD = np.uint64(0x9E3779B97F4A7C15)
+
+
+def _fmix64(z):
+    with np.errstate(over="ignore"):
+        return _fmix64_(z)
+
+
+def _fmix64_(z):
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def _base_of(seed, dom, j):
+    """Stream bases (host_gen.cpp base_of); j an int64 array."""
+    c = np.uint64((seed * 0xD1B54A32D192ED03 + dom * 0xA24BAED4963EE407) & _M64)
+    with np.errstate(over="ignore"):
+        return _fmix64(c + (np.asarray(j, np.int64) + 1).astype(np.uint64) * _GOLD)
+
+
+def _draw(base, ctr):
+    with np.errstate(over="ignore"):
+        return _fmix64(base + (np.asarray(ctr).astype(np.uint64) + np.uint64(1)) * _GOLD)
+
+
+def _normal4(base, i):
+    """host_gen.cpp normal4: Irwin-Hall sum of four 32-bit uniforms, unit variance."""
+    i = np.asarray(i).astype(np.uint64)
+    a = _draw(base, np.uint64(2) * i)
+    b = _draw(base, np.uint64(2) * i + np.uint64(1))
+    lo = np.uint64(0xFFFFFFFF)
+    s32 = np.uint64(32)
+    u1 = (a >> s32).astype(np.float64) * 2.0 ** -32
+    u2 = (a & lo).astype(np.float64) * 2.0 ** -32
+    u3 = (b >> s32).astype(np.float64) * 2.0 ** -32
+    u4 = (b & lo).astype(np.float64) * 2.0 ** -32
+    return (((u1 + u2) + u3) + u4 - 2.0) * 1.7320508075688772
+
+
+def _hashed_columns(seed, j0, j1, k, q):
+    """Rows (sorted, distinct) and values of F columns [j0, j1), k entries
+    each: host_gen.cpp f_column, vectorised over columns."""
+    js = np.arange(j0, j1, dtype=np.int64)
+    br = _base_of(seed, 0, js)[:, None]
+    bv = _base_of(seed, 1, js)[:, None]
+    if k == 0:
+        return np.zeros((js.size, 0), np.int64), np.zeros((js.size, 0))
+    if 2 * k > q:
+        r = np.arange(q, dtype=np.int64)
+        key = _draw(br, np.uint64(1 << 40) + r.astype(np.uint64)[None, :])
+        order = np.argsort(key, axis=1, kind="stable")[:, :k]  # ties -> smaller row
+        rows = np.sort(order, axis=1)
+    else:
+        rows = (_draw(br, np.arange(k, dtype=np.uint64)[None, :]) % np.uint64(q)).astype(np.int64)
+        rows.sort(axis=1)
+        rnd = 1
+        while True:
+            dup = np.zeros(rows.shape, bool)
+            dup[:, 1:] = rows[:, 1:] == rows[:, :-1]
+            if not dup.any():
+                break
+            ci, pi = np.nonzero(dup)
+            ctr = (np.uint64(rnd) << np.uint64(32)) | pi.astype(np.uint64)
+            rows[ci, pi] = (_draw(br[ci, 0], ctr) % np.uint64(q)).astype(np.int64)
+            cols = np.unique(ci)
+            rows[cols] = np.sort(rows[cols], axis=1)
+            rnd += 1
+    vals = _normal4(bv, np.arange(k, dtype=np.uint64)[None, :])
+    return rows, vals
+
+
+def gen_lasso_hashed(p, q, nnz_f, seed=1, chunk=4096):
+    """Pure-numpy twin of the native ``scs_gen_lasso`` (host_gen.cpp): the
+    same sparse-F LASSO in gen_lasso's encoding (generators.py:81-120), bit
+    for bit, from counter-based fmix64 streams and IEEE-exact arithmetic.
+    Used where the native library must not be loaded (the CPU reference arm
+    of bench.py, fixture generation).  Returns the usual
+    ``(colptr, rowidx, vals, b, c, cone)``."""
+    if p < 1 or q < 1 or nnz_f < 0 or nnz_f > p * q:
+        raise ValueError("gen_lasso_hashed: bad sizes")
+    n, m, r0 = 2 * p + 1, 2 * p + q + 2, 2 * p
+    kq, kr = divmod(nnz_f, p)
+    kcol = np.full(p, kq, np.int64)
+    kcol[:kr] += 1
+    fptr = np.zeros(p + 1, np.int64)
+    np.cumsum(kcol, out=fptr[1:])
+    frows = np.empty(nnz_f, np.int64)
+    fvals = np.empty(nnz_f, np.float64)
+    for lo_, hi_, k in ((0, kr, kq + 1), (kr, p, kq)):
+        for j0 in range(lo_, hi_, chunk):
+            j1 = min(hi_, j0 + chunk)
+            rr, vv = _hashed_columns(seed, j0, j1, int(k), q)
+            frows[fptr[j0]:fptr[j1]] = rr.reshape(-1)
+            fvals[fptr[j0]:fptr[j1]] = vv.reshape(-1)
+    # planted support: the p/10 columns with the smallest (key, column)
+    ks = max(1, p // 10)
+    key = _draw(_base_of(seed, 2, 0), np.arange(p, dtype=np.uint64))
+    support = np.sort(np.argsort(key, kind="stable")[:ks])
+    zhat = _normal4(_base_of(seed, 3, 0), np.arange(ks, dtype=np.uint64))
+    # g = F zhat (rows accumulated over the support columns in order) + noise
+    sel = np.concatenate([np.arange(fptr[j], fptr[j + 1]) for j in support])
+    zrep = np.repeat(zhat, kcol[support])
+    g = np.bincount(frows[sel], weights=fvals[sel] * zrep, minlength=q)
+    g = g + _normal4(_base_of(seed, 4, 0), np.arange(q, dtype=np.uint64)) * math.sqrt(0.1)
+    fcols = np.repeat(np.arange(p), kcol)
+    ftg = np.bincount(fcols, weights=fvals * g[frows], minlength=p)
+    mu = np.max(np.abs(ftg)) * 0.1
+    # CSC (host_gen.cpp fill): column j < p: [j, p+j, F rows], column p+j: [j, p+j]
+    cnt = np.empty(n, np.int64)
+    cnt[:p] = 2 + kcol
+    cnt[p:2 * p] = 2
+    cnt[2 * p] = 2
+    colptr = np.zeros(n + 1, np.int64)
+    np.cumsum(cnt, out=colptr[1:])
+    nnz = int(colptr[-1])
+    rowidx = np.empty(nnz, np.int64)
+    vals = np.empty(nnz, np.float64)
+    idx = np.arange(p, dtype=np.int64)
+    s0 = colptr[:p]
+    rowidx[s0], vals[s0] = idx, 1.0
+    rowidx[s0 + 1], vals[s0 + 1] = p + idx, -1.0
+    fpos = np.repeat(s0 + 2 - fptr[:p], kcol) + np.arange(nnz_f)
+    rowidx[fpos] = r0 + 2 + frows
+    vals[fpos] = 2.0 * fvals
+    s1 = colptr[p:2 * p]
+    rowidx[s1], vals[s1] = idx, -1.0
+    rowidx[s1 + 1], vals[s1 + 1] = p + idx, -1.0
+    rowidx[colptr[2 * p]], vals[colptr[2 * p]] = r0, -1.0
+    rowidx[colptr[2 * p] + 1], vals[colptr[2 * p] + 1] = r0 + 1, 1.0
+    b = np.zeros(m)
+    b[r0] = b[r0 + 1] = 1.0
+    b[r0 + 2:] = 2.0 * g
+    c = np.zeros(n)
+    c[p:2 * p] = mu
+    c[2 * p] = 0.5
+    return colptr, rowidx, vals, b, c, {"z": 0, "l": 2 * p, "q": [q + 2], "s": [], "ep": 0}
 
 
 def gen_portfolio(p, q, seed, gamma=10.0):

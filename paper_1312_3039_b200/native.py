@@ -31,7 +31,7 @@ EXPORTS = (
     "scs_get_state", "scs_get_scaling", "scs_update_vectors",
     "scs_point_residuals", "scs_extract_point", "scs_apply_a", "scs_project_cone", "scs_destroy",
     "scs_last_error", "scs_abi_version", "scs_nccl_unique_id",
-    "scs_partition_rows", "scs_gen_lasso", "scs_bench_iters", "scs_bench_kernel",
+    "scs_partition_rows", "scs_gen_lasso", "scs_bench_iters", "scs_bench_kernel", "scs_query",
     "scs_emu_group_create", "scs_emu_group_destroy", "scs_allreduce",
     "scs_cone_margin_count", "scs_cone_margins", "scs_check_products",
 )
@@ -109,6 +109,7 @@ def load():
                                        C.c_int64, i64p, C.c_int64, C.c_int32, C.c_int32, f64p,
                                        C.c_int64]),
         "scs_bench_kernel": (C.c_int, [hp, C.c_int, C.c_int64, f64p, f64p]),
+        "scs_query": (C.c_int, [hp, C.c_int32, i64p]),
         "scs_destroy": (None, [hp]),
         "scs_emu_group_create": (C.c_void_p, [C.c_int32]),
         "scs_emu_group_destroy": (None, [C.c_void_p]),
@@ -190,6 +191,17 @@ def check_products(A, x=None, y=None, device=0):
     check(lib.scs_check_products(A.nrows, A.ncols, ptr(cp, i64p), ptr(ri, i64p), ptr(va),
                                  ptr(xx), ptr(yy), ptr(ax), ptr(aty), int(device)))
     return ax, aty
+
+
+(Q_FORMAT_A, Q_FORMAT_AT, Q_LAUNCHES_PER_ITER, Q_STREAM_BYTES_A, Q_STREAM_BYTES_AT,
+ Q_CG_ITERS_TOTAL) = range(6)
+
+
+def query(h, key):
+    """scs_query: layout facts of a handle (SpMV format per matrix, ...)."""
+    out = C.c_int64()
+    check(load().scs_query(h, int(key), C.byref(out)), h)
+    return int(out.value)
 
 
 def gen_lasso(p, q, nnz_f, seed=1, row_lo=0, row_hi=0, threads=0):

@@ -52,22 +52,34 @@ def from_ref(data):
              "s": list(sp.psd_sides), "ep": 0})
 
 
-SNAPSHOTS = (1, 2, 3, 5, 10, 20, 50)
-
-
-def dump_traj(name, data, settings, snapshots=None):
-    """snapshots=None keeps iterates 1..50; else only those iteration numbers."""
-    us, vs, kept = [], [], []
+def dump_traj(name, data, settings, snapshots=None, nsample=4000):
+    """Every iterate k <= 50 is kept: in full (snapshots=None), or -- for
+    the big config-2 problems -- as a seeded sample of `nsample` entries of
+    (u, v) at every k plus the full vectors at the `snapshots`.  The norms
+    ||u||, ||v|| and the cumulative CG count are kept for every k <= 50."""
+    us, vs, kept, unorm, vnorm, cgs, su, sv = [], [], [], [], [], [], [], []
+    ell = data.n + data.m + 1
+    sidx = np.sort(np.random.default_rng(99).choice(ell, min(ell, nsample), replace=False))
+    box = {}
 
     def cb(state):
         k = state.iter
-        if k <= N_TRAJ and (snapshots is None or k in snapshots):
+        if k > N_TRAJ:
+            return
+        unorm.append(np.linalg.norm(state.u))
+        vnorm.append(np.linalg.norm(state.v))
+        cgs.append(box["ws"].cache.cg_iters_total)
+        if snapshots is not None:
+            su.append(state.u[sidx].copy())
+            sv.append(state.v[sidx].copy())
+        if snapshots is None or k in snapshots:
             us.append(state.u.copy())
             vs.append(state.v.copy())
             kept.append(k)
 
     t0 = time.perf_counter()
     ws = ref.Workspace(data, settings)
+    box["ws"] = ws
     sol = ws.solve(on_iteration=cb)
     dt = time.perf_counter() - t0
     colptr, rowidx, vals, b, c, cone = from_ref(data)
@@ -79,6 +91,7 @@ def dump_traj(name, data, settings, snapshots=None):
             "alpha", "max_iters", "eps_pri", "eps_dual", "eps_gap", "eps_infeas",
             "eps_unbdd", "check_interval", "cg_max", "cg_tol", "normalize", "sweeps")}),
         us=np.array(us), vs=np.array(vs), kept=np.array(kept, np.int64),
+        unorm=np.array(unorm), vnorm=np.array(vnorm), cg_total=np.array(cgs, np.int64),
         status=sol.status.value, iterations=sol.info.iterations,
         cg_iters=sol.info.cg_iters,
         primal_obj=sol.primal_obj, dual_obj=sol.dual_obj,
@@ -91,6 +104,8 @@ def dump_traj(name, data, settings, snapshots=None):
                       res.infeas_measure]),
         ref_seconds=dt,
     )
+    if snapshots is not None:
+        out.update(sidx=sidx, us_sample=np.array(su), vs_sample=np.array(sv))
     for key in ("x", "y", "s", "certificate", "certificate_unbounded"):
         val = getattr(sol, key)
         if val is not None:
@@ -183,12 +198,19 @@ def main():
     c1 = gen.gen_lp_soc(3000, 1000, 0.01, 100, 10, seed=0)
     eps5 = dict(eps_pri=1e-5, eps_dual=1e-5, eps_gap=1e-5, eps_infeas=1e-5,
                 eps_unbdd=1e-5)
-    dump_traj("c1_lp_soc", to_ref(*c1), S(**ind, **eps5, max_iters=5000),
-              snapshots=SNAPSHOTS)
+    dump_traj("c1_lp_soc", to_ref(*c1), S(**ind, **eps5, max_iters=5000))
     # config 2: infeasible / unbounded m=30000 n=10000 (BASELINE.json configs[1])
     for kind in ("lp_infeasible", "lp_unbounded"):
         c2 = gen.gen_lp(kind, 10000, 30000, seed=2)
         dump_traj(f"c2_{kind}", to_ref(*c2), S(**ind, **eps5), snapshots=(1, 2, 10, 50))
+    # the post-loop status rule (solver.py:364-369): MAX_ITERS_REACHED when
+    # tau > 1e-8 ||u|| at max_iters, else INDETERMINATE.  The LASSO shape
+    # q = 18 p is the BASELINE regime where the reference stalls.
+    dump_traj("maxit_lasso_q18p", ref.generators.gen_lasso(10, 180, 1), S(**ind, max_iters=400))
+    lpi = ref.generators.gen_lp_family("lp_infeasible", 20, 40, 3)
+    never = dict(eps_infeas=1e-300, eps_unbdd=1e-300)  # certificates never accepted
+    dump_traj("maxit_lp_infeasible", lpi, S(**ind, **never, max_iters=10))
+    dump_traj("indet_lp_infeasible", lpi, S(**ind, **never, max_iters=100))
 
 
 if __name__ == "__main__":

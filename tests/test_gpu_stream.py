@@ -113,7 +113,7 @@ def test_stream_golden_trajectories(stream, name):
     for i, k in enumerate(kept):
         assert rel(got[k], d["us"][i]) < 1e-9, (name, k)
     assert sol.status.value == d["status"]
-    assert abs(sol.info.iterations - d["iterations"]) <= max(2, d["iterations"] // 200)
+    assert sol.info.iterations == d["iterations"]
 
 
 def test_stream_lasso_deterministic(monkeypatch):

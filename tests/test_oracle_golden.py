@@ -50,19 +50,41 @@ def _check(name):
     assert math.isclose(s.rho, float(d["rho"]), rel_tol=1e-13)
     assert rel(s.g, d["g"]) < 1e-12
     kept = list(d["kept"])
-    got = {}
+    got, norms, cgs, samp = {}, [], [], []
+    sidx = d.get("sidx")
 
     def cb(k, u, v):
         if k in kept:
             got[k] = (u.copy(), v.copy())
+        if k <= 50:
+            norms.append((np.linalg.norm(u), np.linalg.norm(v)))
+            cgs.append(s.cg_iters_total)
+            if sidx is not None:
+                samp.append((u[sidx].copy(), v[sidx].copy()))
 
     out = s.solve(on_iteration=cb)
     for i, k in enumerate(kept):
         assert rel(got[k][0], d["us"][i]) < 1e-12, (name, k)
         assert rel(got[k][1], d["vs"][i]) < 1e-12, (name, k)
+    # every iterate k <= 50: norms, cumulative CG count, sampled entries
+    np.testing.assert_allclose([a for a, _ in norms], d["unorm"], rtol=1e-12)
+    np.testing.assert_allclose([b for _, b in norms], d["vnorm"], rtol=1e-12)
+    np.testing.assert_array_equal(cgs, d["cg_total"])
+    for k, (su, sv) in enumerate(samp):
+        assert rel(su, d["us_sample"][k]) < 1e-12 and rel(sv, d["vs_sample"][k]) < 1e-12, k
     assert out["status"] == d["status"]
     assert out["iterations"] == d["iterations"]
     assert out["cg_iters"] == d["cg_iters"]
+    # the reported Residuals of the last check (scaling.py:148-207)
+    r = out["residuals"]
+    fields = ("pri_norm", "dual_norm", "gap", "pri_thresh", "dual_thresh", "gap_thresh",
+              "unbdd_measure", "infeas_measure")
+    for i, (got_r, ref_r) in enumerate(zip([getattr(r, f) for f in fields], d["res"])):
+        if np.isinf(ref_r):
+            assert np.isinf(got_r), (name, i)
+        else:  # the gap crosses zero: scaled by its threshold
+            scale = max(abs(ref_r), abs(d["res"][5])) if i == 2 else abs(ref_r)
+            assert abs(got_r - ref_r) <= 1e-9 * scale, (name, i)
     assert rel(out["u"], d["u_final"]) < 1e-9
     for key in ("x", "y", "s", "certificate"):
         if key in d:
