@@ -5,8 +5,8 @@
  * reference, /root/reference/pkg/src/conesplit).  The reference has no FFI:
  * its hot path is the Python loop body Workspace.solve (solver.py:355-369)
  * over iterate_once (solver.py:153-166), project_affine / solve_kkt indirect
- * (embedding.py:101-114,165-197), cg_solve (sparse_linalg.py:450-487),
- * spmv/spmv_t (sparse_linalg.py:318-335), project_embedding_cone
+ * (embedding.py:101-114,165-197), cg_solve (sparse_linalg.py:253-290),
+ * spmv/spmv_t (sparse_linalg.py:121-138), project_embedding_cone
  * (cones.py:241-249), residuals_original (scaling.py:148-207) and
  * check_termination (solver.py:210-234), with equilibrate
  * (scaling.py:79-129) and setup_cache (embedding.py:117-162) run once.
@@ -34,7 +34,7 @@ extern "C" {
 
 /* error codes -> Python exception classes:
  *   SCS_EINVAL, SCS_ENONFINITE -> ValueError (problem.py:38-53,
- *   sparse_linalg.py:457-484, cones.py:194-200); SCS_ESETUP -> SetupError
+ *   sparse_linalg.py:260-287, cones.py:194-200); SCS_ESETUP -> SetupError
  *   (embedding.py:22-23, 159-161); SCS_ENOCONV, SCS_ECUDA, SCS_ENCCL,
  *   SCS_ENOMEM -> RuntimeError (cones.py:164-167). */
 #define SCS_OK 0
@@ -150,7 +150,7 @@ int scs_create(const scs_problem* prob, const scs_settings* st,
 /* Workspace.solve (solver.py:336-378) up to the loop exit: run the whole
  * loop on the device.  warm_x/y/s (original units, nullable as a group)
  * follow initialize_state (solver.py:128-150) via scale_solution
- * (scaling.py:433-438).  On return `info` holds the status (including
+ * (scaling.py:132-137).  On return `info` holds the status (including
  * MAX_ITERS_REACHED / INDETERMINATE), iteration counts and residuals. */
 int scs_solve(scs_handle* h, const double* warm_x, const double* warm_y,
               const double* warm_s, scs_info* info);
@@ -190,7 +190,7 @@ int scs_point_residuals(scs_handle* h, const double* x, const double* y,
  * dual_obj = -b'y without a second upload of the point. */
 int scs_extract_point(scs_handle* h, double* x, double* y, double* s, double* out5);
 
-/* spmv / spmv_t (sparse_linalg.py:318-335) on the device copy of the
+/* spmv / spmv_t (sparse_linalg.py:121-138) on the device copy of the
  * ORIGINAL (unscaled) A is not kept; these apply the equilibrated A_hat:
  * which = 0: y = A_hat x; which = 1: x = A_hat^T y. */
 int scs_apply_a(scs_handle* h, int which, const double* in, double* out);
@@ -244,6 +244,12 @@ int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms_per_launc
 #define SCS_Q_STREAM_BYTES_AT 4
 #define SCS_Q_CG_ITERS_TOTAL 5
 int scs_query(scs_handle* h, int32_t key, int64_t* out);
+
+/* Page-locked host memory (cudaHostAlloc) for warm starts and solution
+ * buffers: copies to and from it run at full link speed and overlap the
+ * device work (no reference counterpart; the Python layer pools it). */
+int scs_host_alloc(int64_t bytes, void** out);
+void scs_host_free(void* p);
 
 void scs_destroy(scs_handle* h);
 const char* scs_last_error(const scs_handle* h);

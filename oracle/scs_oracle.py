@@ -40,7 +40,7 @@ STATUS = ("solved", "infeasible", "unbounded", "infeasible_and_unbounded",
 
 
 # ---------------------------------------------------------------------------
-# sparse products (sparse_linalg.py:318-335): bincount scatter, ascending
+# sparse products (sparse_linalg.py:121-138): bincount scatter, ascending
 # index order per output entry, products rounded before the sum.
 # ---------------------------------------------------------------------------
 class Csc:
@@ -73,14 +73,14 @@ class Csc:
 
 
 def mul(A: Csc, x):
-    """y = A x   (sparse_linalg.py:318-325)."""
+    """y = A x   (sparse_linalg.py:121-128)."""
     if A.nnz == 0:
         return np.zeros(A.m)
     return np.bincount(A.rowidx, weights=A.vals * x[A.colidx], minlength=A.m)
 
 
 def mul_t(A: Csc, y):
-    """x = A^T y (sparse_linalg.py:328-335)."""
+    """x = A^T y (sparse_linalg.py:131-138)."""
     if A.nnz == 0:
         return np.zeros(A.n)
     return np.bincount(A.colidx, weights=A.vals * y[A.rowidx], minlength=A.n)
@@ -470,7 +470,7 @@ def termination(res: Res, eps):
 
 
 # ---------------------------------------------------------------------------
-# linear system: CG on I + A^T A (sparse_linalg.py:450-487, embedding.py:86-197)
+# linear system: CG on I + A^T A (sparse_linalg.py:253-290, embedding.py:86-197)
 # ---------------------------------------------------------------------------
 def cg(A: Csc, rhs, x0, tol, max_iter, minv=None):
     """Plain warm-started CG; returns (x, iterations).
@@ -624,7 +624,7 @@ class OracleSolver:
         u[-1] = 1.0
         if warm_start is None:
             v[-1] = 1.0
-        else:  # solver.py:345-348, scaling.py:433-438, solver.py:140-149
+        else:  # solver.py:345-348, scaling.py:132-137, solver.py:140-149
             x0, y0, s0 = (np.asarray(t, float) for t in warm_start)
             u[:n] = self.sigma * x0 / self.E
             u[n:n + m] = self.rho * y0 / self.D

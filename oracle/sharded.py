@@ -63,7 +63,7 @@ class ShardedOracle:
 
     # -- equilibration (scaling.py:79-129) --------------------------------------
     def _row_scale(self, rn):
-        """Block means of row norms over the global blocks (scaling.py:375-413)."""
+        """Block means of row norms over the global blocks (scaling.py:74-112)."""
         sums = np.zeros(self.nseg)
         for gid, a, b, _ in self.segs:
             sums[gid] = rn[a:b].sum()

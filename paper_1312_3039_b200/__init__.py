@@ -28,13 +28,10 @@ from .api import (  # noqa: F401
 
 from .problem_io import (  # noqa: F401
     FileFormatError,
-    problem_from_dict,
-    problem_to_dict,
     read_problem,
-    read_solution,
-    solution_from_dict,
     write_problem,
-    write_solution,
 )
+
+from .native import pinned_empty, pinned_zeros  # noqa: F401,E402
 
 __version__ = "0.1.0"

@@ -579,7 +579,9 @@ class Workspace:
         residuals without copying u, v out and the point back in."""
         d = self.data
         sol = Solution(status=status)
-        x, y, s = np.empty(d.n), np.empty(d.m), np.empty(d.m)
+        # page-locked (pooled) result buffers: the device-to-host copies run at
+        # link speed, overlapped with the point residuals
+        x, y, s = native.pinned_empty(d.n), native.pinned_empty(d.m), native.pinned_empty(d.m)
         out = np.empty(5)
         self._call(self._lib.scs_extract_point(self._h, native.ptr(x), native.ptr(y),
                                                native.ptr(s), native.ptr(out)))

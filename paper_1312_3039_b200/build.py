@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libscs_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["solver.cu", "check.cu", "host_gen.cpp"]
-HEADERS = ["common.cuh", "cones.cuh", "kernels.cuh", "tiled.cuh", "stream.cuh"]
+HEADERS = ["common.cuh", "cones.cuh", "kernels.cuh", "stream.cuh"]
 
 
 def _nvcc():

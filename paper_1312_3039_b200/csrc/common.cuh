@@ -22,10 +22,11 @@ constexpr int kMaxGrid = 4096;   // partial slots per scalar
 
 // Device error bits (mapped to SCS_* codes on the host).
 enum : int {
-  ERR_CG_NONFINITE = 1,   // sparse_linalg.py:463-464,480-481
-  ERR_CG_CURVATURE = 2,   // sparse_linalg.py:473-474
+  ERR_CG_NONFINITE = 1,   // sparse_linalg.py:266-267,480-481
+  ERR_CG_CURVATURE = 2,   // sparse_linalg.py:276-277
   ERR_CONE_NONFINITE = 4, // cones.py:194-200
   ERR_JACOBI = 8,         // cones.py:164-167
+  ERR_SCHED = 16,         // internal: iteration graph variant != refresh schedule
 };
 
 // Everything the iteration needs to branch on, kept in device memory.
@@ -64,6 +65,9 @@ struct Ctl {
   double sums[kMaxRed];     // last finished reduction (debug)
   unsigned int counter;     // last-block counter
   unsigned int pad2;
+  // device-side loop (solver.cu build_loop_graph): iterations still to run,
+  // iterations run by the last loop launch, and how many were refreshes
+  long long loop_left, loop_done, loop_refresh;
 };
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -18,7 +18,8 @@ namespace scs {
 //   F(rho) = ((rho-1) r0 + s0) e^rho - (r0 - rho s0) e^-rho
 //            - t0 (rho^2 - rho + 1) = 0
 // on the interval where s > 0 and lam > 0 (F is increasing there).  Solved
-// by bisection on an overflow-free rescaling of F with the same sign.
+// by a safeguarded Newton iteration on an overflow-free rescaling of F with
+// the same sign (the CPU oracle bisects instead: an independent check).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ bool exp_in_primal(double r, double s, double t) {
   return (s > 0.0 && s * exp(r / s) <= t) || (r <= 0.0 && s == 0.0 && t >= 0.0);
@@ -28,24 +29,33 @@ __device__ __forceinline__ bool exp_in_dual(double u, double v, double w) {
          (u == 0.0 && v >= 0.0 && w >= 0.0);
 }
 
-// sign(F(rho)) without overflow: F * q * e^{-rho} for rho >= 0 and
-// F * q * e^{rho} for rho < 0 (q = rho^2 - rho + 1 > 0).
-__device__ __forceinline__ double exp_sign_fn(double rho, double r0, double s0, double t0) {
-  const double q = rho * rho - rho + 1.0;
+// G(rho) = F(rho) * q * e^{-rho} (rho >= 0) or F(rho) * q * e^{rho} (rho < 0),
+// q = rho^2 - rho + 1 > 0: same sign as F, no overflow; and its derivative
+// (for the Newton step).  With a = (rho-1) r0 + s0 (a' = r0),
+// b = r0 - rho s0 (b' = -s0), q' = 2 rho - 1:
+//   rho >= 0: G = a - b e^{-2rho} - t0 q e^{-rho},
+//             G' = r0 + (s0 + 2b) e^{-2rho} - t0 (q' - q) e^{-rho}
+//   rho <  0: G = a e^{2rho} - b - t0 q e^{rho},
+//             G' = (r0 + 2a) e^{2rho} + s0 - t0 (q' + q) e^{rho}
+__device__ __forceinline__ double exp_sign_fn(double rho, double r0, double s0, double t0,
+                                              double* dG = nullptr) {
+  const double q = rho * rho - rho + 1.0, dq = 2.0 * rho - 1.0;
   const double a = (rho - 1.0) * r0 + s0, b = r0 - rho * s0;
   if (rho >= 0.0) {
-    const double e = exp(-rho);
-    return a - b * e * e - t0 * q * e;
+    const double e = exp(-rho), e2 = e * e;
+    if (dG) *dG = r0 + (s0 + 2.0 * b) * e2 - t0 * (dq - q) * e;
+    return a - b * e2 - t0 * q * e;
   }
-  const double e = exp(rho);
-  return a * e * e - b - t0 * q * e;
+  const double e = exp(rho), e2 = e * e;
+  if (dG) *dG = (r0 + 2.0 * a) * e2 + s0 - t0 * (dq + q) * e;
+  return a * e2 - b - t0 * q * e;
 }
 
 __device__ inline void exp_proj_primal(double r0, double s0, double t0, double* out) {
   if (exp_in_primal(r0, s0, t0)) { out[0] = r0; out[1] = s0; out[2] = t0; return; }
   if (exp_in_dual(-r0, -s0, -t0)) { out[0] = 0.0; out[1] = 0.0; out[2] = 0.0; return; }
   if (r0 <= 0.0 && s0 <= 0.0) { out[0] = r0; out[1] = 0.0; out[2] = fmax(t0, 0.0); return; }
-  // root interval: s(rho) > 0 and lam(rho) > 0
+  // root interval: s(rho) > 0 and lam(rho) > 0 (G increasing there)
   double lo = -INFINITY, hi = INFINITY;
   if (r0 > 0.0) lo = fmax(lo, 1.0 - s0 / r0);
   else if (r0 < 0.0) hi = fmin(hi, 1.0 - s0 / r0);
@@ -59,12 +69,24 @@ __device__ inline void exp_proj_primal(double r0, double s0, double t0, double* 
     hi = lo + 1.0;
     for (int i = 0; i < 80 && exp_sign_fn(hi, r0, s0, t0) < 0.0; ++i) hi = 2.0 * fabs(hi) + 1.0;
   }
-  for (int it = 0; it < 200 && hi - lo > 1e-15 * fmax(1.0, fabs(lo)); ++it) {
-    const double mid = 0.5 * (lo + hi);
-    if (mid <= lo || mid >= hi) break;
-    if (exp_sign_fn(mid, r0, s0, t0) < 0.0) lo = mid; else hi = mid;
+  // safeguarded Newton: a Newton step from the current point when it lands
+  // strictly inside the bracket, else bisection; the bracket shrinks with
+  // the sign of G at every evaluated point (typically 4-8 evaluations)
+  double rho = 0.5 * (lo + hi);
+  for (int it = 0; it < 100; ++it) {
+    double dG;
+    const double G = exp_sign_fn(rho, r0, s0, t0, &dG);
+    if (G == 0.0) { lo = hi = rho; break; }
+    if (G < 0.0) lo = rho; else hi = rho;
+    if (!(hi - lo > 1e-15 * fmax(1.0, fabs(rho)))) break;
+    double nx = rho - G / dG;
+    const bool newton = dG > 0.0 && nx > lo && nx < hi;
+    if (!newton) nx = 0.5 * (lo + hi);
+    if (nx <= lo || nx >= hi) break;
+    if (newton && fabs(nx - rho) <= 1e-16 * fmax(1.0, fabs(rho))) { rho = nx; lo = hi = nx; break; }
+    rho = nx;
   }
-  const double rho = 0.5 * (lo + hi);
+  rho = (lo == hi) ? lo : 0.5 * (lo + hi);
   const double q = rho * rho - rho + 1.0;
   const double s = ((rho - 1.0) * r0 + s0) / q;
   const double lam = (r0 - rho * s0) / q;

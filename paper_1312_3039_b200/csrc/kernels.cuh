@@ -6,11 +6,11 @@
 // the Ctl block, so the host never synchronises inside an iteration:
 //
 //   k_prep         w = u+v, rhs = w[:-1] - w_tau h, ||rhs|| -> CG tol       embedding.py:177-185
-//   SpMV A^T  [EpiAtFirst]  cg_rhs = rhs_x - A^T rhs_y, r0 = cg_rhs - G x0   embedding.py:109, sparse_linalg.py:461-469
+//   SpMV A^T  [EpiAtFirst]  cg_rhs = rhs_x - A^T rhs_y, r0 = cg_rhs - G x0   embedding.py:109, sparse_linalg.py:264-272
 //                           (+ A^T u_y of the previous iterate, see below --
 //                           every R-th iteration; the others run EpiAtFirst1,
 //                           NV = 1, with A^T u_y from recurrences)
-//   cg_max x { SpMV A [EpiAp]; SpMV A^T [EpiAtGp]; k_cg_update; k_cg_p }    sparse_linalg.py:470-485
+//   cg_max x { SpMV A [EpiAp]; SpMV A^T [EpiAtGp]; k_cg_update; k_cg_p }    sparse_linalg.py:273-288
 //                           (the first A pass also carries A u_x, below --
 //                           every R-th iteration; the others carry A u_x by
 //                           recurrence in k_cone_tail, SCS_RES_RECUR)
@@ -20,13 +20,13 @@
 //   k_cone_apply   large SOC + PSD (Jacobi) blocks                          cones.py:172-191
 //
 // Matrix passes per iteration: 2 + 2k (k = CG steps); the reference makes 6 + 2k
-// (k = CG steps, sparse_linalg.py:461,471,486 + embedding.py:109,113 +
-// scaling.py:466-467).  Removed, with bit-identical results:
+// (k = CG steps, sparse_linalg.py:264,471,486 + embedding.py:109,113 +
+// scaling.py:165-166).  Removed, with bit-identical results:
 //  * A x_warm at the head of CG: the previous iteration's EpiAFinal already
 //    produced A x for the same x (cg_warm) and stored it (Axw);
-//  * the trailing exact-residual pass (sparse_linalg.py:486), whose value
+//  * the trailing exact-residual pass (sparse_linalg.py:289), whose value
 //    its caller discards (embedding.py:110);
-//  * the two residual passes of the termination check (scaling.py:466-467):
+//  * the two residual passes of the termination check (scaling.py:165-166):
 //    they gather the same interleaved sector as the next iteration's first
 //    A^T / A pass, so they ride along; the next iteration is speculative
 //    until the check of the previous one has passed (its state writes come
@@ -57,7 +57,7 @@ struct Vec {
   double *u, *v;              // n + m + 1 (SolverState)
   const double *c, *b;        // scaled data
   const double *D, *E;        // scalings
-  const double *Dinv, *Einv;  // 1/D, 1/E (scaling.py:464-465)
+  const double *Dinv, *Einv;  // 1/D, 1/E (scaling.py:163-164)
   double *gx, *gy;            // g = M^-1 h
   double *rhs_x, *rhs_y;      // rhs = w[:-1] - w_tau h
   double *x;                  // CG iterate == cg_warm (embedding.py:111)
@@ -70,6 +70,7 @@ struct Vec {
   double *Agx;                // A g_x (m): residual recurrence on (nullptr: off)
   // A^T side of the residual recurrence (n each; T == nullptr: off):
   double *T;                  // A^T A x of the CG iterate (carried through the Gp products)
+  double *AtAp;               // A^T A p of the current CG step (EpiAtGp), for T
   double *Sv;                 // A^T rhs_y of this iteration
   double *Uy;                 // A^T u_y of the current state
   double *Dd;                 // A^T (v_y - u_y) of the current state
@@ -356,10 +357,10 @@ struct EpiBase {
   __device__ __forceinline__ double utau() const { return V.u[V.n + V.m]; }
 };
 
-// First A^T pass of an iteration (sparse_linalg.py:461-469 + scaling.py:467):
+// First A^T pass of an iteration (sparse_linalg.py:264-272 + scaling.py:166):
 //   r0 = (rhs_x - x0) - A^T (rhs_y + A x0); p = r0
 // and, when the previous iteration is due a termination check, A^T u_y of
-// that iterate (dual residual / infeasibility, scaling.py:484-490).  One
+// that iterate (dual residual / infeasibility, scaling.py:183-189).  One
 // 128-bit gather per nonzero serves both products.
 struct EpiAtFirst : EpiBase {
   static constexpr int NV = 2, STRIDE = 2, NR = 5;
@@ -492,7 +493,7 @@ struct EpiTRef : EpiBase {
 };
 
 // q = A p.  MERGED: the first CG pass also carries A u_x of the previous
-// iterate (primal residual / unboundedness, scaling.py:466-489) and closes
+// iterate (primal residual / unboundedness, scaling.py:165-188) and closes
 // that iteration's termination check (solver.py:359-363).
 template <bool MERGED>
 struct EpiAp : EpiBase {
@@ -538,7 +539,7 @@ struct EpiAp : EpiBase {
   }
 };
 
-// Gp = p + A^T q, p'Gp -> alpha (sparse_linalg.py:471-475)
+// Gp = p + A^T q, p'Gp -> alpha (sparse_linalg.py:274-278)
 struct EpiAtGp : EpiBase {
   static constexpr int NV = 1, STRIDE = 1, NR = 1;
   __device__ bool load() { return !V.ctl->stop && !V.ctl->cg_done; }
@@ -548,6 +549,7 @@ struct EpiAtGp : EpiBase {
     const double pj = pf.p;
     const double g = pj + s[0];
     V.Gp[j] = g;
+    if (V.AtAp) V.AtAp[j] = s[0];  // T += alpha A^T A p without the Gp - p cancellation
     red[0] += pj * g;
   }
   __device__ void finish(const double* tot) const {
@@ -598,6 +600,7 @@ struct EpiAFinal : EpiBase {
 // forced residual evaluation): A u_x ...
 struct EpiResA : EpiBase {
   static constexpr int NV = 1, STRIDE = 1, NR = 3;
+  double* store;  // A u_x of the checked state (V.Aux: reused by the extraction)
   __device__ bool load() {
     const Ctl* c = V.ctl;
     return !c->stop && (c->check_pending || c->force_check);
@@ -611,6 +614,7 @@ struct EpiResA : EpiBase {
     const double di = p.d;
     const double pr = di * (t / p.ut - p.b);
     const double ub = di * t;
+    if (store) store[i] = s[0];
     red[0] += pr * pr;
     red[1] += ub * ub;
     red[2] += p.b * p.uy;
@@ -623,9 +627,10 @@ struct EpiResA : EpiBase {
   }
 };
 
-// ... and A^T u_y, then the status (scaling.py:467-507, solver.py:210-234)
+// ... and A^T u_y, then the status (scaling.py:166-206, solver.py:210-234)
 struct EpiResAt : EpiBase {
   static constexpr int NV = 1, STRIDE = 1, NR = 3;
+  double* store;  // A^T u_y of the checked state (V.Uy: reused by the extraction)
   __device__ bool load() {
     const Ctl* c = V.ctl;
     return !c->stop && (c->check_pending || c->force_check);
@@ -641,6 +646,7 @@ struct EpiResAt : EpiBase {
     red[0] += du * du;
     red[1] += inf * inf;
     red[2] += p.c * p.ux;
+    if (store) store[j] = s[0];
   }
   __device__ void finish(const double* tot) const {
     if (threadIdx.x) return;
@@ -670,7 +676,7 @@ struct EpiApPlain2 : EpiBase {
   __device__ void finish(const double*) const {}
 };
 // ... then the residual terms of A u_x and the termination check
-// (scaling.py:466-489, solver.py:359-363): EpiAp<true>'s epilogue over Aux
+// (scaling.py:165-188, solver.py:359-363): EpiAp<true>'s epilogue over Aux
 struct EpiResY : EpiBase {
   static constexpr int NV = 1, STRIDE = 1, NR = 3;
   __device__ bool load() {

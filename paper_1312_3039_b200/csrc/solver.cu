@@ -24,7 +24,6 @@
 #include "common.cuh"
 #include "cones.cuh"
 #include "kernels.cuh"
-#include "tiled.cuh"
 #include "stream.cuh"
 
 #ifdef SCS_WITH_NCCL
@@ -38,8 +37,12 @@ namespace scs {
 // ===========================================================================
 
 // CG tolerance of this iteration from ||rhs||^2 (embedding.py:179-185)
-__device__ void prep_finish(Ctl* c, double rhs2) {
+__device__ void prep_finish(Ctl* c, double rhs2, int variant, int R) {
   const long long k = ++c->k_sched;
+  // graph variant of this iteration (1: non-refresh, 2: refresh of the
+  // residual recurrences, solver.cu run_iteration) must match the schedule
+  // the gated epilogues use (kernels.cuh EpiBase::gate_ok)
+  if (variant && ((k - 1) % R == 0) != (variant == 2)) { c->err |= ERR_SCHED; c->stop = 1; }
   c->tol = c->cg_tol > 0.0 ? c->cg_tol
                            : 1e-3 * (1.0 + sqrt(rhs2)) / pow((double)(k < 1 ? 1 : k), 1.5);
   c->cg_done = 0;
@@ -49,7 +52,7 @@ __device__ void prep_finish(Ctl* c, double rhs2) {
 // w = u + v; rhs = w[:-1] - w_tau h; ||rhs||^2 (embedding.py:177-185).
 // Row-sharded (defer): the x-part counts on rank 0 only (V.xw) and the
 // total is all-reduced before k_prep_finish.
-__global__ void __launch_bounds__(kBlock) k_prep(Vec V, int defer) {
+__global__ void __launch_bounds__(kBlock) k_prep(Vec V, int defer, int variant, int R) {
   Ctl* c = V.ctl;
   if (c->stop) return;
   const long long n = V.n, m = V.m;
@@ -75,15 +78,33 @@ __global__ void __launch_bounds__(kBlock) k_prep(Vec V, int defer) {
   }
   if (grid_sum_last<1>(red, V.part, &c->counter) && threadIdx.x == 0) {
     if (defer) V.dred[0] = red[0];
-    else prep_finish(c, red[0]);
+    else prep_finish(c, red[0], variant, R);
   }
 }
-__global__ void k_prep_finish(Vec V) {
+__global__ void k_prep_finish(Vec V, int variant, int R) {
   if (V.ctl->stop || threadIdx.x) return;
-  prep_finish(V.ctl, V.dred[0]);
+  prep_finish(V.ctl, V.dred[0], variant, R);
 }
 
-// x += alpha p; r -= alpha Gp; r'r -> stop test / beta (sparse_linalg.py:476-485).
+// Device-side loop control (build_loop_graph): the body of a WHILE graph
+// node is [k_loop_pick -> SWITCH(non-refresh graph, refresh graph) ->
+// k_loop_next].  k_loop_pick selects this iteration's variant from the
+// refresh schedule (k_sched = 1, 1 + R, ...); k_loop_next counts the
+// iteration and keeps looping while iterations are left and no kernel has
+// stopped the solve (termination status, error).  One solve is one graph
+// launch: no host synchronisation and no no-op iterations after the stop.
+__global__ void k_loop_pick(Ctl* c, cudaGraphConditionalHandle sw, int R) {
+  const bool refresh = R > 0 && c->k_sched % R == 0;  // before k_prep's increment
+  if (refresh) c->loop_refresh += 1;
+  cudaGraphSetConditional(sw, refresh ? 1u : 0u);
+}
+__global__ void k_loop_next(Ctl* c, cudaGraphConditionalHandle wh) {
+  c->loop_done += 1;
+  c->loop_left -= 1;
+  cudaGraphSetConditional(wh, (c->loop_left > 0 && !c->stop) ? 1u : 0u);
+}
+
+// x += alpha p; r -= alpha Gp; r'r -> stop test / beta (sparse_linalg.py:279-288).
 // Opt-in PCG: beta from r'M^-1 r.  Opt-in recurrence (recur): A x is carried
 // as Axw += alpha q over the m rows (the final A pass is then skipped).
 __global__ void __launch_bounds__(kBlock) k_cg_update(Vec V, long long cap, int recur) {
@@ -94,7 +115,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(Vec V, long long cap, int 
   const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
   const long long nt = (long long)gridDim.x * kBlock;
   for (long long j = tid; j < V.n; j += nt) {
-    if (V.T) V.T[j] += a * (V.Gp[j] - V.X2[2 * j]);  // A^T A x += alpha A^T A p
+    if (V.T) V.T[j] += a * V.AtAp[j];  // A^T A x += alpha A^T A p
     V.x[j] += a * V.X2[2 * j];
     const double r = V.r[j] - a * V.Gp[j];
     V.r[j] = r;
@@ -114,7 +135,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(Vec V, long long cap, int 
   }
 }
 
-// p = r + beta p (sparse_linalg.py:484); PCG: p = M^-1 r + beta p
+// p = r + beta p (sparse_linalg.py:287); PCG: p = M^-1 r + beta p
 __global__ void __launch_bounds__(kBlock) k_cg_p(Vec V) {
   Ctl* c = V.ctl;
   if (c->stop || c->cg_done) return;
@@ -748,7 +769,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_psd_grid(Vec V, Cones K, double* 
 
 __device__ void finish_residuals(Ctl* c, double ut, double s_pri, double s_unb, double buy,
                                  double s_dual, double s_inf, double cux) {
-  // scaling.py:472-507
+  // scaling.py:171-206
   const double unbdd = cux < 0.0 ? sqrt(s_unb) * c->c_ref / (-cux) : INFINITY;
   const double infeas = buy < 0.0 ? sqrt(s_inf) * c->b_ref / (-buy) : INFINITY;
   double pri, dual, gap, gth;
@@ -825,53 +846,7 @@ __global__ void k_gather_csr(const int* perm, const int* colidx, const double* v
     av[k] = vals[s];
   }
 }
-// Row bands of A for the A^T passes (L2 blocking, see setup_bands): the
-// banded CSR(A^T) has S*n rows; row s*n + j holds the entries of column j
-// whose row index lies in band s, in their original order.  One warp per
-// column; per-warp band counters in shared memory; __match_any_sync groups
-// the lanes of a 32-entry step by band, so placement is stable.
-__global__ void __launch_bounds__(kBlock) k_band_pass(Csr At, int band_rows, int S, long long n,
-                                                      const long long* base, long long* cnt,
-                                                      int* ci2, double* v2) {
-  __shared__ long long sc[kBlock / 32][32];
-  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long j = w; j < n; j += nw) {
-    sc[wi][lane] = (base && lane < S) ? base[(long long)lane * n + j] : 0;
-    __syncwarp();
-    const long long k0 = At.rp[j], k1 = At.rp[j + 1];
-    for (long long kb = k0; kb < k1; kb += 32) {
-      const long long k = kb + lane;
-      const bool ok = k < k1;
-      const int r = ok ? At.ci[k] : 0;
-      const int b = ok ? min(r / band_rows, S - 1) : -1;
-      const unsigned mm = __match_any_sync(0xffffffffu, b);
-      const long long at = sc[wi][b < 0 ? 0 : b];
-      __syncwarp();
-      if (ok && base) {
-        const long long d = at + __popc(mm & ((1u << lane) - 1u));
-        ci2[d] = r;
-        v2[d] = At.v[k];
-      }
-      if (ok && lane == __ffs(mm) - 1) sc[wi][b] = at + __popc(mm);
-      __syncwarp();
-    }
-    if (!base && lane < S) cnt[(long long)lane * n + j] = sc[wi][lane];
-    __syncwarp();
-  }
-}
-// out[i] = sum over bands of P[s*len + i], bands in order (== k_rows' sum)
-__global__ void k_band_sum(const double* P, long long len, int S, double* out) {
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nt = (long long)gridDim.x * blockDim.x;
-  for (long long i = tid; i < len; i += nt) {
-    double s = P[i];
-    for (int b = 1; b < S; ++b) s += P[b * len + i];
-    out[i] = s;
-  }
-}
-// per-row Euclidean norm (scaling.py:397-401), warp per row
+// per-row Euclidean norm (scaling.py:96-100), warp per row
 __global__ void k_row_norms(Csr A, double* out) {
   const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -897,7 +872,7 @@ __global__ void k_row_sumsq(Csr A, double* out) {
   }
 }
 // nrm = sqrt(sumsq); scale = where(nrm > 0, 1/sqrt(nrm), 1); acc *= scale
-// (scaling.py:398, 405-407)
+// (scaling.py:97, 405-407)
 __global__ void k_inv_sqrt_scale(double* sumsq, long long n, double* scale, double* acc) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
@@ -925,7 +900,7 @@ __global__ void k_scale_cols(const int* ci, double* v, long long nnz, const doub
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long k = tid; k < nnz; k += nt) v[k] *= s[ci[k]];
 }
-// Row-block means (scaling.py:375-377, 409-413).  Every non-singleton
+// Row-block means (scaling.py:74-76, 409-413).  Every non-singleton
 // cone block is a segment with a global id; each shard sums the row norms
 // of its part into seg_sum[gid] (all-reduced when sharded), the mean is
 // seg_sum / global length.  Singleton (zero/nonneg) rows keep their norm.
@@ -993,13 +968,13 @@ __global__ void k_norm2(const double* a, const double* b, long long n, int mode,
   }
   if (grid_sum_last<1>(red, part, counter) && threadIdx.x == 0) *out = red[0];
 }
-// out = (s * w) * x   (b_hat = sigma D b, c_hat = rho E c: scaling.py:429)
+// out = (s * w) * x   (b_hat = sigma D b, c_hat = rho E c: scaling.py:128)
 __global__ void k_scale_vec(const double* x, const double* w, double s, long long n, double* out) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long i = tid; i < n; i += nt) out[i] = s * w[i] * x[i];
 }
-// Warm start (scaling.py:433-438, solver.py:128-150)
+// Warm start (scaling.py:132-137, solver.py:128-150)
 __global__ void k_init_state(Vec V, const double* wx, const double* wy, const double* ws,
                              double sigma, double rho) {
   const long long n = V.n, m = V.m;
@@ -1037,6 +1012,15 @@ __global__ void k_point_pri(const double* ax, const double* D, const double* s, 
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long i = tid; i < m; i += nt) out[i] = ax[i] / D[i] + s[i] - b[i];
+}
+// A x from the kept product of the final state: A_hat (x / E) = A_hat u_x / (tau sigma)
+// (x = E (u_x / tau) / sigma, solver.py:262), likewise A_hat^T (y / D) = A_hat^T u_y / (tau rho)
+__global__ void k_prod_scale(const double* prod, const double* utau, double scal, long long n,
+                             double* out) {
+  const double ut = *utau;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) out[i] = prod[i] / ut / scal;
 }
 __global__ void k_point_dual(const double* aty, const double* E, const double* c, long long n,
                              double* out) {
@@ -1199,7 +1183,6 @@ struct scs_handle {
   int dev = 0;
   int sms = 148;
   cudaStream_t st = nullptr;
-  cudaGraphExec_t gexec = nullptr;
   std::string err;
   // sizes
   long long m = 0, n = 0, nnz = 0, m_glob = 0, row_lo = 0;
@@ -1212,11 +1195,6 @@ struct scs_handle {
   // matrices
   Csr A{}, At{};
   int LA = 32, LAt = 32;
-  // slab-tiled copies (tiled.cuh) and their launch shapes per NV
-  bool tiled_m[2] = {false, false};  // [A, A^T]
-  Tiled tA{}, tAt{};
-  int tsub[2][3] = {}, tsplit[2][3] = {};  // [matrix][NV]
-  double* Ptile = nullptr;
   // TMA-streamed tiles (stream.cuh): format per matrix, schedules [matrix][pair]
   bool stm_m[2] = {false, false};
   Stm sF[2] = {};
@@ -1228,8 +1206,6 @@ struct scs_handle {
   } ssch[2][2];
   double* Pstm = nullptr;
   unsigned long long stm_bytes[2] = {0, 0};
-  // row-banded CSR(A^T) (setup_bands): S*n rows, raw band partials
-  int nband = 1, LAb = 32;
   int recur_refresh = 20;  // opt-in recurrence: direct A x every k iterations
   int res_rec = 32;        // A u_x of the residual check by recurrence, direct every k (0: always direct)
   bool res_rec_at = true;  // ... and A^T u_y (SCS_RES_RECUR_AT=0: only A u_x)
@@ -1242,8 +1218,6 @@ struct scs_handle {
   long long n_long[2] = {0, 0};
   double* Psplit = nullptr;                // raw piece products (2 per piece)
   double* Minv = nullptr;  // opt-in PCG diagonal
-  Csr Ab{};
-  double* Praw = nullptr;
   size_t l2_persist = 0, l2_window_max = 0;  // L2 set-aside for gather vectors
   // cones
   Cones K{};
@@ -1281,6 +1255,20 @@ struct scs_handle {
   double setup_seconds = 0.0;
   long long launches = 0, launches_per_iter = 0;
   long long launched_iters = 0;
+  // iteration graph variants (build_graph): with the residual recurrences
+  // on, a non-refresh (gvar[0]) and a refresh (gvar[1]) iteration, each
+  // without the passes gated to the other kind; `variant` is the one being
+  // enqueued (0: every pass, gated on the device)
+  int variant = 0;
+  int R = 0;                            // refresh period (0: one variant)
+  cudaGraphExec_t gvar[2] = {nullptr, nullptr};
+  long long lpi_var[2] = {0, 0};
+  cudaGraphExec_t gloop = nullptr;      // device-side loop over the variants (one GPU)
+  long long* loop_arg = nullptr;        // pinned: the iteration budget of a loop launch
+  // V.Aux = A_hat u_x and V.Uy = A_hat^T u_y hold the products of the final
+  // state (set by do_finish; the extraction then needs no matrix pass)
+  bool prod_current = false;
+  cudaStream_t st_copy = nullptr;       // extraction D2H overlapped with the point residuals
   std::vector<DevBuf> bufs;
   int grid_full = 148 * 4;
 };
@@ -1335,6 +1323,11 @@ void d2h(scs_handle* h, T* dst, const T* src, size_t count) {
 int elem_grid(scs_handle* h, long long work) {
   long long g = (work + kBlock - 1) / kBlock;
   return (int)std::max<long long>(1, std::min<long long>(g, h->grid_full));
+}
+
+// a pass gated to the other kind of iteration than the variant being enqueued
+bool gated_off(const scs_handle* h, int rgate) {
+  return (h->variant == 1 && rgate > 0) || (h->variant == 2 && rgate < 0);
 }
 
 // lanes per row: about 8 nonzeros per lane (two predicated 4-load steps)
@@ -1394,26 +1387,6 @@ void launch_spmv(scs_handle* h, const Csr& M, int L, const Epi& epi) {
   h->launches++;
 }
 
-// Opt the tiled kernel into the device's full dynamic shared memory once
-// (a per-launch, size-dependent setting would race between handles).
-template <int NV, int STRIDE, class Epi>
-void set_tiled_smem(int dev, size_t bytes) {
-  static std::once_flag once;
-  static int optin = 0;
-  std::call_once(once, [&] {
-    int dev_optin = 0;
-    cudaDeviceGetAttribute(&dev_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_tiled<NV, STRIDE, Epi>);
-    optin = dev_optin - (int)fa.sharedSizeBytes;  // dynamic = opt-in minus static
-    if (cudaFuncSetAttribute(k_tiled<NV, STRIDE, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             optin) != cudaSuccess)
-      optin = 48 * 1024 - (int)fa.sharedSizeBytes;
-    cudaGetLastError();
-  });
-  if (bytes > (size_t)optin) throw Fail{SCS_EINVAL, "tiled SpMV: shared memory budget exceeded"};
-}
-
 // Streamed-tile SpMV (stream.cuh).  NV = 1 passes run pair units (two
 // sub-blocks share every slab load), NV = 2 passes single sub-blocks; the
 // shared-memory ring gets as many 'cap'-byte stages (<= 4) as fit beside
@@ -1443,15 +1416,16 @@ void launch_stream(scs_handle* h, int mat, const Epi& epi) {
   CK(cudaGetLastError());
   h->launches++;
   if (S.splits > 1) {
-    k_tiled_combine<Epi><<<elem_grid(h, F.rows), kBlock, 0, h->st>>>(h->Pstm, S.splits, F.rows, epi);
+    k_split_combine<Epi><<<elem_grid(h, F.rows), kBlock, 0, h->st>>>(h->Pstm, S.splits, F.rows, epi);
     h->launches++;
   }
 }
 
-// SpMV with the matrix A (mat = 0) or A^T (mat = 1): streamed tiles, slab-
-// tiled kernel or CSR kernel, as chosen at setup.
+// SpMV with the matrix A (mat = 0) or A^T (mat = 1): streamed tiles or the
+// CSR kernel, as chosen at setup.
 template <class Epi>
 void launch_mat(scs_handle* h, int mat, const Epi& epi) {
+  if (gated_off(h, epi.rgate)) return;
   if (h->stm_m[mat] && ((uintptr_t)epi.xb & 15) == 0) {
     launch_stream<Epi::NV, Epi::STRIDE, Epi>(h, mat, epi);
     return;
@@ -1471,54 +1445,8 @@ void launch_mat(scs_handle* h, int mat, const Epi& epi) {
     h->launches++;
     return;
   }
-  if (!h->tiled_m[mat]) {
-    if (mat == 0) launch_spmv(h, h->A, h->LA, epi);
-    else launch_spmv(h, h->At, h->LAt, epi);
-    return;
-  }
-  constexpr int NV = Epi::NV, STRIDE = Epi::STRIDE;
-  const Tiled& T = mat == 0 ? h->tA : h->tAt;
-  const int sub = h->tsub[mat][NV], splits = h->tsplit[mat][NV];
-  const int splits_ = h->tsplit[mat][NV];
-  const size_t smem = 2 * (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8 +
-                      2 * (size_t)((T.S + splits_ - 1) / splits_ + 1);
-  set_tiled_smem<NV, STRIDE, Epi>(h->dev, smem);
-  const int ctas = T.NB * sub * splits;
-  k_tiled<NV, STRIDE, Epi><<<ctas, kTileThreads, smem, h->st>>>(T, epi, sub, splits, h->Ptile);
-  CK(cudaGetLastError());
-  h->launches++;
-  if (splits > 1) {
-    k_tiled_combine<Epi><<<elem_grid(h, T.rows), kBlock, 0, h->st>>>(h->Ptile, splits, T.rows, epi);
-    h->launches++;
-  }
-}
-
-// Pick (row sub-blocks per CTA, slab splits) for a tiled matrix and NV:
-// smem budget, then a two-level bandwidth model (DRAM: matrix stream and
-// split partials; L2: + slab staging) with wave quantisation on the SMs.
-void tile_shapes(scs_handle* h, int mat, const Tiled& T, long long nnz) {
-  for (int NV = 1; NV <= 2; ++NV) {
-    double best = 1e300;
-    for (int sub = 1; sub <= kTileNsub; sub *= 2) {
-      for (int splits = 1; splits <= 64 && splits <= T.S; splits *= 2) {
-        const size_t smem = 2 * (size_t)T.W * NV * 8 + (size_t)(T.RB / sub) * NV * 8 +
-                            2 * (size_t)((T.S + splits - 1) / splits + 1);
-        if (smem > 200 * 1024) continue;
-        const double ctas = (double)T.NB * sub * splits;
-        const double stream = 12.0 * nnz + 8.0 * NV * T.rows;
-        const double slabs = (double)T.NB * sub * T.cols * NV * 8.0;
-        const double part = splits > 1 ? 16.0 * splits * T.rows * NV : 0.0;
-        const double waves = std::ceil(ctas / h->sms);
-        const double eff = ctas / (h->sms * waves);
-        const double t = std::max((stream + part) / 5.5e12, (stream + slabs + part) / 12e12) / eff;
-        if (t < best * 0.97) {
-          best = t;
-          h->tsub[mat][NV] = sub;
-          h->tsplit[mat][NV] = splits;
-        }
-      }
-    }
-  }
+  if (mat == 0) launch_spmv(h, h->A, h->LA, epi);
+  else launch_spmv(h, h->At, h->LAt, epi);
 }
 
 template <class T>
@@ -1530,173 +1458,13 @@ void exclusive_scan(scs_handle* h, const T* in, T* out, long long n) {
   CK(cudaStreamSynchronize(h->st));
   dfree(h, tmp);
 }
+
 template <class T>
 T read_dev(scs_handle* h, const T* p) {
   T v{};
   CK(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   return v;
-}
-__global__ void k_key_hi(const unsigned long long* k2, long long n, int* out) {
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nt = (long long)gridDim.x * blockDim.x;
-  for (long long i = tid; i < n; i += nt) out[i] = (int)(k2[i] >> 20);
-}
-
-// Re-lay a CSR matrix out as slab tiles with SELL-style sub-tiles
-// (tiled.cuh): entries sorted by sub-tile (stable radix sort keeps the
-// row-major order), row segments found, segments sorted by (sub-tile,
-// length desc), grouped 32 per chunk and scattered column-interleaved.
-void build_tiled(scs_handle* h, const Csr& M, long long cols, Tiled& T) {
-  const long long rows = M.rows;
-  const long long nz = read_dev(h, M.rp + rows);
-  T.rows = rows;
-  T.cols = cols;
-  T.RB = 16384;
-  T.W = 4096;
-  T.S = (int)((cols + T.W - 1) / T.W);
-  T.NB = (int)((rows + T.RB - 1) / T.RB);
-  const long long ntile = (long long)T.NB * T.S * kTileNsub;
-  if (ntile >= (1LL << 31) - 1 || nz >= (1LL << 31) - 1)
-    throw Fail{SCS_EINVAL, "tiled layout: too many tiles or nonzeros"};
-  // 1. entries by sub-tile
-  int* rowid = dalloc<int>(h, nz);
-  int* key = dalloc<int>(h, nz);
-  int* skey = dalloc<int>(h, nz);
-  int* perm_in = dalloc<int>(h, nz);
-  int* perm = dalloc<int>(h, nz);
-  k_expand_rows<<<elem_grid(h, rows * 32), kBlock, 0, h->st>>>(M.rp, rows, rowid);
-  k_tile_keys<<<elem_grid(h, nz), kBlock, 0, h->st>>>(rowid, M.ci, nz, T.RB, T.W, T.S, key);
-  k_iota<<<elem_grid(h, nz), kBlock, 0, h->st>>>(perm_in, nz);
-  int bits = 1;
-  while ((1LL << bits) < ntile) ++bits;
-  {
-    size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const int*)key, skey, (const int*)perm_in, perm,
-                                       (int)nz, 0, bits, h->st));
-    void* tmp = dalloc<char>(h, tb);
-    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, (const int*)key, skey, (const int*)perm_in, perm,
-                                       (int)nz, 0, bits, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    dfree(h, tmp);
-  }
-  dfree(h, key);
-  // 2. row segments
-  int* flag = perm_in;  // reuse
-  int* incl = dalloc<int>(h, nz);
-  k_seg_flags<<<elem_grid(h, nz), kBlock, 0, h->st>>>(skey, perm, rowid, nz, flag);
-  {
-    size_t tb = 0;
-    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flag, incl, (int)nz, h->st));
-    void* tmp = dalloc<char>(h, tb);
-    CK(cub::DeviceScan::InclusiveSum(tmp, tb, flag, incl, (int)nz, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    dfree(h, tmp);
-  }
-  const long long nseg = read_dev(h, incl + nz - 1);
-  long long* seg_start = dalloc<long long>(h, nseg);
-  k_seg_starts<<<elem_grid(h, nz), kBlock, 0, h->st>>>(flag, incl, nz, seg_start);
-  dfree(h, incl);
-  // 3. segments by (sub-tile, length desc)
-  unsigned long long* key2 = dalloc<unsigned long long>(h, nseg);
-  unsigned long long* key2s = dalloc<unsigned long long>(h, nseg);
-  int* tile_of = dalloc<int>(h, nseg);
-  int* sidx = dalloc<int>(h, nseg);
-  int* order = dalloc<int>(h, nseg);
-  k_seg_keys<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(seg_start, nseg, nz, skey, key2, tile_of);
-  k_iota<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(sidx, nseg);
-  {
-    size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned long long*)key2, key2s,
-                                       (const int*)sidx, order, (int)nseg, 0, 20 + bits, h->st));
-    void* tmp = dalloc<char>(h, tb);
-    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, (const unsigned long long*)key2, key2s,
-                                       (const int*)sidx, order, (int)nseg, 0, 20 + bits, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    dfree(h, tmp);
-  }
-  int* tile_sorted = tile_of;  // reuse
-  k_key_hi<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(key2s, nseg, tile_sorted);
-  dfree(h, key2);
-  dfree(h, key2s);
-  dfree(h, sidx);
-  // 4. chunks
-  long long* tss = dalloc<long long>(h, ntile + 1);
-  long long* nch = dalloc<long long>(h, ntile + 1);
-  long long* cs = dalloc<long long>(h, ntile + 1);
-  k_rowptr<<<elem_grid(h, ntile + 1), kBlock, 0, h->st>>>(tile_sorted, nseg, ntile, tss);
-  k_tile_chunks<<<elem_grid(h, ntile), kBlock, 0, h->st>>>(tss, ntile, nch);
-  CK(cudaMemsetAsync(nch + ntile, 0, sizeof(long long), h->st));
-  exclusive_scan(h, nch, cs, ntile + 1);
-  const long long nchunk = read_dev(h, cs + ntile);
-  long long* csz = dalloc<long long>(h, nchunk + 1);
-  long long* co = dalloc<long long>(h, nchunk + 1);
-  k_chunk_sizes<<<elem_grid(h, ntile), kBlock, 0, h->st>>>(tss, cs, ntile, order, seg_start, nseg,
-                                                            nz, csz);
-  CK(cudaMemsetAsync(csz + nchunk, 0, sizeof(long long), h->st));
-  exclusive_scan(h, csz, co, nchunk + 1);
-  const long long nent = read_dev(h, co + nchunk);
-  // 5. scatter
-  unsigned short* rid = dalloc<unsigned short>(h, nchunk * 32);
-  unsigned short* col = dalloc<unsigned short>(h, nent);
-  double* tv = dalloc<double>(h, nent);
-  k_fill_u16<<<elem_grid(h, nchunk * 32), kBlock, 0, h->st>>>(rid, nchunk * 32, 0xffff);
-  k_fill_u16<<<elem_grid(h, nent), kBlock, 0, h->st>>>(col, nent, 0);
-  CK(cudaMemsetAsync(tv, 0, std::max<long long>(nent, 1) * sizeof(double), h->st));
-  k_sell_scatter<<<elem_grid(h, nseg), kBlock, 0, h->st>>>(tss, cs, co, order, tile_sorted, seg_start,
-                                                           nseg, nz, perm, rowid, M.ci, M.v, T.RB,
-                                                           T.W, rid, col, tv);
-  CK(cudaStreamSynchronize(h->st));
-  dfree(h, csz);
-  dfree(h, nch);
-  dfree(h, tss);
-  dfree(h, order);
-  dfree(h, tile_sorted);
-  dfree(h, seg_start);
-  dfree(h, perm_in);
-  dfree(h, perm);
-  dfree(h, skey);
-  dfree(h, rowid);
-  T.cs = cs;
-  T.co = co;
-  T.rid = rid;
-  T.col = col;
-  T.v = tv;
-  dbg("tiled layout rows=%lld cols=%lld nnz=%lld segments=%lld chunks=%lld entries=%lld (pad %.1f%%)",
-      rows, cols, nz, nseg, nchunk, nent, nz ? 100.0 * (nent - nz) / nz : 0.0);
-}
-
-// Tiling pays when a row meets a slab often enough: the expected row
-// segment per (row, slab) tile, nnz/row * W/cols, must be a few entries;
-// for very wide matrices with short rows (config 5) the per-slab CTA
-// synchronisation outweighs the gather savings and the CSR kernel stays.
-void setup_tiled(scs_handle* h) {
-  const char* env = getenv("SCS_TILED");
-  const int force = env ? atoi(env) : -1;  // 0 off, 1 on, unset: heuristic
-  if (force == 0 || h->nnz == 0) return;
-  const double W = 4096.0;
-  for (int mat = 0; mat < 2; ++mat) {
-    const double rows = mat == 0 ? h->m : h->n, cols = mat == 0 ? h->n : h->m;
-    const double seg = (double)h->nnz / std::max(rows, 1.0) * std::min(1.0, W / std::max(cols, 1.0));
-    const bool want = force == 1 || (h->nnz >= 4000000LL && seg >= 3.0);
-    if (!want || h->stm_m[mat]) continue;
-    Tiled& T = mat == 0 ? h->tA : h->tAt;
-    build_tiled(h, mat == 0 ? h->A : h->At, mat == 0 ? h->n : h->m, T);
-    tile_shapes(h, mat, T, h->nnz);
-    h->tiled_m[mat] = true;
-  }
-  size_t need = 0;
-  for (int mat = 0; mat < 2; ++mat)
-    for (int NV = 1; NV <= 2; ++NV) {
-      const Tiled& T = mat == 0 ? h->tA : h->tAt;
-      if (h->tiled_m[mat] && h->tsplit[mat][NV] > 1)
-        need = std::max<size_t>(need, (size_t)h->tsplit[mat][NV] * (size_t)T.rows * NV);
-    }
-  if (need) h->Ptile = dalloc<double>(h, need);
-  dbg("tiled: A=%d (NB=%d S=%d nv1=(%d,%d) nv2=(%d,%d)) At=%d (NB=%d S=%d nv1=(%d,%d) nv2=(%d,%d))",
-      (int)h->tiled_m[0], h->tA.NB, h->tA.S, h->tsub[0][1], h->tsplit[0][1], h->tsub[0][2],
-      h->tsplit[0][2], (int)h->tiled_m[1], h->tAt.NB, h->tAt.S, h->tsub[1][1], h->tsplit[1][1],
-      h->tsub[1][2], h->tsplit[1][2]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1739,7 +1507,7 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T) {
   const int G0 = h->sms;
   int splits = 1;
   // splits: the split count minimising (LPT makespan bound) + (split
-  // partial rows written and read back by k_tiled_combine, + a launch)
+  // partial rows written and read back by k_split_combine, + a launch)
   if (ntiled > 0) {
     double bytes = 0.0;
     for (long long t = 0; t < (long long)T.NB * T.S; ++t) bytes += 10.0 * (double)T.slots[t];
@@ -2134,8 +1902,7 @@ __global__ void k_pcg_diag(const double* colsq, long long n, double* out) {
 }
 
 // Opt-in Jacobi PCG: M^-1 = 1 / (1 + ||A_hat e_j||^2) from the equilibrated
-// CSR(A^T) (column sums all-reduced when rows are sharded); before
-// setup_bands, which drops the unbanded copy.
+// CSR(A^T) (column sums all-reduced when rows are sharded).
 void setup_pcg(scs_handle* h) {
   if (!(h->set.fast & SCS_FAST_PCG)) return;
   const long long n = h->n;
@@ -2145,54 +1912,6 @@ void setup_pcg(scs_handle* h) {
   k_pcg_diag<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->tmp_n, n, h->Minv);
   CK(cudaStreamSynchronize(h->st));
   h->V.Minv = h->Minv;
-}
-
-// L2 blocking of the A^T passes.  Their gathered vectors (q: 8m bytes, the
-// first pass's interleaved Y2: 16m) exceed the 126 MB L2 at config 5
-// (m = 1e7), so random gathers miss to DRAM (ncu: 20-43 GB read per pass for
-// 12 GB of matrix).  Splitting A's rows into S bands of <= 32 MB of Y2 and
-// streaming CSR(A^T) band by band (row s*n + j = column j restricted to band
-// s) keeps every band's slice L2-resident; the partial products per band are
-// summed by the epilogue kernel.  Used when 16m > 64 MB and A^T is not
-// slab-tiled; SCS_BANDS=k forces k bands (1 = off).
-void setup_bands(scs_handle* h) {
-  if (h->tiled_m[1] || h->stm_m[1] || h->nnz == 0 || h->m < 2) return;
-  const char* env = getenv("SCS_BANDS");
-  long long S = env ? atoll(env) : -1;
-  if (S < 0) {
-    const double y2 = 16.0 * (double)h->m, budget = 32.0 * (1 << 20);
-    S = (y2 > 2 * budget && h->nnz >= 50000000LL) ? (long long)std::ceil(y2 / budget) : 1;
-  }
-  S = std::min<long long>(std::min<long long>(S, 32), h->m);
-  if (S <= 1) return;
-  const long long n = h->n, nnz = h->nnz;
-  const int band_rows = (int)((h->m + S - 1) / S);
-  S = (h->m + band_rows - 1) / band_rows;
-  if (S * n >= (1LL << 31) - 1) return;
-  long long* cnt = dalloc<long long>(h, S * n + 1);
-  long long* rpb = dalloc<long long>(h, S * n + 1);
-  CK(cudaMemsetAsync(cnt, 0, (S * n + 1) * sizeof(long long), h->st));
-  const int grid = elem_grid(h, n * 32);
-  k_band_pass<<<grid, kBlock, 0, h->st>>>(h->At, band_rows, (int)S, n, nullptr, cnt, nullptr, nullptr);
-  CK(cudaGetLastError());
-  exclusive_scan(h, cnt, rpb, S * n + 1);
-  dfree(h, cnt);
-  int* ci2 = dalloc<int>(h, nnz);
-  double* v2 = dalloc<double>(h, nnz);
-  k_band_pass<<<grid, kBlock, 0, h->st>>>(h->At, band_rows, (int)S, n, rpb, nullptr, ci2, v2);
-  CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(h->st));
-  // the unbanded copy is not used after setup
-  dfree(h, (void*)h->At.ci);
-  dfree(h, (void*)h->At.v);
-  h->At.ci = nullptr;
-  h->At.v = nullptr;
-  h->Ab = Csr{rpb, ci2, v2, S * n};
-  h->nband = (int)S;
-  h->LAb = pick_lanes(nnz, S * n);
-  if (const char* e = getenv("SCS_LANES_AT")) h->LAb = atoi(e);
-  h->Praw = dalloc<double>(h, 2 * S * n);
-  dbg("bands: S=%lld band_rows=%d LAb=%d", S, band_rows, h->LAb);
 }
 
 // Skewed rows (SURVEY §7 hard part 1): a CSR kernel with L lanes per row
@@ -2210,7 +1929,7 @@ void setup_split(scs_handle* h) {
   if (force == 0 || h->nnz == 0) return;
   size_t need = 0;
   for (int mat = 0; mat < 2; ++mat) {
-    if (h->tiled_m[mat] || h->stm_m[mat] || (mat == 1 && h->nband > 1)) continue;
+    if (h->stm_m[mat]) continue;
     const Csr& M = mat == 0 ? h->A : h->At;
     const long long rows = M.rows;
     std::vector<long long> rp(rows + 1);
@@ -2261,6 +1980,7 @@ void setup_split(scs_handle* h) {
 // all-reduced and finished by k_finish.
 template <class Epi>
 void a_pass(scs_handle* h, Epi epi) {
+  if (gated_off(h, epi.rgate)) return;
   epi.defer = (h->sharded && Epi::NR > 0) ? 1 : 0;
   launch_mat(h, 0, epi);
   if (epi.defer) {
@@ -2273,38 +1993,21 @@ void a_pass(scs_handle* h, Epi epi) {
 // A^T pass.  Row-sharded: raw partial products of the local rows, one
 // all-reduce of NV n-vectors, then the epilogue on the reduced products
 // (its reductions are over replicated x-space data: no further all-reduce).
-// Row-banded (setup_bands): raw products per band, the epilogue kernel sums
-// the band partials in band order.
 template <class Epi>
 void at_pass(scs_handle* h, Epi epi) {
+  if (gated_off(h, epi.rgate)) return;
   epi.defer = 0;
-  const bool banded = h->nband > 1;
-  if (!h->sharded && !banded) {
+  if (!h->sharded) {
     launch_mat(h, 1, epi);
     return;
   }
   const long long n = h->n;
   EpiRaw<Epi> raw{};
   static_cast<Epi&>(raw) = epi;
-  const double* T = h->Traw;
-  int nsum = 1;
-  if (banded) {
-    raw.T = h->Praw;
-    launch_spmv(h, h->Ab, h->LAb, raw);
-    if (h->sharded) {
-      k_band_sum<<<elem_grid(h, n * Epi::NV), kBlock, 0, h->st>>>(h->Praw, n * Epi::NV, h->nband,
-                                                                  h->Traw);
-      h->launches++;
-    } else {
-      T = h->Praw;
-      nsum = h->nband;
-    }
-  } else {
-    raw.T = h->Traw;
-    launch_mat(h, 1, raw);
-  }
+  raw.T = h->Traw;
+  launch_mat(h, 1, raw);
   allreduce(h, h->Traw, (size_t)n * Epi::NV);
-  k_rows<Epi><<<elem_grid(h, n), kBlock, 0, h->st>>>(T, n, nsum, epi);
+  k_rows<Epi><<<elem_grid(h, n), kBlock, 0, h->st>>>(h->Traw, n, 1, epi);
   h->launches++;
 }
 
@@ -2312,6 +2015,7 @@ void at_pass(scs_handle* h, Epi epi) {
 // its y-part totals are all-reduced when rows are sharded.
 template <class Epi>
 void y_rows(scs_handle* h, const double* T, Epi epi) {
+  if (gated_off(h, epi.rgate)) return;
   epi.defer = (h->sharded && Epi::NR > 0) ? 1 : 0;
   k_rows<Epi><<<elem_grid(h, h->m), kBlock, 0, h->st>>>(T, h->m, 1, epi);
   h->launches++;
@@ -2325,7 +2029,7 @@ void y_rows(scs_handle* h, const double* T, Epi epi) {
 // final A pass of solve_kkt: z_y = rhs_y + A x (embedding.py:113)
 void a_final(scs_handle* h, const Vec& V, double* zy_out, int setup) {
   const bool recur = !setup && (h->set.fast & SCS_FAST_RECURRENCE);
-  if (!(h->tiled_m[0] || h->stm_m[0]) || recur) {
+  if (!h->stm_m[0] || recur) {
     EpiAxPlain ax{};
     ax.V = V;
     ax.xb = V.x;
@@ -2719,7 +2423,7 @@ void push_ctl(scs_handle* h) {
   CK(cudaStreamSynchronize(h->st));
 }
 
-// sigma, rho, b_hat, c_hat and the residual constants (scaling.py:422-429,
+// sigma, rho, b_hat, c_hat and the residual constants (scaling.py:121-128,
 // 469-478)
 void scale_vectors(scs_handle* h) {
   const long long m = h->m, n = h->n;
@@ -2753,6 +2457,8 @@ void check_err(scs_handle* h) {
     throw Fail{SCS_ENONFINITE, "cg_solve: operator is not positive definite on iterates"};
   if (e & ERR_CG_NONFINITE) throw Fail{SCS_ENONFINITE, "cg_solve: non-finite residual"};
   if (e & ERR_CONE_NONFINITE) throw Fail{SCS_ENONFINITE, "project_embedding_cone: non-finite input"};
+  if (e & ERR_SCHED)
+    throw Fail{SCS_ECUDA, "internal: iteration graph variant does not match the refresh schedule"};
   if (e & ERR_JACOBI) {
     if (h->V.dbg) {
       const int cap = 2 + h->K.max_side * (h->K.max_side + 1) / 2;
@@ -2774,7 +2480,7 @@ void cg_step(scs_handle* h, const Vec& V, long long cap, bool with_p, bool merge
   // iterations only (and stores A u_x); the others check from Aux and run
   // a plain A p pass
   const int R = (merged && V.Agx) ? h->res_rec : 0;
-  if (merged && !(h->tiled_m[0] || h->stm_m[0])) {  // CSR: plain SpMV + elementwise residual pass
+  if (merged && !h->stm_m[0]) {  // CSR: plain SpMV + elementwise residual pass
     EpiApPlain2 ea{};
     ea.V = V;
     ea.xb = V.X2;
@@ -2890,11 +2596,12 @@ void launch_cone_apply(scs_handle* h, const Vec& V);
 // between kernels when rows are sharded)
 void enqueue_iteration(scs_handle* h) {
   const Vec V = h->V;
-  k_prep<<<elem_grid(h, h->n + h->m), kBlock, 0, h->st>>>(V, h->sharded ? 1 : 0);
+  k_prep<<<elem_grid(h, h->n + h->m), kBlock, 0, h->st>>>(V, h->sharded ? 1 : 0, h->variant,
+                                                          std::max(h->R, 1));
   h->launches++;
   if (h->sharded) {
     allreduce(h, V.dred, 1);
-    k_prep_finish<<<1, 32, 0, h->st>>>(V);
+    k_prep_finish<<<1, 32, 0, h->st>>>(V, h->variant, std::max(h->R, 1));
     h->launches++;
   }
   const int RA = V.T ? h->res_rec : 0;  // A^T-side residual recurrence
@@ -2910,12 +2617,12 @@ void enqueue_iteration(scs_handle* h) {
   e0.xb = V.Y2;
   e0.rgate = RA;
   at_pass(h, e0);
-  if (RA) {
+  if (RA && !gated_off(h, -RA)) {
     EpiAtFirst1 e1{};
     e1.V = V;
     e1.xb = V.Yc;
     e1.rgate = -RA;
-    if (!h->sharded && h->nband <= 1) {  // products into Sv, then the epilogue coalesced
+    if (!h->sharded) {  // products into Sv, then the epilogue coalesced
       EpiStoreF sf{};
       sf.V = V;
       sf.xb = V.Yc;
@@ -2977,45 +2684,200 @@ void launch_cone_apply(scs_handle* h, const Vec& V) {
   }
 }
 
-// capture one ADMM iteration into a CUDA graph (NCCL calls are capturable;
-// the emulated group is not, and runs the sequence directly)
-void build_graph(scs_handle* h) {
-  if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+// Capture one ADMM iteration of the given variant into a CUDA graph (NCCL
+// calls are capturable; the emulated group is not, and runs the sequence
+// directly).
+cudaGraphExec_t capture_iteration(scs_handle* h, int variant, long long* lpi) {
   const long long before = h->launches;
-  if (!h->use_graph) {
-    // count launches with a dry count (no capture)
-    h->launches_per_iter = 0;
-    return;
-  }
+  h->variant = variant;
   CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
   enqueue_iteration(h);
   cudaGraph_t g;
   CK(cudaStreamEndCapture(h->st, &g));
-  CK(cudaGraphInstantiate(&h->gexec, g, 0));
+  h->variant = 0;
+  cudaGraphExec_t ex;
+  CK(cudaGraphInstantiate(&ex, g, 0));
   cudaGraphDestroy(g);
-  h->launches_per_iter = h->launches - before;
+  *lpi = h->launches - before;
+  h->launches = before;
+  return ex;
 }
 
+__global__ void k_loop_arm(Ctl* c, cudaGraphConditionalHandle wh) {
+  c->loop_done = 0;
+  c->loop_refresh = 0;
+  cudaGraphSetConditional(wh, (c->loop_left > 0 && !c->stop) ? 1u : 0u);
+}
+
+// One GPU: the whole loop as one graph --
+//   [k_loop_arm] -> WHILE { [k_loop_pick] -> SWITCH { non-refresh iteration,
+//                                                     refresh iteration }
+//                           -> [k_loop_next] }
+// (no SWITCH when the residual recurrences are off).  The host writes the
+// iteration budget into Ctl.loop_left (8-byte copy) before each launch.
+// Returns false (and leaves gloop unset) if the driver rejects the graph.
+bool build_loop_graph(scs_handle* h) {
+  const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
+  cudaGraph_t g = nullptr;
+  CK(cudaGraphCreate(&g, 0));
+  auto fail = [&](const char* what, cudaError_t e) {
+    dbg("loop graph: %s failed: %s", what, cudaGetErrorString(e));
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(h->st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(h->st, &junk);
+      if (junk) cudaGraphDestroy(junk);
+    }
+    cudaGetLastError();
+    h->variant = 0;
+    cudaGraphDestroy(g);
+    return false;
+  };
+  cudaError_t e;
+  cudaGraphConditionalHandle wh;
+  if ((e = cudaGraphConditionalHandleCreate(&wh, g, 0, 0)) != cudaSuccess) return fail("handle", e);
+  if ((e = cudaStreamBeginCaptureToGraph(h->st, g, nullptr, nullptr, 0, mode)) != cudaSuccess)
+    return fail("capture arm", e);
+  k_loop_arm<<<1, 1, 0, h->st>>>(h->ctl, wh);
+  if ((e = cudaStreamEndCapture(h->st, &g)) != cudaSuccess) return fail("end arm", e);
+  cudaGraphNode_t arm = nullptr;
+  size_t nn = 1;
+  if ((e = cudaGraphGetNodes(g, &arm, &nn)) != cudaSuccess || nn != 1) return fail("arm node", e);
+  cudaGraphNodeParams wp{};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = wh;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  if ((e = cudaGraphAddNode(&wnode, g, &arm, 1, &wp)) != cudaSuccess) return fail("while", e);
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  cudaGraphNode_t last = nullptr;
+  long long tmp = 0;
+  const long long before = h->launches;
+  if (h->R > 0) {
+    cudaGraphConditionalHandle sh;
+    if ((e = cudaGraphConditionalHandleCreate(&sh, body, 0, 0)) != cudaSuccess)
+      return fail("switch handle", e);
+    if ((e = cudaStreamBeginCaptureToGraph(h->st, body, nullptr, nullptr, 0, mode)) != cudaSuccess)
+      return fail("capture pick", e);
+    k_loop_pick<<<1, 1, 0, h->st>>>(h->ctl, sh, h->R);
+    if ((e = cudaStreamEndCapture(h->st, &body)) != cudaSuccess) return fail("end pick", e);
+    cudaGraphNode_t pick = nullptr;
+    nn = 1;
+    if ((e = cudaGraphGetNodes(body, &pick, &nn)) != cudaSuccess || nn != 1)
+      return fail("pick node", e);
+    cudaGraphNodeParams sp{};
+    sp.type = cudaGraphNodeTypeConditional;
+    sp.conditional.handle = sh;
+    sp.conditional.type = cudaGraphCondTypeSwitch;
+    sp.conditional.size = 2;
+    if ((e = cudaGraphAddNode(&last, body, &pick, 1, &sp)) != cudaSuccess) return fail("switch", e);
+    for (int b = 0; b < 2; ++b) {
+      cudaGraph_t br = sp.conditional.phGraph_out[b];
+      if ((e = cudaStreamBeginCaptureToGraph(h->st, br, nullptr, nullptr, 0, mode)) != cudaSuccess)
+        return fail("capture branch", e);
+      h->variant = b ? 2 : 1;
+      enqueue_iteration(h);
+      h->variant = 0;
+      if ((e = cudaStreamEndCapture(h->st, &br)) != cudaSuccess) return fail("end branch", e);
+    }
+    if ((e = cudaStreamBeginCaptureToGraph(h->st, body, &last, nullptr, 1, mode)) != cudaSuccess)
+      return fail("capture next", e);
+  } else {
+    if ((e = cudaStreamBeginCaptureToGraph(h->st, body, nullptr, nullptr, 0, mode)) != cudaSuccess)
+      return fail("capture body", e);
+    enqueue_iteration(h);
+  }
+  k_loop_next<<<1, 1, 0, h->st>>>(h->ctl, wh);
+  if ((e = cudaStreamEndCapture(h->st, &body)) != cudaSuccess) return fail("end body", e);
+  (void)tmp;
+  h->launches = before;
+  cudaGraphExec_t ex = nullptr;
+  if ((e = cudaGraphInstantiate(&ex, g, 0)) != cudaSuccess) return fail("instantiate", e);
+  cudaGraphDestroy(g);
+  h->gloop = ex;
+  return true;
+}
+
+void destroy_graphs(scs_handle* h) {
+  for (auto* ex : {&h->gvar[0], &h->gvar[1], &h->gloop})
+    if (*ex) { cudaGraphExecDestroy(*ex); *ex = nullptr; }
+}
+
+// The iteration graphs: with the residual recurrences on, one graph per
+// variant (refresh iterations k_sched = 1, 1 + R, ... carry the direct
+// residual passes, the others the recurrence passes), so no gated-off pass
+// is launched (and, row-sharded, no all-reduce of a gated-off pass runs).
+// On one GPU, also the device-side loop over them (build_loop_graph).
+void build_graph(scs_handle* h) {
+  destroy_graphs(h);
+  h->R = (h->V.Agx || h->V.T) ? h->res_rec : 0;
+  if (!h->use_graph) {
+    h->launches_per_iter = 0;
+    return;
+  }
+  if (h->R > 0) {
+    h->gvar[0] = capture_iteration(h, 1, &h->lpi_var[0]);
+    h->gvar[1] = capture_iteration(h, 2, &h->lpi_var[1]);
+  } else {
+    h->gvar[0] = capture_iteration(h, 0, &h->lpi_var[0]);
+    h->lpi_var[1] = h->lpi_var[0];
+  }
+  h->launches_per_iter = h->lpi_var[0];
+  if (!h->sharded && env_ll("SCS_LOOP_GRAPH", 1)) build_loop_graph(h);
+  dbg("graphs: R=%d launches/iter %lld (refresh %lld), loop graph %d", h->R, h->lpi_var[0],
+      h->lpi_var[1], h->gloop != nullptr);
+}
+
+// One iteration from the host: the variant follows the refresh schedule,
+// predicted from the iterations launched since scs_begin (k_sched before
+// this iteration; k_prep verifies the prediction on the device).
 void run_iteration(scs_handle* h) {
+  const int refresh = (h->R > 0 && h->launched_iters % h->R == 0) ? 1 : 0;
   if (h->use_graph) {
-    CK(cudaGraphLaunch(h->gexec, h->st));
-    h->launches += h->launches_per_iter;
+    CK(cudaGraphLaunch(h->gvar[h->R > 0 ? refresh : 0], h->st));
+    h->launches += h->lpi_var[refresh];
   } else {
     const long long before = h->launches;
+    h->variant = h->R > 0 ? 1 + refresh : 0;
     enqueue_iteration(h);
+    h->variant = 0;
     h->launches_per_iter = h->launches - before;
   }
+  h->launched_iters++;
+}
+
+// Up to k iterations as one launch of the loop graph (stops on the device
+// at termination or error); returns after the graph is enqueued.
+void enqueue_loop(scs_handle* h, long long k) {
+  *h->loop_arg = k;
+  CK(cudaMemcpyAsync(&h->ctl->loop_left, h->loop_arg, sizeof(long long), cudaMemcpyHostToDevice,
+                     h->st));
+  CK(cudaGraphLaunch(h->gloop, h->st));
+}
+
+// bookkeeping after a loop launch (Ctl pulled)
+void account_loop(scs_handle* h) {
+  const Ctl* c = h->ctl_h;
+  const long long done = c->loop_done, refr = c->loop_refresh;
+  h->launched_iters += done;
+  // the iterations' kernels, k_loop_next (+ k_loop_pick) per iteration, k_loop_arm
+  h->launches += (done - refr) * h->lpi_var[0] + refr * h->lpi_var[1] + done +
+                 (h->R > 0 ? done : 0) + 1;
 }
 
 // stand-alone termination check / residual evaluation of the current state
+// (the products are kept: A u_x in V.Aux, A^T u_y in V.Uy when allocated)
 void launch_residuals(scs_handle* h) {
   EpiResA ra{};
   ra.V = h->V;
   ra.xb = h->V.u;
+  ra.store = h->V.Aux;
   a_pass(h, ra);
   EpiResAt rt{};
   rt.V = h->V;
   rt.xb = h->V.u + h->n;
+  rt.store = h->V.Uy;
   at_pass(h, rt);
 }
 
@@ -3032,6 +2894,7 @@ void fill_info(scs_handle* h, scs_info* info) {
 
 void do_begin(scs_handle* h, const double* wx, const double* wy, const double* ws) {
   const long long n = h->n, m = h->m;
+  h->prod_current = false;
   double *dx = nullptr, *dy = nullptr, *ds = nullptr;
   if (wx) {
     dx = h->tmp_n;
@@ -3084,11 +2947,19 @@ void share_err(scs_handle* h) {
 void do_steps(scs_handle* h, long long k) {
   Ctl* c = h->ctl_h;
   long long todo = std::min(k, h->set.max_iters - h->launched_iters);
+  if (todo > 0 && h->gloop) {  // one launch, the loop runs on the device
+    enqueue_loop(h, todo);
+    pull_ctl(h);
+    account_loop(h);
+    dbg("loop: launched=%lld iter=%lld status=%d stop=%d err=%d", h->launched_iters, c->iter,
+        c->status, c->stop, c->err);
+    check_err(h);
+    return;
+  }
   long long batch = 1;
   while (todo > 0) {
     const long long b = std::min(batch, todo);
     for (long long i = 0; i < b; ++i) run_iteration(h);
-    h->launched_iters += b;
     todo -= b;
     share_err(h);
     pull_ctl(h);
@@ -3106,17 +2977,25 @@ void do_steps(scs_handle* h, long long k) {
 void do_finish(scs_handle* h) {
   Ctl* c = h->ctl_h;
   pull_ctl(h);
+  // V.Aux / V.Uy end up holding A_hat u_x / A_hat^T u_y of the final state:
+  // from the check that stopped the loop (direct on refresh iterations, else
+  // by the recurrences), or from launch_residuals below
+  h->prod_current = h->R > 0 && h->V.Uy != nullptr;
   if (c->status != SCS_RUNNING) return;
+  bool fresh = false;
   if (c->check_pending && !c->stop) {
     launch_residuals(h);
     pull_ctl(h);
     check_err(h);
     if (c->status != SCS_RUNNING) return;
+    fresh = true;  // Ctl.res already holds the final state's residuals
   }
-  c->force_check = 1;
-  c->stop = 0;
-  push_ctl(h);
-  launch_residuals(h);
+  if (!fresh) {  // post-loop residuals (solver.py:365) of a state that was not checked
+    c->force_check = 1;
+    c->stop = 0;
+    push_ctl(h);
+    launch_residuals(h);
+  }
   // tau > 1e-8 ||u|| ?  (x-part and tau replicated, y-part sharded)
   const long long n = h->n, m = h->m;
   const double un2 = norm2_dev(h, h->V.u, h->V.u, n, 2) +
@@ -3166,11 +3045,13 @@ const char* scs_last_error(const scs_handle* h) {
 void scs_destroy(scs_handle* h) {
   if (!h) return;
   cudaSetDevice(h->dev);
-  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  destroy_graphs(h);
   for (auto& b : h->bufs)
     if (b.p) cudaFree(b.p);
   if (h->ctl_h) cudaFreeHost(h->ctl_h);
+  if (h->loop_arg) cudaFreeHost(h->loop_arg);
   if (h->st) cudaStreamDestroy(h->st);
+  if (h->st_copy) cudaStreamDestroy(h->st_copy);
   delete h->comm;
   delete h;
 }
@@ -3224,6 +3105,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     h->grid_full = h->sms * (2048 / kBlock);
     if (h->grid_full > kMaxGrid) h->grid_full = kMaxGrid;
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->st_copy, cudaStreamNonBlocking));
     {
       // opt-in (SCS_L2_PERSIST=1): measured slower at config 5 -- the
       // set-aside shrinks the L2 left for everything else
@@ -3282,6 +3164,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
       throw Fail{SCS_EINVAL, "a row slice needs a scs_dist"};
     }
     CK(cudaMallocHost((void**)&h->ctl_h, sizeof(Ctl)));
+    CK(cudaMallocHost((void**)&h->loop_arg, sizeof(long long)));
     memset(h->ctl_h, 0, sizeof(Ctl));
     h->ctl = dalloc<Ctl>(h, 1);
     Ctl* c = h->ctl_h;
@@ -3327,6 +3210,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     V.Agx = h->res_rec > 0 ? dalloc<double>(h, m) : nullptr;
     if (h->res_rec > 0 && h->res_rec_at) {
       V.T = dalloc<double>(h, n);
+      V.AtAp = dalloc<double>(h, n);
       V.Sv = dalloc<double>(h, n);
       V.Uy = dalloc<double>(h, n);
       V.Dd = dalloc<double>(h, n);
@@ -3367,9 +3251,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     k_recip<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->E, n, (double*)V.Einv);
     dbg("equilibrated mean_col=%g mean_row=%g", h->mean_col, h->mean_row);
     setup_stream(h);
-    setup_tiled(h);
     setup_pcg(h);
-    setup_bands(h);
     setup_split(h);
     scale_vectors(h);
     dbg("scaled sigma=%g rho=%g", h->sigma, h->rho);
@@ -3479,25 +3361,36 @@ int scs_apply_a(scs_handle* h, int which, const double* in, double* out) {
 // dy, ds: m; dx is also read after the passes).  out = {pri, dual, gap,
 // c'x, b'y} (m-length sums all-reduced over row shards).
 void point_residuals_dev(scs_handle* h, const double* dx, const double* dy, const double* ds,
-                         double* out5) {
+                         double* out5, bool prod = false) {
   const long long n = h->n, m = h->m;
+  const double* utau = h->V.u + n + m;
   // A x = D^-1 A_hat E^-1 x ; A^T y = E^-1 A_hat^T D^-1 y  (rows may be sharded:
-  // m-length sums are all-reduced, A^T products go through at_pass)
-  k_div<<<elem_grid(h, n), kBlock, 0, h->st>>>(dx, h->E, n, h->V.r);
-  EpiPlain e{};
-  e.V = h->V;
-  e.xb = h->V.r;
-  e.out = h->tmp_m2;
-  a_pass(h, e);
+  // m-length sums are all-reduced, A^T products go through at_pass).  With
+  // `prod` (extraction of the final state), A_hat E^-1 x and A_hat^T D^-1 y
+  // come from the products the last check kept (V.Aux, V.Uy): no matrix pass.
+  if (prod) {
+    k_prod_scale<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->V.Aux, utau, h->sigma, m, h->tmp_m2);
+  } else {
+    k_div<<<elem_grid(h, n), kBlock, 0, h->st>>>(dx, h->E, n, h->V.r);
+    EpiPlain e{};
+    e.V = h->V;
+    e.xb = h->V.r;
+    e.out = h->tmp_m2;
+    a_pass(h, e);
+  }
   k_point_pri<<<elem_grid(h, m), kBlock, 0, h->st>>>(h->tmp_m2, h->D, ds, h->b0, m, h->V.q);
   const double pri = sqrt(norm2_dev(h, h->V.q, h->V.q, m, 2, true));
   const double bn = sqrt(norm2_dev(h, h->b0, h->b0, m, 2, true));
-  k_div<<<elem_grid(h, m), kBlock, 0, h->st>>>(dy, h->D, m, h->tmp_m2);
-  EpiPlain f{};
-  f.V = h->V;
-  f.xb = h->tmp_m2;
-  f.out = h->V.Gp;
-  at_pass(h, f);
+  if (prod) {
+    k_prod_scale<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->V.Uy, utau, h->rho, n, h->V.Gp);
+  } else {
+    k_div<<<elem_grid(h, m), kBlock, 0, h->st>>>(dy, h->D, m, h->tmp_m2);
+    EpiPlain f{};
+    f.V = h->V;
+    f.xb = h->tmp_m2;
+    f.out = h->V.Gp;
+    at_pass(h, f);
+  }
   k_point_dual<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->V.Gp, h->E, h->c0, n, h->V.r);
   const double dual = sqrt(norm2_dev(h, h->V.r, h->V.r, n, 2));
   const double cn = sqrt(norm2_dev(h, h->c0, h->c0, n, 2));
@@ -3557,11 +3450,21 @@ int scs_extract_point(scs_handle* h, double* x, double* y, double* s, double* ou
     double* dy = ext_y(h);
     k_extract<<<elem_grid(h, h->n + h->m), kBlock, 0, h->st>>>(h->V, h->D, h->E, h->sigma,
                                                                 h->rho, h->tmp_n, dy, h->tmp_m);
-    if (x) d2h(h, x, h->tmp_n, h->n);
-    if (y) d2h(h, y, dy, h->m);
-    if (s) d2h(h, s, h->tmp_m, h->m);
-    point_residuals_dev(h, h->tmp_n, dy, h->tmp_m, out5);
+    // the copies out run on a second stream, overlapped with the point
+    // residuals (at full link speed when the caller's buffers are pinned)
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, h->st));
+    CK(cudaStreamWaitEvent(h->st_copy, ev, 0));
+    const long long n = h->n, m = h->m;
+    if (x && n) CK(cudaMemcpyAsync(x, h->tmp_n, n * 8, cudaMemcpyDeviceToHost, h->st_copy));
+    if (y && m) CK(cudaMemcpyAsync(y, dy, m * 8, cudaMemcpyDeviceToHost, h->st_copy));
+    if (s && m) CK(cudaMemcpyAsync(s, h->tmp_m, m * 8, cudaMemcpyDeviceToHost, h->st_copy));
+    // (tmp_n, dy, tmp_m are only read by the point residuals below)
+    point_residuals_dev(h, h->tmp_n, dy, h->tmp_m, out5, h->prod_current);
     CK(cudaStreamSynchronize(h->st));
+    CK(cudaStreamSynchronize(h->st_copy));
+    cudaEventDestroy(ev);
   });
 }
 
@@ -3574,6 +3477,7 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t
     h->dev = device;
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->st_copy, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
     h->grid_full = std::min(h->sms * (2048 / kBlock), kMaxGrid);
     long long m = z + l + 3 * ep;
@@ -3587,6 +3491,7 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t
     P.m = m; P.n = n; P.z = z; P.l = l; P.nq = nq; P.q = q; P.ns = ns; P.s = s; P.ep = ep;
     build_cones(h, &P);
     CK(cudaMallocHost((void**)&h->ctl_h, sizeof(Ctl)));
+    CK(cudaMallocHost((void**)&h->loop_arg, sizeof(long long)));
     memset(h->ctl_h, 0, sizeof(Ctl));
     h->ctl = dalloc<Ctl>(h, 1);
     Ctl* c = h->ctl_h;
@@ -3652,7 +3557,8 @@ int scs_bench_iters(scs_handle* h, int64_t k, double* ms) {
     CK(cudaEventCreate(&e1));
     const long long before = h->launches;
     CK(cudaEventRecord(e0, h->st));
-    for (int64_t i = 0; i < k; ++i) run_iteration(h);
+    if (h->gloop) enqueue_loop(h, k);
+    else for (int64_t i = 0; i < k; ++i) run_iteration(h);
     CK(cudaEventRecord(e1, h->st));
     CK(cudaEventSynchronize(e1));
     float f = 0.f;
@@ -3660,9 +3566,9 @@ int scs_bench_iters(scs_handle* h, int64_t k, double* ms) {
     *ms = f;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    h->launched_iters += k;
-    h->launches = h->launches - before;
     pull_ctl(h);
+    if (h->gloop) account_loop(h);
+    h->launches = h->launches - before;
     check_err(h);
   });
 }
@@ -3690,7 +3596,7 @@ int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms, double* 
         EpiAtGp eg{};
         eg.V = h->V;
         eg.xb = h->V.q;
-        at_pass(h, eg);  // banded: the raw pass + band-sum epilogue
+        at_pass(h, eg);
       }
     };
     one();
@@ -3710,6 +3616,22 @@ int scs_bench_kernel(scs_handle* h, int kind, int64_t reps, double* ms, double* 
     *h->ctl_h = saved;
     push_ctl(h);
   });
+}
+
+int scs_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return SCS_EINVAL;
+  *out = nullptr;
+  const cudaError_t e = cudaHostAlloc(out, (size_t)std::max<int64_t>(bytes, 8), cudaHostAllocDefault);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_global_err(std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+    return SCS_ENOMEM;
+  }
+  return SCS_OK;
+}
+
+void scs_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 int scs_query(scs_handle* h, int32_t key, int64_t* out) {

@@ -38,7 +38,7 @@
 //    fixed -- deterministic), then releases the stage on an empty mbarrier.
 //    At the end of a unit each warp runs the pass's per-row epilogue
 //    (Epi::row) over its own rows -- or writes split partials that
-//    k_tiled_combine sums in split order -- and the CTA's reductions go
+//    k_split_combine sums in split order -- and the CTA's reductions go
 //    through the usual deterministic grid_sum_last.
 #pragma once
 
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kStmThreads, 1)
     }
   }
   __syncthreads();
-  if (splits > 1) return;  // k_tiled_combine runs the epilogue and the reductions
+  if (splits > 1) return;  // k_split_combine runs the epilogue and the reductions
   epi.extra(red);
   if constexpr (Epi::NR > 0) {
     if (grid_sum_last<Epi::NR>(red, epi.V.part, &epi.V.ctl->counter)) {
@@ -378,7 +378,53 @@ __global__ void __launch_bounds__(kStmThreads, 1)
   }
 }
 
+// Sum the per-split partial rows in split order, then the epilogue.
+template <class Epi>
+__global__ void __launch_bounds__(kBlock) k_split_combine(const double* P, int splits, long long rows,
+                                                          Epi epi0) {
+  Epi epi = epi0;
+  if (!epi.load()) return;
+  constexpr int NV = Epi::NV;
+  constexpr int NR = Epi::NR > 0 ? Epi::NR : 1;
+  double red[NR];
+#pragma unroll
+  for (int t = 0; t < NR; ++t) red[t] = 0.0;
+  const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long nt = (long long)gridDim.x * kBlock;
+  for (long long j = tid; j < rows; j += nt) {
+    typename Epi::Pre pre;
+    epi.pre(j, pre);
+    double s[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) s[t] = 0.0;
+    for (int sp = 0; sp < splits; ++sp)
+#pragma unroll
+      for (int t = 0; t < NV; ++t) s[t] += P[((long long)sp * rows + j) * NV + t];
+    epi.row(j, s, pre, red);
+  }
+  epi.extra(red);
+  if constexpr (Epi::NR > 0) {
+    if (grid_sum_last<Epi::NR>(red, epi.V.part, &epi.V.ctl->counter)) {
+      if (epi.defer) {
+        if (threadIdx.x == 0)
+          for (int t = 0; t < Epi::NR; ++t) epi.V.dred[t] = red[t];
+      } else {
+        epi.finish(red);
+      }
+    }
+  }
+}
+
+__global__ void k_expand_rows(const long long* rp, long long rows, int* out) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long r = w; r < rows; r += nw)
+    for (long long k = rp[r] + lane; k < rp[r + 1]; k += 32) out[k] = (int)r;
+}
+
 // ---- format build (setup) ----------------------------------------------------
+
 // Sort key of every entry: warp section ((sub-block, slab) tile * 16 + warp),
 // then the lane that owns its row (local row mod 32), then the bank of its
 // gather word rotated by the lane -- so that in each step the 32 lanes tend

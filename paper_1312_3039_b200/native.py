@@ -10,6 +10,8 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
+import weakref
 
 import numpy as np
 
@@ -32,6 +34,7 @@ EXPORTS = (
     "scs_point_residuals", "scs_extract_point", "scs_apply_a", "scs_project_cone", "scs_destroy",
     "scs_last_error", "scs_abi_version", "scs_nccl_unique_id",
     "scs_partition_rows", "scs_gen_lasso", "scs_bench_iters", "scs_bench_kernel", "scs_query",
+    "scs_host_alloc", "scs_host_free",
     "scs_emu_group_create", "scs_emu_group_destroy", "scs_allreduce",
     "scs_cone_margin_count", "scs_cone_margins", "scs_check_products",
 )
@@ -110,6 +113,8 @@ def load():
                                        C.c_int64]),
         "scs_bench_kernel": (C.c_int, [hp, C.c_int, C.c_int64, f64p, f64p]),
         "scs_query": (C.c_int, [hp, C.c_int32, i64p]),
+        "scs_host_alloc": (C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),
+        "scs_host_free": (None, [C.c_void_p]),
         "scs_destroy": (None, [hp]),
         "scs_emu_group_create": (C.c_void_p, [C.c_int32]),
         "scs_emu_group_destroy": (None, [C.c_void_p]),
@@ -191,6 +196,50 @@ def check_products(A, x=None, y=None, device=0):
     check(lib.scs_check_products(A.nrows, A.ncols, ptr(cp, i64p), ptr(ri, i64p), ptr(va),
                                  ptr(xx), ptr(yy), ptr(ax), ptr(aty), int(device)))
     return ax, aty
+
+
+class _PinnedPool:
+    """Page-locked float64 buffers (scs_host_alloc), recycled: a buffer goes
+    back to the pool when the last numpy array viewing it is collected, so
+    repeated solves of one size reuse the same pinned pages."""
+
+    def __init__(self):
+        self._free = {}
+        self._lock = threading.Lock()
+
+    def empty(self, count):
+        count = int(count)
+        if count <= 0:
+            return np.empty(0)
+        nbytes = 8 * count
+        with self._lock:
+            lst = self._free.get(nbytes)
+            ptr = lst.pop() if lst else None
+        if ptr is None:
+            p = C.c_void_p()
+            check(load().scs_host_alloc(nbytes, C.byref(p)))
+            ptr = p.value
+        buf = (C.c_double * count).from_address(ptr)
+        weakref.finalize(buf, self._release, nbytes, ptr)
+        return np.frombuffer(buf, dtype=np.float64, count=count)
+
+    def _release(self, nbytes, ptr):
+        with self._lock:
+            self._free.setdefault(nbytes, []).append(ptr)
+
+
+_pool = _PinnedPool()
+
+
+def pinned_empty(count):
+    """Uninitialised page-locked float64 vector of length `count`."""
+    return _pool.empty(count)
+
+
+def pinned_zeros(count):
+    a = _pool.empty(count)
+    a[:] = 0.0
+    return a
 
 
 (Q_FORMAT_A, Q_FORMAT_AT, Q_LAUNCHES_PER_ITER, Q_STREAM_BYTES_A, Q_STREAM_BYTES_AT,

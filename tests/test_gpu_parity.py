@@ -57,8 +57,8 @@ def _vec_close(a, b, tol):
 # chaotic here -- injecting 1-ulp noise into its SpMV outputs moves its own
 # iterates by 1.4e-9 at iteration 30 and 1.6e-7 at iteration 50 (see
 # DESIGN.md, parity).  Trajectory checked to iteration 20; after that only
-# the outcome (INDETERMINATE at max_iters, the post-loop rule of
-# solver.py:364-369) is compared.
+# the iteration count and a post-loop status (solver.py:364-369) -- which
+# the reference itself does not reproduce under 1-ulp noise -- are checked.
 TRAJ_ONLY = {"mixed_nonorm_cgtol": 20}
 # Residual tolerance: the default residual recurrences carry
 # A u_x and A^T u_y at rounding level between direct refreshes.
@@ -111,10 +111,16 @@ def test_golden_solve(name):
     for k in range(min(len(samp), lim)):
         assert rel(samp[k][0], d["us_sample"][k]) < ITERATE_TOL, (name, k)
         assert rel(samp[k][1], d["vs_sample"][k]) < ITERATE_TOL, (name, k)
+    if name in TRAJ_ONLY:
+        # the reference's own post-loop status flips under 1-ulp SpMV noise
+        # here (3 of 6 noisy runs end max_iters_reached instead of
+        # indeterminate: tools/ref_noise_status.py); the rule itself is
+        # pinned by the maxit_* / indet_* fixtures
+        assert sol.status.value in ("indeterminate", "max_iters_reached")
+        assert sol.info.iterations == d["iterations"]
+        return
     # status: exact, including the post-loop MAX_ITERS_REACHED / INDETERMINATE rule
     assert sol.status.value == d["status"], (name, sol.status, d["status"])
-    if name in TRAJ_ONLY:
-        return
     assert len(norms) == min(50, d["iterations"])
     # cumulative CG count (setup solve of g included, embedding.py:112) after
     # every iteration, and the reported total (solver.py:376)
@@ -318,3 +324,42 @@ def test_large_psd_sides_vs_eigh(sides):
         exp = O.mat_to_svec((v * np.maximum(w, 0.0)) @ v.T)
         np.testing.assert_allclose(got[off:off + d], exp, atol=1e-9 * (1 + np.abs(x).max()))
         off += d
+
+
+@pytest.mark.parametrize("name", ["c1_lp_soc", "c2_lp_unbounded", "maxit_lasso_q18p",
+                                  "ref_portfolio"])
+def test_device_loop_matches_host_loop(name, monkeypatch):
+    """One solve = one launch of the device-side loop graph (WHILE node over
+    a SWITCH of the refresh / non-refresh iteration graphs) must give the
+    same bits as the host-driven loop over the same iteration graphs
+    (SCS_LOOP_GRAPH=0), and stop on the same iteration."""
+    d = load(name)
+    st = settings_from(d["settings"])
+    sols = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SCS_LOOP_GRAPH", flag)
+        ws = P.Workspace(fixture_problem(d), st)
+        sols.append((ws.solve(), ws.final_state))
+    (a, fa), (b, fb) = sols
+    assert a.status == b.status and a.info.iterations == b.info.iterations == d["iterations"]
+    assert a.info.cg_iters == b.info.cg_iters == d["cg_iters"]
+    assert np.array_equal(fa.u, fb.u) and np.array_equal(fa.v, fb.v)
+    for key in ("x", "y", "s", "certificate"):
+        va, vb = getattr(a, key), getattr(b, key)
+        assert (va is None) == (vb is None)
+        if va is not None:
+            assert np.array_equal(va, vb), key
+
+
+def test_pinned_buffers_roundtrip():
+    """Warm start from page-locked host buffers, solution returned in pooled
+    page-locked buffers (recycled after the arrays die)."""
+    d = load("ref_lp_feasible")
+    ws = P.Workspace(fixture_problem(d), settings_from(d["settings"]))
+    sol = ws.solve()
+    x0, y0, s0 = P.pinned_empty(d["n"]), P.pinned_empty(d["m"]), P.pinned_empty(d["m"])
+    x0[:], y0[:], s0[:] = sol.x, sol.y, sol.s
+    again = ws.solve(warm_start=(x0, y0, s0))
+    plain = ws.solve(warm_start=(np.array(sol.x), np.array(sol.y), np.array(sol.s)))
+    assert again.info.iterations == plain.info.iterations
+    assert np.array_equal(again.x, plain.x) and np.array_equal(again.y, plain.y)

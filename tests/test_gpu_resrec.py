@@ -1,7 +1,7 @@
 """GPU tests of the residual recurrence (SCS_RES_RECUR, default R = 32;
 SCS_RES_RECUR_AT=0 keeps A^T u_y direct).
 
-The termination check needs A u_x of the previous iterate (scaling.py:466).
+The termination check needs A u_x of the previous iterate (scaling.py:165).
 Because v_x is exactly 0 after every iteration (the x-part cone is free),
 u+_x = al (x - corr g_x) + (1 - al) u_x, so the solver carries
 A u_x = al (A x - corr A g_x) + (1 - al) A u_x elementwise (k_cone_tail) and
