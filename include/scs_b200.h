@@ -113,12 +113,19 @@ typedef struct {
  * rows [bounds[k], bounds[k+1]) (scs_problem.row_lo / m / m_global).  Ranks
  * are one process per GPU joined by NCCL (nccl_id), or -- to test the
  * sharded kernels on one GPU -- one host thread per shard in one process
- * joined by an emulated group (emu_group).  flags & 1 forces the sharded
- * code path (all-reduce points included) even when world == 1. */
+ * joined by an emulated group (emu_group), or one process per shard on one
+ * node joined through POSIX shared memory (flags & SCS_DIST_HOST: nccl_id
+ * then carries a NUL-terminated shared-memory name agreed by the ranks;
+ * the host all-reduce sums in rank order, so every rank gets the same
+ * bits).  flags & SCS_DIST_FORCE forces the sharded code path (all-reduce
+ * points included) even when world == 1. */
+#define SCS_DIST_FORCE 1
+#define SCS_DIST_HOST 2
 typedef struct scs_emu_group scs_emu_group;
 typedef struct {
   int32_t rank, world;
-  const uint8_t* nccl_id;  /* 128 bytes from scs_nccl_unique_id on rank 0 */
+  const uint8_t* nccl_id;  /* 128 bytes from scs_nccl_unique_id on rank 0
+                              (SCS_DIST_HOST: the shared-memory name) */
   scs_emu_group* emu_group;
   const int64_t* bounds;   /* world + 1 global row bounds */
   int32_t flags;

@@ -426,14 +426,21 @@ class Workspace:
             sp = self._dist
             self._bounds = native.i64(sp.bounds)
             self._nid = None
-            if sp.nccl_id is not None:
+            flags = 1 if sp.force else 0
+            if getattr(sp, "host_name", None):
+                nm = sp.host_name.encode()
+                if len(nm) > 127:
+                    raise ValueError("shared-memory group name longer than 127 bytes")
+                self._nid = (native.C.c_uint8 * 128).from_buffer_copy(nm.ljust(128, b"\0"))
+                flags |= 2
+            elif sp.nccl_id is not None:
                 self._nid = (native.C.c_uint8 * 128).from_buffer_copy(bytes(sp.nccl_id))
             dist = native.Dist(
                 rank=sp.rank, world=sp.world,
                 nccl_id=native.C.cast(self._nid, native.C.POINTER(native.C.c_uint8))
                 if self._nid is not None else None,
                 emu_group=sp.emu_group, bounds=native.ptr(self._bounds, native.i64p),
-                flags=1 if sp.force else 0)
+                flags=flags)
         h = native.C.c_void_p()
         rc = self._lib.scs_create(native.C.byref(P), native.C.byref(S),
                                   native.C.byref(dist) if dist is not None else None,

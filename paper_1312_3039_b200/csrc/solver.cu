@@ -7,7 +7,14 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <errno.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -18,6 +25,7 @@
 #include <mutex>
 #include <queue>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/scs_b200.h"
@@ -1163,6 +1171,123 @@ struct EmuComm : ScsComm {
   bool capturable() const override { return false; }
 };
 
+// One process per shard on one node, joined through a POSIX shared-memory
+// segment (SCS_DIST_HOST): the all-reduce copies the buffer to this rank's
+// slot, meets the others at a process-shared barrier, sums the slots in
+// rank order (identical bits on every rank), and copies the sum back; big
+// buffers go through in chunks.  Host-synchronised like EmuComm (not
+// capturable): it exists to run the multi-process path -- bootstrap,
+// per-rank generation, bounds -- where NCCL cannot (two ranks on one GPU).
+struct ShmHeader {
+  std::atomic<int> ready;
+  std::atomic<int> broken;
+  std::atomic<long long> arrived;
+  std::atomic<long long> gen;
+  int world;
+  int pad;
+  long long slot;  // doubles per rank slot
+};
+constexpr long long kShmSlot = 1 << 20;  // 8 MB per rank per chunk
+
+struct ShmComm : ScsComm {
+  ShmHeader* hd = nullptr;
+  double* slots = nullptr;
+  size_t bytes = 0;
+  int rank = 0, world = 1;
+  std::string name;
+  std::vector<double> sum;
+  ShmComm(const char* nm, int r, int w) : rank(r), world(w), name(nm) {
+    bytes = sizeof(ShmHeader) + 64 + (size_t)w * kShmSlot * sizeof(double);
+    int fd = -1;
+    if (rank == 0) {
+      shm_unlink(name.c_str());
+      fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+      if (fd < 0) throw Fail{SCS_ENCCL, "shm_open(create) " + name + ": " + strerror(errno)};
+      if (ftruncate(fd, (off_t)bytes) != 0) {
+        close(fd);
+        throw Fail{SCS_ENCCL, std::string("ftruncate: ") + strerror(errno)};
+      }
+    } else {
+      for (int t = 0; t < 12000 && fd < 0; ++t) {  // rank 0 creates it (<= 120 s)
+        fd = shm_open(name.c_str(), O_RDWR, 0600);
+        if (fd < 0) std::this_thread::sleep_for(std::chrono::milliseconds(10));
+      }
+      if (fd < 0) throw Fail{SCS_ENCCL, "shm_open " + name + ": " + strerror(errno)};
+      struct stat stt;
+      for (int t = 0; t < 12000; ++t) {
+        if (fstat(fd, &stt) == 0 && (size_t)stt.st_size >= bytes) break;
+        std::this_thread::sleep_for(std::chrono::milliseconds(10));
+      }
+    }
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) throw Fail{SCS_ENCCL, std::string("mmap: ") + strerror(errno)};
+    hd = reinterpret_cast<ShmHeader*>(p);
+    slots = reinterpret_cast<double*>(reinterpret_cast<char*>(p) + sizeof(ShmHeader) + 64);
+    if (rank == 0) {
+      hd->world = w;
+      hd->slot = kShmSlot;
+      hd->arrived.store(0);
+      hd->gen.store(0);
+      hd->broken.store(0);
+      hd->ready.store(1, std::memory_order_release);
+    } else {
+      for (int t = 0; t < 12000 && hd->ready.load(std::memory_order_acquire) != 1; ++t)
+        std::this_thread::sleep_for(std::chrono::milliseconds(10));
+      if (hd->ready.load() != 1 || hd->world != w)
+        throw Fail{SCS_ENCCL, "shared-memory group " + name + " not initialised for this world"};
+    }
+    cudaHostRegister(slots, (size_t)w * kShmSlot * sizeof(double), cudaHostRegisterDefault);
+    cudaGetLastError();  // registration is an optimisation only
+    barrier();           // every rank mapped before the first exchange
+    if (rank == 0) shm_unlink(name.c_str());
+  }
+  ~ShmComm() override {
+    if (hd) {
+      cudaHostUnregister(slots);
+      cudaGetLastError();
+      munmap(hd, bytes);
+    }
+  }
+  void barrier() {
+    const long long my = hd->gen.load(std::memory_order_acquire);
+    if (hd->arrived.fetch_add(1) + 1 == world) {
+      hd->arrived.store(0);
+      hd->gen.fetch_add(1, std::memory_order_release);
+      return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (long long spin = 0; hd->gen.load(std::memory_order_acquire) == my; ++spin) {
+      if (hd->broken.load()) throw Fail{SCS_ENCCL, "shared-memory group broken by another rank"};
+      if (spin > 1000) std::this_thread::sleep_for(std::chrono::microseconds(20));
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) {
+        hd->broken.store(1);
+        throw Fail{SCS_ENCCL, "shared-memory all-reduce timed out"};
+      }
+    }
+  }
+  void allreduce(cudaStream_t st, double* d, size_t n) override {
+    for (size_t off = 0; off < n || (n == 0 && off == 0); off += kShmSlot) {
+      const size_t k = std::min<size_t>(kShmSlot, n - off);
+      double* mine = slots + (size_t)rank * kShmSlot;
+      if (k) CK(cudaMemcpyAsync(mine, d + off, k * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      barrier();
+      sum.assign(k, 0.0);
+      for (int r = 0; r < world; ++r) {
+        const double* o = slots + (size_t)r * kShmSlot;
+        if (r == 0) std::copy(o, o + k, sum.begin());
+        else for (size_t i = 0; i < k; ++i) sum[i] += o[i];
+      }
+      barrier();  // slots free for the next chunk
+      if (k) CK(cudaMemcpyAsync(d + off, sum.data(), k * sizeof(double), cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+      if (n == 0) break;
+    }
+  }
+  bool capturable() const override { return false; }
+};
+
 #ifdef SCS_WITH_NCCL
 struct NcclComm : ScsComm {
   ncclComm_t c = nullptr;
@@ -1406,13 +1531,21 @@ void launch_stream(scs_handle* h, int mat, const Epi& epi) {
     cudaFuncSetAttribute(k_stream<NV, STRIDE, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     cudaGetLastError();
   });
-  const size_t fixed = kStmAccBytes + 2 * (size_t)F.W * STRIDE * 8 + kStmMaxStages * (2 * 8 + 16);
-  const int NS = (int)std::min<long long>(kStmMaxStages, ((long long)optin - (long long)fixed) / F.cap);
-  if (NS < 2) throw Fail{SCS_EINVAL, "streamed SpMV: shared memory budget exceeded"};
+  // two slab buffers (the next slab loads while the current one is read)
+  // when at least 3 stages fit beside them, else one buffer (NV = 2 with
+  // 4096-column slabs: 64 KB per slab)
+  int NB = 2, NS = 0;
+  size_t fixed = 0;
+  for (; NB >= 1; --NB) {
+    fixed = kStmAccBytes + (size_t)NB * F.W * STRIDE * 8 + kStmMaxStages * (2 * 8 + 16);
+    NS = (int)std::min<long long>(kStmMaxStages, ((long long)optin - (long long)fixed) / F.cap);
+    if (NS >= 3 || (NB == 1 && NS >= 2)) break;
+  }
+  if (NB < 1 || NS < 2) throw Fail{SCS_EINVAL, "streamed SpMV: shared memory budget exceeded"};
   const size_t smem = fixed + (size_t)NS * F.cap;
   const Csr& M = mat == 0 ? h->A : h->At;
   k_stream<NV, STRIDE, Epi><<<S.G, kStmThreads, smem, h->st>>>(F, S.cmds, S.coff, M, epi, S.splits,
-                                                              h->Pstm, NS);
+                                                              h->Pstm, NS, NB);
   CK(cudaGetLastError());
   h->launches++;
   if (S.splits > 1) {
@@ -1639,10 +1772,10 @@ void build_stream(scs_handle* h, int mat) {
   Stm& F = h->sF[mat];
   F.rows = rows;
   F.cols = cols;
-  // slab width: 2048 columns, narrowed (/4, down to 256) when dense rows
+  // slab width: 4096 columns, narrowed (/4, down to 256) when dense rows
   // make warp sections deeper than k_stm_pin handles (> 0.1% flagged)
   const bool wforced = getenv("SCS_STREAM_W") != nullptr;
-  long long W = std::min<long long>(kStmMaxW, std::max<long long>(32, env_ll("SCS_STREAM_W", 2048)));  // >= 32: padding gathers column = lane
+  long long W = std::min<long long>(kStmMaxW, std::max<long long>(32, env_ll("SCS_STREAM_W", 4096)));  // >= 32: padding gathers column = lane
   F.cap = (int)(env_ll("SCS_STREAM_CAP", 32768) & ~15LL);
   const int min_cap = (int)stm_piece_bytes(32 * kStmWarps);
   if (F.cap < min_cap) F.cap = (min_cap + 15) & ~15;
@@ -3138,12 +3271,18 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
       if (h->bounds[h->rank] != h->row_lo || h->bounds[h->rank + 1] - h->bounds[h->rank] != m ||
           h->bounds.front() != 0 || h->bounds.back() != h->m_glob)
         throw Fail{SCS_EINVAL, "shard bounds do not match row_lo / m / m_global"};
-      h->sharded = h->world > 1 || (dist->flags & 1);
+      h->sharded = h->world > 1 || (dist->flags & SCS_DIST_FORCE);
       if (h->sharded) {
         if (dist->emu_group) {
           scs_emu_group* g = (scs_emu_group*)dist->emu_group;
           if (g->world != h->world) throw Fail{SCS_EINVAL, "emulated group size != world"};
           h->comm = new EmuComm(g, h->rank);
+        } else if (dist->flags & SCS_DIST_HOST) {
+          if (!dist->nccl_id || !dist->nccl_id[0])
+            throw Fail{SCS_EINVAL, "host-shared-memory group needs its name in nccl_id"};
+          char nm[129] = {0};
+          memcpy(nm, dist->nccl_id, 128);
+          h->comm = new ShmComm(nm, h->rank, h->world);
         } else {
 #ifdef SCS_WITH_NCCL
           if (!dist->nccl_id) throw Fail{SCS_EINVAL, "row-sharded create needs an NCCL id"};

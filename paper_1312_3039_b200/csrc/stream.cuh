@@ -54,14 +54,13 @@ constexpr int kStmThreads = (kStmWarps + 1) * 32;
 constexpr int kStmHdr = 48;         // piece header bytes: u32 nslots, u16 wsec[17]
 constexpr int kStmOwn = 32 * 16;    // + per warp section, per lane: owner lane of its overflow slots
 constexpr int kStmData = kStmHdr + kStmOwn;  // values start here; then u16 slot words
-constexpr int kStmMaxW = 2048;      // slot word column field: 11 bits
+constexpr int kStmMaxW = 4096;      // slot word column field: 12 bits
 __host__ __device__ constexpr unsigned long long stm_piece_bytes(unsigned long long ns) {
   return kStmData + 10ULL * ns;
 }
 constexpr int kStmAccBytes = 2 * kStmRS * 8;
 constexpr int kStmMaxStages = 4;
 constexpr int kStmPin = kStmSecRows / 32;  // rows pinned to each lane
-constexpr unsigned kStmSentinel = 2u << 14;   // padding slot word (flags 2)
 
 enum : unsigned short { STM_END = 1, STM_CSR = 2, STM_PAIR = 4, STM_TILE = 8, STM_CSR32 = 16 };
 
@@ -153,33 +152,37 @@ __device__ __forceinline__ void stm_rows(Epi& epi, double* a, long long r0, int 
   }
 }
 
-// One warp section of a piece.  Slot word: column (16 bits) | local row
-// (8 bits) << 16 | overflow << 24 | padding << 25.  A pinned entry's row is
+// One warp section of a piece.  Slot word (16 bits): column in the slab
+// (12 bits) | j << 12 (3 bits) | overflow << 15.  A pinned entry's row is
 // owned by its lane (local row = 32 j + lane), so the pinned read-modify-
 // writes of a step hit 32 distinct rows in the minimum number of shared-
 // memory wavefronts; overflow entries (in another lane's free slots) share
 // the same update: all overflow entries of one owner lane sit in one lane,
 // and k_stm_pin keeps them off the steps where the owner lane holds the
-// same row, so the rows of a step are always distinct.
+// same row, so the rows of a step are always distinct.  Padding slots hold
+// value 0 (word: column = lane, pinned, j = 0): the update is predicated on
+// a nonzero value, which skips them -- and explicit zeros, whose products
+// add nothing to a row sum (x + 0 = x, 0 + -0 = 0).
 template <int NV, int STRIDE, int U>
 __device__ __forceinline__ void stm_steps(const double* vals, const unsigned short* idx, int k,
                                           const double* xs, double* a, unsigned own) {
   const int lane = threadIdx.x & 31;
   double pr[U][NV];
-  unsigned rw[U], fl[U];
+  unsigned rw[U];
+  bool live[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {  // every load of the batch before its stores
     const double v = vals[(k + u) * 32 + lane];
     const unsigned id = idx[(k + u) * 32 + lane];
-    fl[u] = id >> 14;
-    rw[u] = ((id >> 11) & 7u) << 5 | (fl[u] == 1u ? own : (unsigned)lane);
-    const unsigned col = id & 0x7ffu;
+    live[u] = v != 0.0;
+    rw[u] = ((id >> 12) & 7u) << 5 | ((id >> 15) ? own : (unsigned)lane);
+    const unsigned col = id & 0xfffu;
 #pragma unroll
     for (int t = 0; t < NV; ++t) pr[u][t] = v * xs[col * STRIDE + t];
   }
 #pragma unroll
   for (int u = 0; u < U; ++u)
-    if (fl[u] < 2u)  // pinned or overflow (padding: 2)
+    if (live[u])
 #pragma unroll
       for (int t = 0; t < NV; ++t) a[rw[u] * NV + t] += pr[u][t];
 }
@@ -222,14 +225,14 @@ __device__ __forceinline__ void stm_csr(Epi& epi, const Csr& M, long long r0, lo
 template <int NV, int STRIDE, class Epi>
 __global__ void __launch_bounds__(kStmThreads, 1)
     k_stream(Stm F, const StmCmd* __restrict__ cmds, const long long* __restrict__ coff, Csr M,
-             Epi epi0, int splits, double* P, int NS) {
+             Epi epi0, int splits, double* P, int NS, int NB) {
   Epi epi = epi0;
   if (!epi.load()) return;
   extern __shared__ __align__(128) unsigned char stm_sm[];
   double* acc = reinterpret_cast<double*>(stm_sm);
   const int xbytes = F.W * STRIDE * 8;
   double* xbuf0 = reinterpret_cast<double*>(stm_sm + kStmAccBytes);
-  unsigned char* stages = stm_sm + kStmAccBytes + 2 * xbytes;
+  unsigned char* stages = stm_sm + kStmAccBytes + NB * xbytes;  // NB = 2 (double-buffered) or 1 slab buffers
   unsigned long long* full = reinterpret_cast<unsigned long long*>(stages + (size_t)NS * F.cap);
   unsigned long long* empty = full + kStmMaxStages;
   StmCtl* sctl = reinterpret_cast<StmCtl*>(empty + kStmMaxStages);
@@ -277,7 +280,8 @@ __global__ void __launch_bounds__(kStmThreads, 1)
         unsigned slab_bytes = 0;
         long long cstart = 0;
         if (tile && (long long)slab != slab_cur) {
-          xb ^= 1;
+          if (NB == 2) xb ^= 1;
+          else xb = 0;  // one buffer: wait below for the last stage that read it
           const long long jlast = xb ? last1 : last0;
           if (jlast >= 0 && jlast > i - NS) mbar_wait(empty + (int)(jlast % NS), (unsigned)((jlast / NS) & 1));
           slab_cur = slab;
@@ -462,6 +466,96 @@ __global__ void k_stm_sec(const unsigned long long* key, long long nnz, int* sec
 // 0xffff and their sub-block becomes a CSR unit.
 // slot = step * 32 + lane, | 1 << 30 for overflow.
 constexpr int kStmPinMax = 128;
+constexpr int kStmSearchMax = 24;  // local search on sections of at most this depth
+
+// Modelled shared-memory wavefronts of one (step, half-warp) of a section:
+// the gather (8-byte words: entries of one bank class col & 15 conflict;
+// padding slots gather column = lane) plus twice the accumulator read-
+// modify-write (rows of one class row & 15; padding is skipped).  Per
+// (step, half) the class counts are kept as 16 packed 4-bit counters.
+__device__ __forceinline__ int stm_nib_max(unsigned long long c) {
+  int m = 0;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) m = max(m, (int)((c >> (4 * b)) & 15ull));
+  return m;
+}
+__device__ __forceinline__ unsigned long long stm_gbit(unsigned c, int l) {
+  return 1ull << (4 * ((c >> 31) ? ((c >> 24) & 15u) : (unsigned)(l & 15)));
+}
+__device__ __forceinline__ unsigned long long stm_rbit(unsigned c) {
+  return (c >> 31) ? 1ull << (4 * ((c >> 11) & 15u)) : 0ull;
+}
+
+// Local search after the greedy placement: within each lane, swap the
+// contents of two steps (entries of the lane's own rows, hosted overflow
+// entries, padding) when the rows of both steps stay distinct and the
+// modelled wavefronts of the two steps drop.  On C5-like sections this
+// lowers the gather conflicts by ~15% and the accumulator ones by ~5%
+// (tools/stm_sim.cpp).  Grid cell: valid << 31 | class << 24 | row << 11 |
+// entry.  Updates slot[] of the moved entries.
+__device__ void stm_search(const unsigned long long* key, long long p0, long long E, int D, int* slot) {
+  unsigned g[kStmSearchMax * 32];
+  unsigned long long rows[kStmSearchMax][4], gc[kStmSearchMax][2], rc[kStmSearchMax][2];
+  for (int i = 0; i < D * 32; ++i) g[i] = 0;
+  for (int k = 0; k < D; ++k) {
+    rows[k][0] = rows[k][1] = rows[k][2] = rows[k][3] = 0;
+  }
+  for (long long e = 0; e < E; ++e) {
+    const unsigned long long kk = key[p0 + e];
+    const unsigned row = (unsigned)(kk & 7u) * 32u + (unsigned)((kk >> 7) & 31u);
+    const unsigned cls = (unsigned)(((kk >> 3) + (kk >> 7)) & 15u);
+    const int sl = slot[p0 + e] & ((1 << 30) - 1);
+    g[sl] = 1u << 31 | cls << 24 | row << 11 | (unsigned)e;
+    rows[sl >> 5][row >> 6] |= 1ull << (row & 63);
+  }
+  for (int k = 0; k < D; ++k)
+    for (int h = 0; h < 2; ++h) {
+      unsigned long long a = 0, r = 0;
+      for (int l = h * 16; l < h * 16 + 16; ++l) {
+        a += stm_gbit(g[k * 32 + l], l);
+        r += stm_rbit(g[k * 32 + l]);
+      }
+      gc[k][h] = a;
+      rc[k][h] = r;
+    }
+  for (int pass = 0; pass < 2; ++pass) {
+    bool any = false;
+    for (int l = 0; l < 32; ++l) {
+      const int h = l >> 4;
+      for (int k1 = 0; k1 < D; ++k1)
+        for (int k2 = k1 + 1; k2 < D; ++k2) {
+          const unsigned a = g[k1 * 32 + l], b = g[k2 * 32 + l];
+          if (!((a | b) >> 31)) continue;
+          const unsigned ra = (a >> 11) & 255u, rb = (b >> 11) & 255u;
+          // rows stay distinct: a's row absent from step k2, b's from k1
+          if ((a >> 31) && ((rows[k2][ra >> 6] >> (ra & 63)) & 1ull)) continue;
+          if ((b >> 31) && ((rows[k1][rb >> 6] >> (rb & 63)) & 1ull)) continue;
+          const unsigned long long ga = stm_gbit(a, l), gb = stm_gbit(b, l);
+          const unsigned long long xa = stm_rbit(a), xb = stm_rbit(b);
+          const unsigned long long g1 = gc[k1][h] - ga + gb, g2 = gc[k2][h] - gb + ga;
+          const unsigned long long r1 = rc[k1][h] - xa + xb, r2 = rc[k2][h] - xb + xa;
+          const int before = stm_nib_max(gc[k1][h]) + stm_nib_max(gc[k2][h]) +
+                             2 * (stm_nib_max(rc[k1][h]) + stm_nib_max(rc[k2][h]));
+          const int after = stm_nib_max(g1) + stm_nib_max(g2) + 2 * (stm_nib_max(r1) + stm_nib_max(r2));
+          if (after >= before) continue;
+          any = true;
+          g[k1 * 32 + l] = b;
+          g[k2 * 32 + l] = a;
+          gc[k1][h] = g1; gc[k2][h] = g2; rc[k1][h] = r1; rc[k2][h] = r2;
+          if (a >> 31) { rows[k1][ra >> 6] &= ~(1ull << (ra & 63)); rows[k2][ra >> 6] |= 1ull << (ra & 63); }
+          if (b >> 31) { rows[k2][rb >> 6] &= ~(1ull << (rb & 63)); rows[k1][rb >> 6] |= 1ull << (rb & 63); }
+        }
+    }
+    if (!any) break;
+  }
+  for (int i = 0; i < D * 32; ++i) {
+    const unsigned c = g[i];
+    if (!(c >> 31)) continue;
+    const long long e = p0 + (c & 2047u);
+    slot[e] = (slot[e] & (1 << 30)) | i;
+  }
+}
+
 __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned long long* key,
                           int* perm, int* slot, unsigned short* depth, unsigned char* hown) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -605,6 +699,7 @@ __global__ void k_stm_pin(const long long* sec_ptr, long long nsec, unsigned lon
             slot[a] = k * 32 + l;
           }
         }
+        if (D <= kStmSearchMax && E <= 2047) stm_search(key, p0, E, D, slot);
       }
     }
     if (!ok) { depth[s] = 0xffff; continue; }
@@ -634,7 +729,7 @@ __global__ void k_stm_init(unsigned char* blob, const unsigned long long* poff, 
     // padding gathers column = lane: distinct banks, no conflict with the real entries
     for (unsigned k = lane; k < ns; k += 32) {
       v[k] = 0.0;
-      id[k] = (unsigned short)(kStmSentinel | (unsigned)lane);
+      id[k] = (unsigned short)lane;
     }
   }
 }
@@ -666,7 +761,7 @@ __global__ void k_stm_scatter(const int* sec, const int* slot, long long nnz, co
     const unsigned rl = (unsigned)(rowid[s] % kStmSecRows);
     reinterpret_cast<double*>(bl + kStmData)[at] = val[s];
     reinterpret_cast<unsigned short*>(bl + kStmData + 8 * (size_t)ns)[at] =
-        (unsigned short)((unsigned)(ci[s] % W) | ((rl >> 5) << 11) | (ovf << 14));
+        (unsigned short)((unsigned)(ci[s] % W) | ((rl >> 5) << 12) | (ovf << 15));
   }
 }
 

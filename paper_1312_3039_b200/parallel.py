@@ -10,8 +10,9 @@ inside a PSD or exponential block, balanced by nonzeros.
 
 Ranks are one process per GPU joined by NCCL (``nccl_bootstrap`` uses
 torch.distributed only to broadcast the 128-byte NCCL id), or -- to test the
-sharded kernels with a single GPU -- one host thread per shard joined by an
-in-process emulated group (``emulated_solve``).
+sharded path with a single GPU -- one host thread per shard joined by an
+in-process emulated group (``emulated_solve``), or one process per shard
+joined by a host shared-memory group (``host_bootstrap``).
 """
 
 from __future__ import annotations
@@ -32,6 +33,7 @@ class ShardSpec:
     nccl_id: bytes = None
     emu_group: int = None     # scs_emu_group* (emulated group)
     force: bool = False       # sharded code path even with world == 1
+    host_name: str = None     # POSIX shared-memory group name (one process per shard, one node)
 
 
 class ShardProblem:
@@ -130,6 +132,21 @@ def emulated_solve(prob, settings, world, bounds=None, warm_start=None, on_itera
 def gather_vector(parts):
     """Concatenate per-rank slices of an m-length vector."""
     return np.concatenate([np.asarray(p) for p in parts])
+
+
+def host_bootstrap(rank, world):
+    """Name of a POSIX shared-memory group from rank 0, broadcast with
+    torch.distributed (the process group must already be initialised): the
+    host all-reduce joins one process per shard on one node without NCCL
+    (e.g. two ranks sharing one GPU)."""
+    import os
+    import uuid
+
+    import torch.distributed as dist
+
+    obj = [f"/scs_{os.getpid()}_{uuid.uuid4().hex[:12]}" if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
 
 
 def nccl_bootstrap(rank, world):
