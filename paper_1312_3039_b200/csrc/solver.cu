@@ -1331,6 +1331,7 @@ struct scs_handle {
   } ssch[2][2];
   double* Pstm = nullptr;
   unsigned long long stm_bytes[2] = {0, 0};
+  bool stm_pair = false;  // NV = 1 passes on pair units sharing slab loads (SCS_STREAM_PAIR=1)
   int recur_refresh = 20;  // opt-in recurrence: direct A x every k iterations
   int res_rec = 32;        // A u_x of the residual check by recurrence, direct every k (0: always direct)
   bool res_rec_at = true;  // ... and A^T u_y (SCS_RES_RECUR_AT=0: only A u_x)
@@ -1519,7 +1520,9 @@ void launch_spmv(scs_handle* h, const Csr& M, int L, const Epi& epi) {
 template <int NV, int STRIDE, class Epi>
 void launch_stream(scs_handle* h, int mat, const Epi& epi) {
   const Stm& F = h->sF[mat];
-  const auto& S = h->ssch[mat][NV == 1 ? 1 : 0];
+  const int pair = (NV == 1 && h->stm_pair) ? 1 : 0;  // NV = 1: pairs of sub-blocks share slab loads
+  const auto& S = h->ssch[mat][pair];
+  const int accb = (pair ? 2 : 1) * kStmRS * NV * 8;
   static std::once_flag once;
   static int optin = 0;
   std::call_once(once, [&] {
@@ -1537,7 +1540,7 @@ void launch_stream(scs_handle* h, int mat, const Epi& epi) {
   int NB = 2, NS = 0;
   size_t fixed = 0;
   for (; NB >= 1; --NB) {
-    fixed = kStmAccBytes + (size_t)NB * F.W * STRIDE * 8 + kStmMaxStages * (2 * 8 + 16);
+    fixed = accb + (size_t)NB * F.W * STRIDE * 8 + kStmMaxStages * (2 * 8 + 16);
     NS = (int)std::min<long long>(kStmMaxStages, ((long long)optin - (long long)fixed) / F.cap);
     if (NS >= 3 || (NB == 1 && NS >= 2)) break;
   }
@@ -1545,7 +1548,7 @@ void launch_stream(scs_handle* h, int mat, const Epi& epi) {
   const size_t smem = fixed + (size_t)NS * F.cap;
   const Csr& M = mat == 0 ? h->A : h->At;
   k_stream<NV, STRIDE, Epi><<<S.G, kStmThreads, smem, h->st>>>(F, S.cmds, S.coff, M, epi, S.splits,
-                                                              h->Pstm, NS, NB);
+                                                              h->Pstm, NS, NB, accb);
   CK(cudaGetLastError());
   h->launches++;
   if (S.splits > 1) {
@@ -1776,9 +1779,9 @@ void build_stream(scs_handle* h, int mat) {
   // make warp sections deeper than k_stm_pin handles (> 0.1% flagged)
   const bool wforced = getenv("SCS_STREAM_W") != nullptr;
   long long W = std::min<long long>(kStmMaxW, std::max<long long>(32, env_ll("SCS_STREAM_W", 4096)));  // >= 32: padding gathers column = lane
-  F.cap = (int)(env_ll("SCS_STREAM_CAP", 32768) & ~15LL);
+  F.cap = (int)(env_ll("SCS_STREAM_CAP", 0) & ~15LL);
   const int min_cap = (int)stm_piece_bytes(32 * kStmWarps);
-  if (F.cap < min_cap) F.cap = (min_cap + 15) & ~15;
+  if (F.cap > 0 && F.cap < min_cap) F.cap = (min_cap + 15) & ~15;
   F.NB = (int)((rows + kStmRS - 1) / kStmRS);
   long long ntile = 0, nsec = 0;
   int *rowid = nullptr, *perm = nullptr, *sec = nullptr, *slot = nullptr;
@@ -1840,6 +1843,23 @@ void build_stream(scs_handle* h, int mat) {
   for (void* p : {(void*)rowid, (void*)perm, (void*)sec, (void*)slot, (void*)hown}) dfree(h, p);
   W /= 4;
   }
+  if (F.cap <= 0) {
+    // default piece cap: three stages beside the accumulators and two slab
+    // buffers of an NV = 1 pass, so that a piece is a whole tile (~42 KB at
+    // config 5): measured at C5, whole-tile pieces beat deeper rings of
+    // smaller pieces (the per-piece synchronisation of 16 consumer warps
+    // costs more than the extra bytes in flight gain), and single sub-block
+    // units (32 KB of accumulators) beat slab-sharing pairs (64 KB), whose
+    // stages would have to be half as large
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+    const long long avail = (long long)optin - 1024 - (h->stm_pair ? 2 : 1) * kStmRS * 8LL -
+                            2LL * F.W * 8 - kStmMaxStages * (2 * 8 + 16);
+    const long long nst = env_ll("SCS_STREAM_STAGES", 3);
+    F.cap = (int)(std::min<long long>(65536, std::max<long long>(min_cap, avail / nst)) & ~15LL);
+    if (F.cap < min_cap) F.cap = (min_cap + 15) & ~15;
+  }
+  dbg("stream piece cap mat=%d: %d bytes", mat, F.cap);
   std::vector<long long> rp_h(rows + 1);
   d2h(h, rp_h.data(), M.rp, rows + 1);
   CK(cudaStreamSynchronize(h->st));
@@ -1872,7 +1892,10 @@ void build_stream(scs_handle* h, int mat) {
     // CSR units only for short rows (the consumers run them at 4 lanes per row)
     T.tiled[sb] = !bad && (nt == 0 || sl >= min_avg * nt || T.nnz_sb[sb] > 16 * (r1 - r0)) ? 1 : 0;
   }
-  std::vector<unsigned short> tile_kp(ntile, 1), pwsec;
+  // pieces: consecutive step ranges [s_j, s_j+1) of all sections of a tile,
+  // each grown greedily up to `cap` bytes, so the ring's stages carry full
+  // pieces (the bytes in flight per SM set the achievable DRAM rate)
+  std::vector<unsigned short> pstep0, pwsec;
   std::vector<long long> ptile;  // tile of every piece
   long long npiece = 0;
   unsigned long long bytes = 0;
@@ -1881,43 +1904,48 @@ void build_stream(scs_handle* h, int mat) {
     const unsigned short* d = &D[t * kStmWarps];
     int maxd = 0;
     for (int w = 0; w < kStmWarps; ++w) maxd = std::max<int>(maxd, d[w]);
-    int np = (int)std::max<long long>(1, (10 * T.slots[t] + (F.cap - kStmData) - 1) / (F.cap - kStmData));
-    int kp = 0;
-    for (;; ++np) {
-      kp = (maxd + np - 1) / np;
-      long long first = 0;  // piece 0 is the largest
-      for (int w = 0; w < kStmWarps; ++w) first += std::min<int>(d[w], kp);
-      if (stm_piece_bytes(32ULL * first) <= (unsigned long long)F.cap) break;
-    }
-    np = (maxd + kp - 1) / kp;
-    tile_kp[t] = (unsigned short)kp;
     T.pf[t] = npiece;
-    T.np[t] = np;
-    for (int j = 0; j < np; ++j) {
+    int np = 0;
+    for (int s0 = 0; s0 < maxd;) {
+      long long cnt = 0;
+      int e = s0;
+      for (;;) {  // at least one step (a step of every section fits: cap >= min_cap)
+        long long add = 0;
+        for (int w = 0; w < kStmWarps; ++w) add += d[w] > e;
+        if (e > s0 && stm_piece_bytes(32ULL * (cnt + add)) > (unsigned long long)F.cap) break;
+        cnt += add;
+        if (++e >= maxd) break;
+      }
       unsigned short acc = 0;
       pwsec.push_back(0);
       for (int w = 0; w < kStmWarps; ++w) {
-        const int st = std::max(0, std::min<int>(d[w] - j * kp, kp));
+        const int st = std::max(0, std::min<int>(d[w], e) - s0);
         acc = (unsigned short)(acc + st);
         pwsec.push_back(acc);
       }
       const unsigned ns = 32u * acc;
       T.poff.push_back(bytes);
       ptile.push_back(t);
+      pstep0.push_back((unsigned short)s0);
       T.pslots.push_back(ns);
       bytes += stm_piece_bytes(ns);
       ++npiece;
+      ++np;
+      s0 = e;
     }
+    T.np[t] = np;
   }
   // 6. device blob
   unsigned char* blob = dalloc<unsigned char>(h, std::max<unsigned long long>(bytes, 16));
   long long* d_pf = dalloc<long long>(h, ntile);
-  unsigned short* d_kp = dalloc<unsigned short>(h, ntile);
+  unsigned short* d_ps0 = dalloc<unsigned short>(h, std::max<long long>(npiece, 1));
+  int* d_np = dalloc<int>(h, ntile);
   unsigned long long* d_poff = dalloc<unsigned long long>(h, npiece);
   unsigned* d_pslots = dalloc<unsigned>(h, npiece);
   unsigned short* d_pwsec = dalloc<unsigned short>(h, pwsec.size());
   h2d(h, d_pf, T.pf.data(), ntile);
-  h2d(h, d_kp, tile_kp.data(), ntile);
+  h2d(h, d_ps0, pstep0.data(), npiece);
+  h2d(h, d_np, T.np.data(), ntile);
   h2d(h, d_poff, T.poff.data(), npiece);
   h2d(h, d_pslots, T.pslots.data(), npiece);
   h2d(h, d_pwsec, pwsec.data(), pwsec.size());
@@ -1927,13 +1955,13 @@ void build_stream(scs_handle* h, int mat) {
     k_stm_init<<<elem_grid(h, npiece * 32), kBlock, 0, h->st>>>(blob, d_poff, d_pslots, d_pwsec,
                                                                 d_ptile, hown, npiece);
     k_stm_scatter<<<elem_grid(h, nz), kBlock, 0, h->st>>>(sec, slot, nz, perm, rowid, M.ci, M.v, d_pf,
-                                                          d_kp, d_poff, d_pslots, d_pwsec, F.W, blob);
+                                                          d_ps0, d_np, d_poff, d_pslots, d_pwsec, F.W, blob);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(h->st));
     dfree(h, d_ptile);
   }
   CK(cudaStreamSynchronize(h->st));
-  for (void* p : {(void*)d_pf, (void*)d_kp, (void*)d_poff, (void*)d_pslots, (void*)d_pwsec,
+  for (void* p : {(void*)d_pf, (void*)d_ps0, (void*)d_np, (void*)d_poff, (void*)d_pslots, (void*)d_pwsec,
                   (void*)sec, (void*)slot, (void*)perm, (void*)rowid, (void*)hown})
     dfree(h, p);
   F.blob = blob;
@@ -2014,6 +2042,7 @@ void stm_selfcheck(scs_handle* h) {
 // Streamed tiles for large matrices (SCS_STREAM=0 off, 1 force on).
 void setup_stream(scs_handle* h) {
   const long long force = env_ll("SCS_STREAM", -1);
+  h->stm_pair = env_ll("SCS_STREAM_PAIR", 0) != 0;
   if (force == 0 || h->nnz == 0) return;
   if (force < 0 && h->nnz < 20000000LL) return;
   size_t need = 0;

@@ -59,7 +59,7 @@ __host__ __device__ constexpr unsigned long long stm_piece_bytes(unsigned long l
   return kStmData + 10ULL * ns;
 }
 constexpr int kStmAccBytes = 2 * kStmRS * 8;
-constexpr int kStmMaxStages = 4;
+constexpr int kStmMaxStages = 8;
 constexpr int kStmPin = kStmSecRows / 32;  // rows pinned to each lane
 
 enum : unsigned short { STM_END = 1, STM_CSR = 2, STM_PAIR = 4, STM_TILE = 8, STM_CSR32 = 16 };
@@ -163,15 +163,20 @@ __device__ __forceinline__ void stm_rows(Epi& epi, double* a, long long r0, int 
 // value 0 (word: column = lane, pinned, j = 0): the update is predicated on
 // a nonzero value, which skips them -- and explicit zeros, whose products
 // add nothing to a row sum (x + 0 = x, 0 + -0 = 0).
-template <int NV, int STRIDE, int U>
+template <int NV, int STRIDE, int U, bool MASK>
 __device__ __forceinline__ void stm_steps(const double* vals, const unsigned short* idx, int k,
-                                          const double* xs, double* a, unsigned own) {
+                                          int k1, const double* xs, double* a, unsigned own) {
   const int lane = threadIdx.x & 31;
   double pr[U][NV];
   unsigned rw[U];
   bool live[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {  // every load of the batch before its stores
+    live[u] = false;
+    rw[u] = 0;
+#pragma unroll
+    for (int t = 0; t < NV; ++t) pr[u][t] = 0.0;
+    if (MASK && k + u >= k1) continue;  // warp-uniform: no load issued past the section's end
     const double v = vals[(k + u) * 32 + lane];
     const unsigned id = idx[(k + u) * 32 + lane];
     live[u] = v != 0.0;
@@ -187,12 +192,15 @@ __device__ __forceinline__ void stm_steps(const double* vals, const unsigned sho
       for (int t = 0; t < NV; ++t) a[rw[u] * NV + t] += pr[u][t];
 }
 
+// A warp's steps of one piece: batches of 4 steps, then the 1-3 left as one
+// masked batch (sections hold ~4-9 steps per piece), so a section's tail
+// keeps its loads in flight together instead of running step by step.
 template <int NV, int STRIDE>
 __device__ __forceinline__ void stm_piece(const double* vals, const unsigned short* idx, int k0,
                                           int k1, const double* xs, double* a, unsigned own) {
   int k = k0;
-  for (; k + 4 <= k1; k += 4) stm_steps<NV, STRIDE, 4>(vals, idx, k, xs, a, own);
-  for (; k < k1; ++k) stm_steps<NV, STRIDE, 1>(vals, idx, k, xs, a, own);
+  for (; k + 4 <= k1; k += 4) stm_steps<NV, STRIDE, 4, false>(vals, idx, k, k1, xs, a, own);
+  if (k < k1) stm_steps<NV, STRIDE, 3, true>(vals, idx, k, k1, xs, a, own);
 }
 
 // CSR unit rows [r0, rend) of this warp, L lanes per row (warp-uniform loop)
@@ -225,19 +233,20 @@ __device__ __forceinline__ void stm_csr(Epi& epi, const Csr& M, long long r0, lo
 template <int NV, int STRIDE, class Epi>
 __global__ void __launch_bounds__(kStmThreads, 1)
     k_stream(Stm F, const StmCmd* __restrict__ cmds, const long long* __restrict__ coff, Csr M,
-             Epi epi0, int splits, double* P, int NS, int NB) {
+             Epi epi0, int splits, double* P, int NS, int NB, int accb) {
   Epi epi = epi0;
   if (!epi.load()) return;
   extern __shared__ __align__(128) unsigned char stm_sm[];
   double* acc = reinterpret_cast<double*>(stm_sm);
   const int xbytes = F.W * STRIDE * 8;
-  double* xbuf0 = reinterpret_cast<double*>(stm_sm + kStmAccBytes);
-  unsigned char* stages = stm_sm + kStmAccBytes + NB * xbytes;  // NB = 2 (double-buffered) or 1 slab buffers
+  // accb: accumulator bytes (sub-blocks per unit x 4096 rows x NV doubles)
+  double* xbuf0 = reinterpret_cast<double*>(stm_sm + accb);
+  unsigned char* stages = stm_sm + accb + NB * xbytes;  // NB = 2 (double-buffered) or 1 slab buffers
   unsigned long long* full = reinterpret_cast<unsigned long long*>(stages + (size_t)NS * F.cap);
   unsigned long long* empty = full + kStmMaxStages;
   StmCtl* sctl = reinterpret_cast<StmCtl*>(empty + kStmMaxStages);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kStmAccBytes / 8; i += blockDim.x) acc[i] = 0.0;
+  for (int i = tid; i < accb / 8; i += blockDim.x) acc[i] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(full + s, 1);
@@ -737,7 +746,8 @@ __global__ void k_stm_init(unsigned char* blob, const unsigned long long* poff, 
 // scatter every entry of a tiled sub-block into its piece
 __global__ void k_stm_scatter(const int* sec, const int* slot, long long nnz, const int* perm,
                               const int* rowid, const int* ci, const double* val,
-                              const long long* tile_pf, const unsigned short* tile_kp,
+                              const long long* tile_pf, const unsigned short* pstep0,
+                              const int* tile_np,
                               const unsigned long long* poff, const unsigned* pslots,
                               const unsigned short* pwsec, int W, unsigned char* blob) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -748,12 +758,12 @@ __global__ void k_stm_scatter(const int* sec, const int* slot, long long nnz, co
     const int w = sc % kStmWarps;
     const long long pf = tile_pf[tile];
     if (pf < 0) continue;  // CSR sub-block
-    const int kp = tile_kp[tile];
     const int sl = slot[e];
     const unsigned ovf = (unsigned)(sl >> 30) & 1u;
     const int k = (sl & ((1 << 30) - 1)) >> 5, lane = sl & 31;
-    const long long piece = pf + k / kp;
-    const int kk = k % kp;
+    long long piece = pf;  // the piece whose step range holds step k
+    for (const long long pend = pf + tile_np[tile]; piece + 1 < pend && pstep0[piece + 1] <= k;) ++piece;
+    const int kk = k - pstep0[piece];
     unsigned char* bl = blob + poff[piece];
     const unsigned ns = pslots[piece];
     const long long at = ((long long)pwsec[piece * (kStmWarps + 1) + w] + kk) * 32 + lane;
