@@ -1331,6 +1331,14 @@ struct scs_handle {
   } ssch[2][2];
   double* Pstm = nullptr;
   unsigned long long stm_bytes[2] = {0, 0};
+  // row-sharded: the A^T pass in row chunks, each chunk's all-reduce on a
+  // second stream overlapping the next chunk's SpMV (SCS_AT_CHUNKS)
+  static constexpr int kMaxChunks = 8;
+  int at_chunks = 1;
+  Sched at_sch[kMaxChunks][2];
+  long long at_row[kMaxChunks + 1] = {};
+  cudaStream_t st_comm = nullptr;
+  cudaEvent_t ev_chunk[kMaxChunks] = {}, ev_comm = nullptr;
   bool stm_pair = false;  // NV = 1 passes on pair units sharing slab loads (SCS_STREAM_PAIR=1)
   int recur_refresh = 20;  // opt-in recurrence: direct A x every k iterations
   int res_rec = 32;        // A u_x of the residual check by recurrence, direct every k (0: always direct)
@@ -1518,10 +1526,11 @@ void launch_spmv(scs_handle* h, const Csr& M, int L, const Epi& epi) {
 // shared-memory ring gets as many 'cap'-byte stages (<= 4) as fit beside
 // the accumulators and the two slab buffers.
 template <int NV, int STRIDE, class Epi>
-void launch_stream(scs_handle* h, int mat, const Epi& epi) {
+void launch_stream(scs_handle* h, int mat, const Epi& epi, int chunk = -1) {
   const Stm& F = h->sF[mat];
   const int pair = (NV == 1 && h->stm_pair) ? 1 : 0;  // NV = 1: pairs of sub-blocks share slab loads
-  const auto& S = h->ssch[mat][pair];
+  const auto& S = chunk < 0 ? h->ssch[mat][pair] : h->at_sch[chunk][pair];
+  const long long r0 = chunk < 0 ? 0 : h->at_row[chunk], r1 = chunk < 0 ? F.rows : h->at_row[chunk + 1];
   const int accb = (pair ? 2 : 1) * kStmRS * NV * 8;
   static std::once_flag once;
   static int optin = 0;
@@ -1552,7 +1561,8 @@ void launch_stream(scs_handle* h, int mat, const Epi& epi) {
   CK(cudaGetLastError());
   h->launches++;
   if (S.splits > 1) {
-    k_split_combine<Epi><<<elem_grid(h, F.rows), kBlock, 0, h->st>>>(h->Pstm, S.splits, F.rows, epi);
+    k_split_combine<Epi><<<elem_grid(h, r1 - r0), kBlock, 0, h->st>>>(h->Pstm, S.splits, F.rows, r0,
+                                                                     r1, epi);
     h->launches++;
   }
 }
@@ -1620,33 +1630,34 @@ struct StmTiles {
   std::vector<long long> slots;       // per tile
   std::vector<unsigned long long> poff;
   std::vector<unsigned> pslots;
+  std::vector<unsigned> pbytes;       // per piece
   std::vector<long long> nnz_sb;      // per sub-block (CSR units' cost)
 };
 
 // Units -> LPT over persistent CTAs -> flat command lists (stream.cuh).
-void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T) {
+void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T, long long sb_lo,
+                     long long sb_hi, scs_handle::Sched& S, int G0) {
   const Stm& F = h->sF[mat];
   struct Unit { long long sb0; int nsb; bool csr; int s_lo, s_hi, sp; double cost; };
   std::vector<Unit> units;
   long long ntiled = 0;
-  for (long long sb = 0; sb < T.NB;) {
+  for (long long sb = sb_lo; sb < sb_hi;) {
     if (!T.tiled[sb]) {
       units.push_back({sb, 1, true, 0, 0, 0, 0.0});
       ++sb;
       continue;
     }
-    const int nsb = (pair && sb + 1 < T.NB && T.tiled[sb + 1]) ? 2 : 1;
+    const int nsb = (pair && sb + 1 < sb_hi && T.tiled[sb + 1]) ? 2 : 1;
     units.push_back({sb, nsb, false, 0, T.S, 0, 0.0});
     ++ntiled;
     sb += nsb;
   }
-  const int G0 = h->sms;
   int splits = 1;
   // splits: the split count minimising (LPT makespan bound) + (split
   // partial rows written and read back by k_split_combine, + a launch)
   if (ntiled > 0) {
     double bytes = 0.0;
-    for (long long t = 0; t < (long long)T.NB * T.S; ++t) bytes += 10.0 * (double)T.slots[t];
+    for (long long t = sb_lo * T.S; t < sb_hi * T.S; ++t) bytes += 10.0 * (double)T.slots[t];
     const double part = 16.0 * (pair ? 1 : 2) * (double)F.rows;
     double best = 1e300;
     for (int sp = 1; sp <= std::min(32, std::max(1, T.S)); ++sp) {
@@ -1736,7 +1747,7 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T) {
             const long long p = T.pf[t] + j;
             StmCmd c{};
             c.off = T.poff[p];
-            c.bytes = (unsigned)stm_piece_bytes(T.pslots[p]);
+            c.bytes = T.pbytes[p];
             c.slab = (unsigned)s;
             c.row0 = u.sb0 * kStmRS;
             c.flags = pf;
@@ -1756,8 +1767,7 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T) {
     }
   }
   coff[G] = (long long)cmds.size();
-  auto& S = h->ssch[mat][pair];
-  S.cmds = dalloc<StmCmd>(h, cmds.size());
+  S.cmds = dalloc<StmCmd>(h, std::max<size_t>(cmds.size(), 1));
   S.coff = dalloc<long long>(h, G + 1);
   h2d(h, S.cmds, cmds.data(), cmds.size());
   h2d(h, S.coff, coff.data(), G + 1);
@@ -1780,7 +1790,7 @@ void build_stream(scs_handle* h, int mat) {
   const bool wforced = getenv("SCS_STREAM_W") != nullptr;
   long long W = std::min<long long>(kStmMaxW, std::max<long long>(32, env_ll("SCS_STREAM_W", 4096)));  // >= 32: padding gathers column = lane
   F.cap = (int)(env_ll("SCS_STREAM_CAP", 0) & ~15LL);
-  const int min_cap = (int)stm_piece_bytes(32 * kStmWarps);
+  const int min_cap = (int)stm_piece_bytes(32 * kStmWarps, kStmWarps);
   if (F.cap > 0 && F.cap < min_cap) F.cap = (min_cap + 15) & ~15;
   F.NB = (int)((rows + kStmRS - 1) / kStmRS);
   long long ntile = 0, nsec = 0;
@@ -1907,13 +1917,16 @@ void build_stream(scs_handle* h, int mat) {
     T.pf[t] = npiece;
     int np = 0;
     for (int s0 = 0; s0 < maxd;) {
-      long long cnt = 0;
+      long long cnt = 0, npair = 0;
       int e = s0;
       for (;;) {  // at least one step (a step of every section fits: cap >= min_cap)
-        long long add = 0;
-        for (int w = 0; w < kStmWarps; ++w) add += d[w] > e;
-        if (e > s0 && stm_piece_bytes(32ULL * (cnt + add)) > (unsigned long long)F.cap) break;
+        long long add = 0, addp = 0;
+        for (int w = 0; w < kStmWarps; ++w)
+          if (d[w] > e) { ++add; addp += ((e - s0) & 1) == 0; }  // a new slot-word pair
+        if (e > s0 && stm_piece_bytes(32ULL * (cnt + add), npair + addp) > (unsigned long long)F.cap)
+          break;
         cnt += add;
+        npair += addp;
         if (++e >= maxd) break;
       }
       unsigned short acc = 0;
@@ -1928,7 +1941,9 @@ void build_stream(scs_handle* h, int mat) {
       ptile.push_back(t);
       pstep0.push_back((unsigned short)s0);
       T.pslots.push_back(ns);
-      bytes += stm_piece_bytes(ns);
+      const unsigned pbyt = (unsigned)stm_piece_bytes(ns, (unsigned long long)npair);
+      T.pbytes.push_back(pbyt);
+      bytes += pbyt;
       ++npiece;
       ++np;
       s0 = e;
@@ -1971,7 +1986,21 @@ void build_stream(scs_handle* h, int mat) {
   dbg("stream layout mat=%d rows=%lld cols=%lld nnz=%lld W=%d S=%d NB=%d csr_sb=%lld pieces=%lld "
       "bytes=%llu (%.2f B/nnz)", mat, rows, cols, nz, F.W, F.S, F.NB, ncsr, npiece, bytes,
       (double)bytes / (double)nz);
-  for (int pair = 0; pair < 2; ++pair) build_stm_sched(h, mat, pair, T);
+  for (int pair = 0; pair < 2; ++pair)
+    build_stm_sched(h, mat, pair, T, 0, F.NB, h->ssch[mat][pair], h->sms);
+  // row-sharded A^T passes: also one schedule per row chunk, so the all-
+  // reduce of chunk c overlaps the SpMV of chunk c + 1 (at_pass); a few SMs
+  // stay free for the NCCL kernels
+  if (mat == 1 && h->sharded && h->at_chunks > 1) {
+    const int C = h->at_chunks;
+    const int G = std::max(1, h->sms - (int)env_ll("SCS_AT_FREE_SMS", 8));
+    for (int c = 0; c < C; ++c) {
+      const long long lo = F.NB * c / C, hi = F.NB * (c + 1) / C;
+      h->at_row[c] = std::min(F.rows, lo * kStmRS);
+      for (int pair = 0; pair < 2; ++pair) build_stm_sched(h, mat, pair, T, lo, hi, h->at_sch[c][pair], G);
+    }
+    h->at_row[C] = F.rows;
+  }
 }
 
 __global__ void k_hash_fill(double* x, long long n, unsigned seed) {
@@ -2045,13 +2074,24 @@ void setup_stream(scs_handle* h) {
   h->stm_pair = env_ll("SCS_STREAM_PAIR", 0) != 0;
   if (force == 0 || h->nnz == 0) return;
   if (force < 0 && h->nnz < 20000000LL) return;
+  h->at_chunks = h->sharded ? (int)std::max<long long>(1, std::min<long long>(
+                                    scs_handle::kMaxChunks, env_ll("SCS_AT_CHUNKS", 2)))
+                             : 1;
   size_t need = 0;
   for (int mat = 0; mat < 2; ++mat) {
     build_stream(h, mat);
     h->stm_m[mat] = true;
-    for (int pair = 0; pair < 2; ++pair)
-      if (h->ssch[mat][pair].splits > 1)
-        need = std::max<size_t>(need, (size_t)h->ssch[mat][pair].splits * h->sF[mat].rows * 2);
+    for (int pair = 0; pair < 2; ++pair) {
+      int sp = h->ssch[mat][pair].splits;
+      if (mat == 1)
+        for (int c = 0; c < h->at_chunks && h->at_chunks > 1; ++c) sp = std::max(sp, h->at_sch[c][pair].splits);
+      if (sp > 1) need = std::max<size_t>(need, (size_t)sp * h->sF[mat].rows * 2);
+    }
+  }
+  if (h->at_chunks > 1) {
+    CK(cudaStreamCreateWithFlags(&h->st_comm, cudaStreamNonBlocking));
+    for (int c = 0; c < h->at_chunks; ++c) CK(cudaEventCreateWithFlags(&h->ev_chunk[c], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_comm, cudaEventDisableTiming));
   }
   if (need) h->Pstm = dalloc<double>(h, need);
   if (env_ll("SCS_STREAM_CHECK", 0)) stm_selfcheck(h);
@@ -2167,8 +2207,21 @@ void at_pass(scs_handle* h, Epi epi) {
   EpiRaw<Epi> raw{};
   static_cast<Epi&>(raw) = epi;
   raw.T = h->Traw;
-  launch_mat(h, 1, raw);
-  allreduce(h, h->Traw, (size_t)n * Epi::NV);
+  if (h->at_chunks > 1 && h->stm_m[1] && ((uintptr_t)raw.xb & 15) == 0) {
+    // chunk c's raw products all-reduced on st_comm while chunk c + 1 runs
+    for (int c = 0; c < h->at_chunks; ++c) {
+      launch_stream<EpiRaw<Epi>::NV, EpiRaw<Epi>::STRIDE, EpiRaw<Epi>>(h, 1, raw, c);
+      CK(cudaEventRecord(h->ev_chunk[c], h->st));
+      CK(cudaStreamWaitEvent(h->st_comm, h->ev_chunk[c], 0));
+      const long long a = h->at_row[c], b = h->at_row[c + 1];
+      if (b > a) h->comm->allreduce(h->st_comm, h->Traw + a * Epi::NV, (size_t)(b - a) * Epi::NV);
+    }
+    CK(cudaEventRecord(h->ev_comm, h->st_comm));
+    CK(cudaStreamWaitEvent(h->st, h->ev_comm, 0));
+  } else {
+    launch_mat(h, 1, raw);
+    allreduce(h, h->Traw, (size_t)n * Epi::NV);
+  }
   k_rows<Epi><<<elem_grid(h, n), kBlock, 0, h->st>>>(h->Traw, n, 1, epi);
   h->launches++;
 }
@@ -3214,6 +3267,10 @@ void scs_destroy(scs_handle* h) {
   if (h->loop_arg) cudaFreeHost(h->loop_arg);
   if (h->st) cudaStreamDestroy(h->st);
   if (h->st_copy) cudaStreamDestroy(h->st_copy);
+  if (h->st_comm) cudaStreamDestroy(h->st_comm);
+  for (auto& e : h->ev_chunk)
+    if (e) cudaEventDestroy(e);
+  if (h->ev_comm) cudaEventDestroy(h->ev_comm);
   delete h->comm;
   delete h;
 }
