@@ -1630,7 +1630,6 @@ struct StmTiles {
   std::vector<long long> slots;       // per tile
   std::vector<unsigned long long> poff;
   std::vector<unsigned> pslots;
-  std::vector<unsigned> pbytes;       // per piece
   std::vector<long long> nnz_sb;      // per sub-block (CSR units' cost)
 };
 
@@ -1747,7 +1746,7 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T, long l
             const long long p = T.pf[t] + j;
             StmCmd c{};
             c.off = T.poff[p];
-            c.bytes = T.pbytes[p];
+            c.bytes = (unsigned)stm_piece_bytes(T.pslots[p]);
             c.slab = (unsigned)s;
             c.row0 = u.sb0 * kStmRS;
             c.flags = pf;
@@ -1790,7 +1789,7 @@ void build_stream(scs_handle* h, int mat) {
   const bool wforced = getenv("SCS_STREAM_W") != nullptr;
   long long W = std::min<long long>(kStmMaxW, std::max<long long>(32, env_ll("SCS_STREAM_W", 4096)));  // >= 32: padding gathers column = lane
   F.cap = (int)(env_ll("SCS_STREAM_CAP", 0) & ~15LL);
-  const int min_cap = (int)stm_piece_bytes(32 * kStmWarps, kStmWarps);
+  const int min_cap = (int)stm_piece_bytes(32 * kStmWarps);
   if (F.cap > 0 && F.cap < min_cap) F.cap = (min_cap + 15) & ~15;
   F.NB = (int)((rows + kStmRS - 1) / kStmRS);
   long long ntile = 0, nsec = 0;
@@ -1917,16 +1916,13 @@ void build_stream(scs_handle* h, int mat) {
     T.pf[t] = npiece;
     int np = 0;
     for (int s0 = 0; s0 < maxd;) {
-      long long cnt = 0, npair = 0;
+      long long cnt = 0;
       int e = s0;
       for (;;) {  // at least one step (a step of every section fits: cap >= min_cap)
-        long long add = 0, addp = 0;
-        for (int w = 0; w < kStmWarps; ++w)
-          if (d[w] > e) { ++add; addp += ((e - s0) & 1) == 0; }  // a new slot-word pair
-        if (e > s0 && stm_piece_bytes(32ULL * (cnt + add), npair + addp) > (unsigned long long)F.cap)
-          break;
+        long long add = 0;
+        for (int w = 0; w < kStmWarps; ++w) add += d[w] > e;
+        if (e > s0 && stm_piece_bytes(32ULL * (cnt + add)) > (unsigned long long)F.cap) break;
         cnt += add;
-        npair += addp;
         if (++e >= maxd) break;
       }
       unsigned short acc = 0;
@@ -1941,9 +1937,7 @@ void build_stream(scs_handle* h, int mat) {
       ptile.push_back(t);
       pstep0.push_back((unsigned short)s0);
       T.pslots.push_back(ns);
-      const unsigned pbyt = (unsigned)stm_piece_bytes(ns, (unsigned long long)npair);
-      T.pbytes.push_back(pbyt);
-      bytes += pbyt;
+      bytes += stm_piece_bytes(ns);
       ++npiece;
       ++np;
       s0 = e;

@@ -53,16 +53,10 @@ constexpr int kStmWarps = kStmRS / kStmSecRows;  // 16 consumer warps
 constexpr int kStmThreads = (kStmWarps + 1) * 32;
 constexpr int kStmHdr = 48;         // piece header bytes: u32 nslots, u16 wsec[17]
 constexpr int kStmOwn = 32 * 16;    // + per warp section, per lane: owner lane of its overflow slots
-constexpr int kStmData = kStmHdr + kStmOwn;  // values start here; then the slot words
+constexpr int kStmData = kStmHdr + kStmOwn;  // values start here; then u16 slot words
 constexpr int kStmMaxW = 4096;      // slot word column field: 12 bits
-// Piece bytes: header, ns fp64 values (step-major: slot (k, lane) at
-// 32 k + lane), then the 16-bit slot words interleaved by step pairs: per
-// section, pair g of its steps is 32 u32 words (lane l: word of step 2g in
-// the low half, step 2g + 1 in the high half), so one 4-byte load per lane
-// fetches two steps' words.  npair = sum over sections of ceil(steps / 2).
-__host__ __device__ constexpr unsigned long long stm_piece_bytes(unsigned long long ns,
-                                                                 unsigned long long npair) {
-  return kStmData + 8ULL * ns + 128ULL * npair;
+__host__ __device__ constexpr unsigned long long stm_piece_bytes(unsigned long long ns) {
+  return kStmData + 10ULL * ns;
 }
 constexpr int kStmAccBytes = 2 * kStmRS * 8;
 constexpr int kStmMaxStages = 8;
@@ -170,17 +164,12 @@ __device__ __forceinline__ void stm_rows(Epi& epi, double* a, long long r0, int 
 // a nonzero value, which skips them -- and explicit zeros, whose products
 // add nothing to a row sum (x + 0 = x, 0 + -0 = 0).
 template <int NV, int STRIDE, int U, bool MASK>
-__device__ __forceinline__ void stm_steps(const double* vals, const unsigned* idx2, int k,
+__device__ __forceinline__ void stm_steps(const double* vals, const unsigned short* idx, int k,
                                           int k1, const double* xs, double* a, unsigned own) {
-  // k: even step of the section (section-relative); vals / idx2 at its start
   const int lane = threadIdx.x & 31;
   double pr[U][NV];
   unsigned rw[U];
   bool live[U];
-  unsigned wd[(U + 1) / 2];
-#pragma unroll
-  for (int q = 0; q < (U + 1) / 2; ++q)  // slot words of two steps per load
-    wd[q] = (!MASK || k + 2 * q < k1) ? idx2[((k >> 1) + q) * 32 + lane] : 0u;
 #pragma unroll
   for (int u = 0; u < U; ++u) {  // every load of the batch before its stores
     live[u] = false;
@@ -189,7 +178,7 @@ __device__ __forceinline__ void stm_steps(const double* vals, const unsigned* id
     for (int t = 0; t < NV; ++t) pr[u][t] = 0.0;
     if (MASK && k + u >= k1) continue;  // warp-uniform: no load issued past the section's end
     const double v = vals[(k + u) * 32 + lane];
-    const unsigned id = (u & 1) ? wd[u >> 1] >> 16 : wd[u >> 1] & 0xffffu;
+    const unsigned id = idx[(k + u) * 32 + lane];
     live[u] = v != 0.0;
     rw[u] = ((id >> 12) & 7u) << 5 | ((id >> 15) ? own : (unsigned)lane);
     const unsigned col = id & 0xfffu;
@@ -207,11 +196,11 @@ __device__ __forceinline__ void stm_steps(const double* vals, const unsigned* id
 // masked batch (sections hold ~4-9 steps per piece), so a section's tail
 // keeps its loads in flight together instead of running step by step.
 template <int NV, int STRIDE>
-__device__ __forceinline__ void stm_piece(const double* vals, const unsigned* idx2, int nk,
-                                          const double* xs, double* a, unsigned own) {
-  int k = 0;
-  for (; k + 4 <= nk; k += 4) stm_steps<NV, STRIDE, 4, false>(vals, idx2, k, nk, xs, a, own);
-  if (k < nk) stm_steps<NV, STRIDE, 3, true>(vals, idx2, k, nk, xs, a, own);
+__device__ __forceinline__ void stm_piece(const double* vals, const unsigned short* idx, int k0,
+                                          int k1, const double* xs, double* a, unsigned own) {
+  int k = k0;
+  for (; k + 4 <= k1; k += 4) stm_steps<NV, STRIDE, 4, false>(vals, idx, k, k1, xs, a, own);
+  if (k < k1) stm_steps<NV, STRIDE, 3, true>(vals, idx, k, k1, xs, a, own);
 }
 
 // CSR unit rows [r0, rend) of this warp, L lanes per row (warp-uniform loop)
@@ -361,26 +350,14 @@ __global__ void __launch_bounds__(kStmThreads, 1)
         const unsigned nslots = *reinterpret_cast<const unsigned*>(blob);
         if (nslots) {
           const unsigned short* wsec = reinterpret_cast<const unsigned short*>(blob + 4);
-          // section step offsets -> this section's slot-word pair base: an
-          // exclusive warp scan of ceil(steps / 2) over the 16 sections
-          const int wl = lane <= kStmWarps ? wsec[lane] : 0;
-          const int wn = __shfl_down_sync(0xffffffffu, wl, 1);
-          int pc = lane < kStmWarps ? (wn - wl + 1) >> 1 : 0;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, pc, o);
-            if (lane >= o) pc += v;
-          }
-          const int k0 = __shfl_sync(0xffffffffu, wl, warp);
-          const int k1 = __shfl_sync(0xffffffffu, wl, warp + 1);
-          const int pb = warp ? __shfl_sync(0xffffffffu, pc, warp - 1) : 0;
+          const int k0 = wsec[warp], k1 = wsec[warp + 1];
           const unsigned own = blob[kStmHdr + warp * 32 + lane];
-          const double* vals = reinterpret_cast<const double*>(blob + kStmData) + (size_t)k0 * 32;
-          const unsigned* idx2 =
-              reinterpret_cast<const unsigned*>(blob + kStmData + 8 * (size_t)nslots) + (size_t)pb * 32;
+          const double* vals = reinterpret_cast<const double*>(blob + kStmData);
+          const unsigned short* idx =
+              reinterpret_cast<const unsigned short*>(blob + kStmData + 8 * (size_t)nslots);
           const double* xs = xbuf0 + (size_t)c.xbuf * (xbytes / 8);
           double* a = acc + ((size_t)c.half * kStmRS + (size_t)warp * kStmSecRows) * NV;
-          stm_piece<NV, STRIDE>(vals, idx2, k1 - k0, xs, a, own);
+          stm_piece<NV, STRIDE>(vals, idx, k0, k1, xs, a, own);
         }
       }
       __syncwarp();
@@ -757,13 +734,12 @@ __global__ void k_stm_init(unsigned char* blob, const unsigned long long* poff, 
     const long long sec0 = ptile[p] * kStmWarps;
     for (int q = lane; q < kStmWarps * 32; q += 32) b[kStmHdr + q] = hown[sec0 * 32 + q];
     double* v = reinterpret_cast<double*>(b + kStmData);
-    unsigned* id2 = reinterpret_cast<unsigned*>(b + kStmData + 8 * (size_t)ns);
-    const unsigned short* ws = pwsec + p * (kStmWarps + 1);
-    unsigned npair = 0;
-    for (int q = 0; q < kStmWarps; ++q) npair += (unsigned)(ws[q + 1] - ws[q] + 1) >> 1;
+    unsigned short* id = reinterpret_cast<unsigned short*>(b + kStmData + 8 * (size_t)ns);
     // padding gathers column = lane: distinct banks, no conflict with the real entries
-    for (unsigned k = lane; k < ns; k += 32) v[k] = 0.0;
-    for (unsigned k = lane; k < 32 * npair; k += 32) id2[k] = (unsigned)lane | (unsigned)lane << 16;
+    for (unsigned k = lane; k < ns; k += 32) {
+      v[k] = 0.0;
+      id[k] = (unsigned short)lane;
+    }
   }
 }
 
@@ -790,15 +766,11 @@ __global__ void k_stm_scatter(const int* sec, const int* slot, long long nnz, co
     const int kk = k - pstep0[piece];
     unsigned char* bl = blob + poff[piece];
     const unsigned ns = pslots[piece];
-    const unsigned short* ws = pwsec + piece * (kStmWarps + 1);
-    const long long at = ((long long)ws[w] + kk) * 32 + lane;
-    long long pb = 0;  // slot-word pairs of the sections before w
-    for (int q = 0; q < w; ++q) pb += (ws[q + 1] - ws[q] + 1) >> 1;
-    const long long wat = ((pb + (kk >> 1)) * 32 + lane) * 2 + (kk & 1);
+    const long long at = ((long long)pwsec[piece * (kStmWarps + 1) + w] + kk) * 32 + lane;
     const int s = perm[e];
     const unsigned rl = (unsigned)(rowid[s] % kStmSecRows);
     reinterpret_cast<double*>(bl + kStmData)[at] = val[s];
-    reinterpret_cast<unsigned short*>(bl + kStmData + 8 * (size_t)ns)[wat] =
+    reinterpret_cast<unsigned short*>(bl + kStmData + 8 * (size_t)ns)[at] =
         (unsigned short)((unsigned)(ci[s] % W) | ((rl >> 5) << 12) | (ovf << 15));
   }
 }
