@@ -302,7 +302,19 @@ __global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows
     } else {
 #pragma unroll
       for (int t = 0; t < Epi::NV; ++t) s[t] = T[j * Epi::NV + t];
-      for (int b = 1; b < nsum; ++b)
+      int b = 1;
+      for (; b + 4 <= nsum; b += 4) {  // four partials' loads in flight, added in order
+        double v[4][Epi::NV];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int t = 0; t < Epi::NV; ++t) v[q][t] = T[((b + q) * rows + j) * Epi::NV + t];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int t = 0; t < Epi::NV; ++t) s[t] += v[q][t];
+      }
+      for (; b < nsum; ++b)
 #pragma unroll
         for (int t = 0; t < Epi::NV; ++t) s[t] += T[(b * rows + j) * Epi::NV + t];
     }

@@ -1525,8 +1525,10 @@ void launch_spmv(scs_handle* h, const Csr& M, int L, const Epi& epi) {
 // sub-blocks share every slab load), NV = 2 passes single sub-blocks; the
 // shared-memory ring gets as many 'cap'-byte stages (<= 4) as fit beside
 // the accumulators and the two slab buffers.
+// Returns the schedule's split count; with combine = false and splits > 1
+// the split partials are left in Pstm for the caller's own epilogue kernel.
 template <int NV, int STRIDE, class Epi>
-void launch_stream(scs_handle* h, int mat, const Epi& epi, int chunk = -1) {
+int launch_stream(scs_handle* h, int mat, const Epi& epi, int chunk = -1, bool combine = true) {
   const Stm& F = h->sF[mat];
   const int pair = (NV == 1 && h->stm_pair) ? 1 : 0;  // NV = 1: pairs of sub-blocks share slab loads
   const auto& S = chunk < 0 ? h->ssch[mat][pair] : h->at_sch[chunk][pair];
@@ -1560,11 +1562,12 @@ void launch_stream(scs_handle* h, int mat, const Epi& epi, int chunk = -1) {
                                                               h->Pstm, NS, NB, accb);
   CK(cudaGetLastError());
   h->launches++;
-  if (S.splits > 1) {
+  if (S.splits > 1 && combine) {
     k_split_combine<Epi><<<elem_grid(h, r1 - r0), kBlock, 0, h->st>>>(h->Pstm, S.splits, F.rows, r0,
                                                                      r1, epi);
     h->launches++;
   }
+  return S.splits;
 }
 
 // SpMV with the matrix A (mat = 0) or A^T (mat = 1): streamed tiles or the
@@ -2836,8 +2839,13 @@ void enqueue_iteration(scs_handle* h) {
       sf.V = V;
       sf.xb = V.Yc;
       sf.rgate = -RA;
-      launch_mat(h, 1, sf);
-      k_rows<EpiAtFirst1><<<elem_grid(h, h->n), kBlock, 0, h->st>>>(V.Sv, h->n, 1, e1);
+      int sp = 1;
+      if (h->stm_m[1] && ((uintptr_t)sf.xb & 15) == 0)  // split partials summed by k_rows below
+        sp = launch_stream<1, 1, EpiStoreF>(h, 1, sf, -1, false);
+      else
+        launch_mat(h, 1, sf);
+      k_rows<EpiAtFirst1><<<elem_grid(h, h->n), kBlock, 0, h->st>>>(sp > 1 ? h->Pstm : V.Sv, h->n, sp,
+                                                                     e1);
       h->launches++;
     } else {
       at_pass(h, e1);

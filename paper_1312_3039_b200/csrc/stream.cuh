@@ -3,8 +3,8 @@
 // Why: the CSR kernels are bound by the L2 slice throughput, not by HBM --
 // every random gather x[col] costs a 32-byte sector for 8-16 useful bytes
 // (config 5: 32 GB of gather sectors + 12 GB of matrix per pass,
-// profiles/r01_ncu_c5_spmv_banded.txt).  The earlier slab-tiled kernel
-// (tiled.cuh) moved the gathers into shared memory but loaded the matrix
+// profiles/r01_ncu_c5_spmv_banded.txt).  r01's slab-tiled kernel (retired
+// in r02) moved the gathers into shared memory but loaded the matrix
 // with ordinary per-chunk loads whose latency it could not cover at
 // config 5's ~1-2 entries per row segment.  This kernel keeps the idea and
 // moves every byte of the matrix and of the gathered vector with the
@@ -14,17 +14,19 @@
 //  * format (built once, after equilibration): rows in sub-blocks of
 //    kStmRS = 4096 rows = 16 warp sections of 256 rows; columns in slabs of
 //    W columns.  A tile = (sub-block, slab).  Inside a warp section the row
-//    segments (a row's entries in the slab, column order kept) are packed
-//    onto 32 lanes by first-fit-decreasing into a depth of D steps; step k
-//    of all 32 lanes is contiguous (coalesced shared-memory reads, no
-//    padding but the lane tails).  Every tile is cut into pieces of at
-//    most `cap` bytes (a piece = a step range of every section) and each
-//    piece is one contiguous blob: header, fp64 values, u32 (local row << 16
-//    | column - slab start).  Sub-blocks whose tiles are too sparse to pay
+//    entries are placed on 32 lanes x D steps: the rows 32 j + l of a
+//    section are pinned to lane l (overflow entries go to free slots of
+//    other lanes, k_stm_pin), step k of all 32 lanes is contiguous.  Every
+//    tile is cut into pieces of at most `cap` bytes (a piece = a step range
+//    of every section; normally the whole tile) and each
+//    piece is one contiguous blob: header, owner table, fp64 values, u16
+//    slot words (column - slab start | j << 12 | overflow << 15).  Sub-
+//    blocks whose tiles are too sparse to pay
 //    for a slab load (config 5: A^T rows of the t-variables, two entries
 //    each) stay CSR units, computed from the CSR arrays by the consumers;
-//  * schedule (host, at setup): a unit = one sub-block (NV = 2) or a pair of
-//    sub-blocks sharing the slab loads (NV = 1), optionally split over slab
+//  * schedule (host, at setup): a unit = one sub-block (or, with
+//    SCS_STREAM_PAIR=1, a pair of sub-blocks sharing the slab loads of an
+//    NV = 1 pass), optionally split over slab
 //    ranges when there are too few units for 148 SMs; units are placed on
 //    persistent CTAs by longest-processing-time first, and each CTA gets a
 //    flat command list (one command per piece, in order);
@@ -32,14 +34,16 @@
 //    stage, the bulk copy of the piece and -- when the slab changes -- of
 //    the slab of the gathered vector (double-buffered) onto a full
 //    mbarrier with expect_tx; 16 consumer warps wait on it, each walks its
-//    own section (lane-local running row sum, flushed into a shared
-//    accumulator when the row changes: each row lives in exactly one lane
-//    of one warp per piece, so updates are exclusive and their order is
-//    fixed -- deterministic), then releases the stage on an empty mbarrier.
+//    own section four steps at a time and adds every product into the
+//    shared accumulator of its row (the rows of a step are distinct, so the
+//    updates need no atomics and their order is fixed -- deterministic),
+//    then releases the stage on an empty mbarrier.
 //    At the end of a unit each warp runs the pass's per-row epilogue
 //    (Epi::row) over its own rows -- or writes split partials that
 //    k_split_combine sums in split order -- and the CTA's reductions go
 //    through the usual deterministic grid_sum_last.
+//  (r02: 4096-column slabs with a 12-bit column field, a local search over
+//  slot placement, whole-tile pieces; DESIGN.md §5.1 has the measurements.)
 #pragma once
 
 #include "common.cuh"
@@ -410,9 +414,22 @@ __global__ void __launch_bounds__(kBlock) k_split_combine(const double* P, int s
     double s[NV];
 #pragma unroll
     for (int t = 0; t < NV; ++t) s[t] = 0.0;
-    for (int sp = 0; sp < splits; ++sp)
+    // eight splits' loads in flight at a time, added in split order
+    int sp = 0;
+    for (; sp + 8 <= splits; sp += 8) {
+      double v[8][NV];
 #pragma unroll
-      for (int t = 0; t < NV; ++t) s[t] += P[((long long)sp * rows + j) * NV + t];
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int t = 0; t < NV; ++t) v[q][t] = __ldcs(P + ((long long)(sp + q) * rows + j) * NV + t);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int t = 0; t < NV; ++t) s[t] += v[q][t];
+    }
+    for (; sp < splits; ++sp)
+#pragma unroll
+      for (int t = 0; t < NV; ++t) s[t] += __ldcs(P + ((long long)sp * rows + j) * NV + t);
     epi.row(j, s, pre, red);
   }
   epi.extra(red);

@@ -54,6 +54,7 @@ int pin(std::vector<uint64_t>& key, std::vector<int>& slot, int* hown_out, int p
       unsigned allow = 0;
       for (int c = 0; c < 32; ++c)
         if (c != l && (host[c] < 0 || host[c] == l)) allow |= 1u << c;
+      if (partner_pref == 2) allow &= 1u << (l ^ 16);  // strict: partner lane only
       const unsigned partner = partner_pref ? ((1u << (l ^ 16)) & allow) : 0u;
       int n = 0;
       for (int k = D - 1; k >= 0 && n < o; --k)
@@ -262,8 +263,9 @@ int main(int argc, char** argv) {
     ents += E;
   }
   const double per32 = 32.0 / ents;
-  printf("search=%d W=%d E=%.0f partner=%d: slots/entry %.3f  steps/32ent %.3f | per 32 entries: gather %.2f  acc(rd) %.2f  vals %.2f idx %.2f  fails %.0f\n",
+  const double tot = wf_g * per32 + 2 * wf_r * per32 + 3 * steps * per32 + (10.0 * slots / ents) * 32 / 128 + 2.2;
+  printf("search=%d W=%d E=%.0f partner=%d: slots/entry %.3f  steps/32ent %.3f | per 32 entries: gather %.2f  acc(rd) %.2f  vals %.2f idx %.2f  fails %.0f  TOTAL %.2f\n",
          search, W, E_mean, partner, slots / ents, steps * per32, wf_g * per32, wf_r * per32, 2 * steps * per32,
-         steps * per32, fails);
+         steps * per32, fails, tot);
   return 0;
 }
