@@ -291,12 +291,11 @@ __global__ void __launch_bounds__(kStmThreads, 1)
         if (i >= NS) mbar_wait(empty + st, ph ^ 1u);
         const bool tile = bytes > 0 && !(fl & STM_CSR);
         unsigned slab_bytes = 0;
-        long long cstart = 0;
+        long long cstart = 0, jlast = -1;
         if (tile && (long long)slab != slab_cur) {
           if (NB == 2) xb ^= 1;
           else xb = 0;  // one buffer: wait below for the last stage that read it
-          const long long jlast = xb ? last1 : last0;
-          if (jlast >= 0 && jlast > i - NS) mbar_wait(empty + (int)(jlast % NS), (unsigned)((jlast / NS) & 1));
+          jlast = xb ? last1 : last0;
           slab_cur = slab;
           cstart = (long long)slab * F.W;
           const long long wc = F.cols - cstart < F.W ? F.cols - cstart : F.W;
@@ -305,6 +304,10 @@ __global__ void __launch_bounds__(kStmThreads, 1)
         if (tile) {
           if (xb) last1 = i; else last0 = i;
         }
+        // the piece is issued as soon as its stage is free; the slab copy
+        // (same full barrier) only once the slab buffer's last reader has
+        // released it -- with one stage per slab, waiting for the buffer
+        // before the piece would cap the ring at two pieces in flight
         if (lane == 0) {
           StmCtl c;
           c.row0 = row0;
@@ -315,13 +318,16 @@ __global__ void __launch_bounds__(kStmThreads, 1)
           sctl[st] = c;
           if (tile) {
             mbar_arrive_tx(full + st, slab_bytes + bytes);
-            if (slab_bytes)
-              bulk_g2s_plain(xbuf0 + (size_t)xb * (xbytes / 8), epi.xb + cstart * STRIDE, slab_bytes,
-                             full + st);
             bulk_g2s(stages + (size_t)st * F.cap, F.blob + off, bytes, full + st, pol);
           } else {
             mbar_arrive(full + st);
           }
+        }
+        if (slab_bytes) {
+          if (jlast >= 0 && jlast > i - NS) mbar_wait(empty + (int)(jlast % NS), (unsigned)((jlast / NS) & 1));
+          if (lane == 0)
+            bulk_g2s_plain(xbuf0 + (size_t)xb * (xbytes / 8), epi.xb + cstart * STRIDE, slab_bytes,
+                           full + st);
         }
         __syncwarp();
       }
