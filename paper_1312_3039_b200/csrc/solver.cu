@@ -1403,6 +1403,7 @@ struct scs_handle {
   // state (set by do_finish; the extraction then needs no matrix pass)
   bool prod_current = false;
   cudaStream_t st_copy = nullptr;       // extraction D2H overlapped with the point residuals
+  void* stage_buf[2] = {nullptr, nullptr};  // pinned H2D staging during setup
   std::vector<DevBuf> bufs;
   int grid_full = 148 * 4;
 };
@@ -1416,9 +1417,11 @@ bool dbg_on() {
 }
 void dbg(const char* fmt, ...) {
   if (!dbg_on()) return;
+  static const auto t0 = std::chrono::steady_clock::now();
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   va_list ap;
   va_start(ap, fmt);
-  fprintf(stderr, "[scs] ");
+  fprintf(stderr, "[scs %9.1f ms] ", ms);
   vfprintf(stderr, fmt, ap);
   fprintf(stderr, "\n");
   fflush(stderr);
@@ -1430,23 +1433,84 @@ void set_global_err(const std::string& s) {
   g_err = s;
 }
 
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync
+// on the solver stream), which keeps freed blocks for reuse: the setup's
+// multi-GB transients (radix-sort keys, permutations, format staging) are
+// allocated and freed several times, and a plain cudaFree of such a block
+// synchronises and unmaps (~1 s per setup at config 5).
 template <class T>
 T* dalloc(scs_handle* h, size_t count) {
   void* p = nullptr;
   const size_t bytes = std::max<size_t>(count, 1) * sizeof(T) + 16;  // +16: bulk-copy tails
-  cudaError_t e = cudaMalloc(&p, bytes);
+  cudaError_t e = cudaMallocAsync(&p, bytes, h->st);
   if (e != cudaSuccess)
-    throw Fail{SCS_ENOMEM, "cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e)};
+    throw Fail{SCS_ENOMEM, "cudaMallocAsync(" + std::to_string(bytes) + " bytes): " +
+                               cudaGetErrorString(e)};
   h->bufs.push_back({p, bytes});
   return (T*)p;
 }
 void dfree(scs_handle* h, void* p) {
   if (!p) return;
   for (auto& b : h->bufs)
-    if (b.p == p) { cudaFree(p); b.p = nullptr; }
+    if (b.p == p) { cudaFreeAsync(p, h->st); b.p = nullptr; }
 }
+// Large copies from pageable host memory (the caller's numpy arrays at
+// setup: 16 GB at config 5): staged through two pinned 64-MB buffers that
+// several host threads fill while the previous buffer's copy is in flight
+// (pageable cudaMemcpy runs at a single staging thread's memcpy rate).
+long long env_ll(const char* name, long long dflt);
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+void h2d_staged(scs_handle* h, void* dst, const void* src, size_t bytes) {
+  constexpr size_t kChunk = 64ull << 20;
+  static const int nthr = std::max(1, std::min(8, (int)std::thread::hardware_concurrency()));
+  void** buf = h->stage_buf;  // allocated once per handle, freed at the end of setup
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  for (int i = 0; i < 2; ++i)
+    if (!buf[i]) CK(cudaMallocHost(&buf[i], kChunk));
+  CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  const char* s = static_cast<const char*>(src);
+  char* d = static_cast<char*>(dst);
+  int k = 0;
+  for (size_t off = 0; off < bytes; off += kChunk, k ^= 1) {
+    const size_t n = std::min(kChunk, bytes - off);
+    CK(cudaEventSynchronize(ev[k]));  // the copy out of this buffer (two chunks ago) is done
+    char* b = static_cast<char*>(buf[k]);
+    const size_t per = (n + nthr - 1) / nthr;
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthr; ++t) {
+      const size_t a = std::min(n, t * per), e = std::min(n, a + per);
+      if (e > a) th.emplace_back([=] { std::memcpy(b + a, s + off + a, e - a); });
+    }
+    for (auto& x : th) x.join();
+    CK(cudaMemcpyAsync(d + off, b, n, cudaMemcpyHostToDevice, h->st));
+    CK(cudaEventRecord(ev[k], h->st));
+  }
+  CK(cudaStreamSynchronize(h->st));
+  for (int i = 0; i < 2; ++i) cudaEventDestroy(ev[i]);
+}
+
+void free_stage(scs_handle* h) {
+  for (auto& b : h->stage_buf)
+    if (b) { cudaFreeHost(b); b = nullptr; }
+}
+
 template <class T>
 void h2d(scs_handle* h, T* dst, const T* src, size_t count) {
+  static const bool staged = env_ll("SCS_H2D_STAGED", 1) != 0;
+  if (staged && count * sizeof(T) >= (256ull << 20) && !host_pinned(src)) {
+    h2d_staged(h, dst, src, count * sizeof(T));
+    return;
+  }
   if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, h->st));
 }
 template <class T>
@@ -1795,6 +1859,31 @@ void build_stream(scs_handle* h, int mat) {
   const int min_cap = (int)stm_piece_bytes(32 * kStmWarps);
   if (F.cap > 0 && F.cap < min_cap) F.cap = (min_cap + 15) & ~15;
   F.NB = (int)((rows + kStmRS - 1) / kStmRS);
+  std::vector<long long> rp_h(rows + 1);
+  d2h(h, rp_h.data(), M.rp, rows + 1);
+  CK(cudaStreamSynchronize(h->st));
+  if (!wforced && nz > 0 && env_ll("SCS_STREAM_PREDICT", 1)) {
+    // expected section depth in the densest slab (column counts from the
+    // other CSR's row pointers): narrow the slab up front where sub-blocks
+    // would exceed the pin depth, instead of building and rebuilding (the
+    // build below still narrows further if sections get flagged)
+    const Csr& O = mat == 0 ? h->At : h->A;
+    std::vector<long long> orp(cols + 1);
+    d2h(h, orp.data(), O.rp, cols + 1);
+    CK(cudaStreamSynchronize(h->st));
+    for (; W > 256; W /= 4) {
+      long long smax = 0;
+      for (long long c0 = 0; c0 < cols; c0 += W) smax = std::max(smax, orp[std::min(cols, c0 + W)] - orp[c0]);
+      const double frac = (double)smax / (double)nz;
+      long long deep = 0, nsb = 0;
+      for (long long r0 = 0; r0 < rows; r0 += kStmRS) {
+        const long long e = rp_h[std::min(rows, r0 + kStmRS)] - rp_h[r0];
+        nsb += e > 0;
+        deep += (double)e / kStmWarps * frac / 32.0 > 96.0;
+      }
+      if (deep * 1000 <= nsb) break;
+    }
+  }
   long long ntile = 0, nsec = 0;
   int *rowid = nullptr, *perm = nullptr, *sec = nullptr, *slot = nullptr;
   unsigned char* hown = nullptr;
@@ -1829,6 +1918,7 @@ void build_stream(scs_handle* h, int mat) {
   }
   dfree(h, key);
   dfree(h, perm_in);
+  dbg("stream mat=%d: sorted", mat);
   // 2. sections, slots (pinned / overflow) and depths
   sec = dalloc<int>(h, nz);
   k_stm_sec<<<elem_grid(h, nz), kBlock, 0, h->st>>>(skey, nz, sec);
@@ -1842,6 +1932,7 @@ void build_stream(scs_handle* h, int mat) {
   D.assign(nsec, 0);
   d2h(h, D.data(), depth, nsec);
   CK(cudaStreamSynchronize(h->st));
+  dbg("stream mat=%d: pinned", mat);
   dfree(h, depth);
   dfree(h, sec_ptr);
   dfree(h, skey);
@@ -1872,9 +1963,6 @@ void build_stream(scs_handle* h, int mat) {
     if (F.cap < min_cap) F.cap = (min_cap + 15) & ~15;
   }
   dbg("stream piece cap mat=%d: %d bytes", mat, F.cap);
-  std::vector<long long> rp_h(rows + 1);
-  d2h(h, rp_h.data(), M.rp, rows + 1);
-  CK(cudaStreamSynchronize(h->st));
   // 5. host: tiled sub-blocks, pieces, blob offsets
   StmTiles T;
   T.NB = F.NB;
@@ -1947,6 +2035,7 @@ void build_stream(scs_handle* h, int mat) {
     }
     T.np[t] = np;
   }
+  dbg("stream mat=%d: piece table (%lld pieces)", mat, npiece);
   // 6. device blob
   unsigned char* blob = dalloc<unsigned char>(h, std::max<unsigned long long>(bytes, 16));
   long long* d_pf = dalloc<long long>(h, ntile);
@@ -3264,8 +3353,18 @@ void scs_destroy(scs_handle* h) {
   cudaSetDevice(h->dev);
   destroy_graphs(h);
   for (auto& b : h->bufs)
-    if (b.p) cudaFree(b.p);
+    if (b.p) {
+      if (h->st) cudaFreeAsync(b.p, h->st);
+      else cudaFree(b.p);
+    }
+  if (h->st) cudaStreamSynchronize(h->st);
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, h->dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    cudaGetLastError();
+  }
   if (h->ctl_h) cudaFreeHost(h->ctl_h);
+  free_stage(h);
   if (h->loop_arg) cudaFreeHost(h->loop_arg);
   if (h->st) cudaStreamDestroy(h->st);
   if (h->st_copy) cudaStreamDestroy(h->st_copy);
@@ -3327,6 +3426,12 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     if (h->grid_full > kMaxGrid) h->grid_full = kMaxGrid;
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&h->st_copy, cudaStreamNonBlocking));
+    {
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, h->dev));
+      unsigned long long keep = ~0ull;  // freed blocks stay in the pool (trimmed at destroy)
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     {
       // opt-in (SCS_L2_PERSIST=1): measured slower at config 5 -- the
       // set-aside shrinks the L2 left for everything else
@@ -3478,6 +3583,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     k_recip<<<elem_grid(h, n), kBlock, 0, h->st>>>(h->E, n, (double*)V.Einv);
     dbg("equilibrated mean_col=%g mean_row=%g", h->mean_col, h->mean_row);
     setup_stream(h);
+    dbg("streamed format built");
     setup_pcg(h);
     setup_split(h);
     scale_vectors(h);
@@ -3485,6 +3591,7 @@ int scs_create(const scs_problem* P, const scs_settings* S, const scs_dist* dist
     solve_g(h);
     dbg("g solved denom=%g cg=%lld", h->ctl_h->denom, h->ctl_h->cg_iters_total);
     build_graph(h);
+    free_stage(h);
     dbg("graph built launches/iter=%lld", h->launches_per_iter);
     CK(cudaStreamSynchronize(h->st));
   });
@@ -3705,6 +3812,12 @@ int scs_project_cone(int64_t z, int64_t l, int64_t nq, const int64_t* q, int64_t
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&h->st_copy, cudaStreamNonBlocking));
+    {
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, h->dev));
+      unsigned long long keep = ~0ull;  // freed blocks stay in the pool (trimmed at destroy)
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
     h->grid_full = std::min(h->sms * (2048 / kBlock), kMaxGrid);
     long long m = z + l + 3 * ep;
