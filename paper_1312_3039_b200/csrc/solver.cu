@@ -3058,7 +3058,6 @@ bool build_loop_graph(scs_handle* h) {
   if ((e = cudaGraphAddNode(&wnode, g, &arm, 1, &wp)) != cudaSuccess) return fail("while", e);
   cudaGraph_t body = wp.conditional.phGraph_out[0];
   cudaGraphNode_t last = nullptr;
-  long long tmp = 0;
   const long long before = h->launches;
   if (h->R > 0) {
     cudaGraphConditionalHandle sh;
@@ -3096,7 +3095,6 @@ bool build_loop_graph(scs_handle* h) {
   }
   k_loop_next<<<1, 1, 0, h->st>>>(h->ctl, wh);
   if ((e = cudaStreamEndCapture(h->st, &body)) != cudaSuccess) return fail("end body", e);
-  (void)tmp;
   h->launches = before;
   cudaGraphExec_t ex = nullptr;
   if ((e = cudaGraphInstantiate(&ex, g, 0)) != cudaSuccess) return fail("instantiate", e);

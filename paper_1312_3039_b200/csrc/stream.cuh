@@ -62,9 +62,7 @@ constexpr int kStmMaxW = 4096;      // slot word column field: 12 bits
 __host__ __device__ constexpr unsigned long long stm_piece_bytes(unsigned long long ns) {
   return kStmData + 10ULL * ns;
 }
-constexpr int kStmAccBytes = 2 * kStmRS * 8;
 constexpr int kStmMaxStages = 8;
-constexpr int kStmPin = kStmSecRows / 32;  // rows pinned to each lane
 
 enum : unsigned short { STM_END = 1, STM_CSR = 2, STM_PAIR = 4, STM_TILE = 8, STM_CSR32 = 16 };
 

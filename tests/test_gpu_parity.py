@@ -363,3 +363,35 @@ def test_pinned_buffers_roundtrip():
     plain = ws.solve(warm_start=(np.array(sol.x), np.array(sol.y), np.array(sol.s)))
     assert again.info.iterations == plain.info.iterations
     assert np.array_equal(again.x, plain.x) and np.array_equal(again.y, plain.y)
+
+
+def test_query_and_cache_counter():
+    """scs_query: the production format switch (CSR below 2e7 nonzeros), the
+    per-iteration launch count, and EmbeddingCache.cg_iters_total kept in
+    step with the reference's (setup solve, then every solve; update_vectors
+    re-solves g, embedding.py:145-162)."""
+    d = load("ref_lp_feasible")
+    ws = P.Workspace(fixture_problem(d), settings_from(d["settings"]))
+    h = ws._h
+    assert native.query(h, native.Q_FORMAT_A) == 0 and native.query(h, native.Q_FORMAT_AT) == 0
+    assert native.query(h, native.Q_STREAM_BYTES_A) == 0
+    assert native.query(h, native.Q_LAUNCHES_PER_ITER) > 0
+    setup_cg = ws.cache.cg_iters_total
+    assert setup_cg > 0
+    sol = ws.solve()
+    assert ws.cache.cg_iters_total == sol.info.cg_iters == d["cg_iters"]
+    ws.update_vectors(b=d["b"])
+    assert ws.cache.cg_iters_total > sol.info.cg_iters
+    with pytest.raises(native.NativeError):
+        native.query(h, 99)
+
+
+def test_pinned_pool_recycles():
+    """Pooled page-locked buffers return to the pool when their arrays die."""
+    import gc
+    a = P.pinned_empty(1000)
+    addr = a.ctypes.data
+    del a
+    gc.collect()
+    b = P.pinned_zeros(1000)
+    assert b.ctypes.data == addr and not b.any()
