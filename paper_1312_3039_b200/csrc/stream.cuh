@@ -104,13 +104,17 @@ __device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned b
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps until the phase
+// completes (or the hint expires) instead of re-issuing the probe, leaving
+// issue slots (and power, under the sustained power cap) to the working warps
+constexpr unsigned kStmSuspendNs = 2000;
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "STM_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra STM_WAIT_%=;\n}" ::"r"(smem_u32(b)),
-      "r"(parity)
+      "r"(parity), "r"(kStmSuspendNs)
       : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
