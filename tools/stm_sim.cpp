@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
+#include <cmath>
 #include <random>
 #include <vector>
 
@@ -193,7 +194,36 @@ int main(int argc, char** argv) {
       for (int b = 0; b < 16; ++b) { mg = std::max(mg, gn[b]); mr = std::max(mr, rn[b]); }
       return mg + 2 * mr;
     };
-    if (search) {
+    if (search < 0) {  // simulated annealing over within-lane step swaps (same constraints)
+      std::mt19937 r2(s + 7);
+      auto conflict2 = [&](long long e, int k, int l) {
+        if (e < 0) return false;
+        const int rr = rowof(e, l);
+        for (int c = 0; c < 32; ++c) {
+          if (c == l) continue;
+          const long long f = grid[k * 32 + c];
+          if (f >= 0 && rowof(f, c) == rr) return true;
+        }
+        return false;
+      };
+      const int iters = -search * 32 * D * D;
+      double T = 2.0;
+      for (int it = 0; it < iters; ++it, T *= 0.9995) {
+        const int l = r2() % 32, k1 = r2() % D, k2 = r2() % D;
+        if (k1 == k2) continue;
+        long long& a = grid[k1 * 32 + l];
+        long long& b = grid[k2 * 32 + l];
+        if (a < 0 && b < 0) continue;
+        if (conflict2(a, k2, l) || conflict2(b, k1, l)) continue;
+        const int h = l >> 4;
+        const int before = cost(k1, h) + cost(k2, h);
+        std::swap(a, b);
+        const int after = cost(k1, h) + cost(k2, h);
+        const int dlt = after - before;
+        if (dlt > 0 && std::uniform_real_distribution<double>(0, 1)(r2) >= std::exp(-dlt / T)) std::swap(a, b);
+      }
+    }
+    if (search > 0) {
       // local search: swap two steps' contents within one lane (pinned entries
       // and padding only), keeping no step with a pinned and an overflow entry
       // of the same row
