@@ -1626,6 +1626,11 @@ int launch_stream(scs_handle* h, int mat, const Epi& epi, int chunk = -1, bool c
                                                               h->Pstm, NS, NB, accb);
   CK(cudaGetLastError());
   h->launches++;
+  // SCS_COMBINE_REPEAT=k (measurement only, tools/r02_combrep.sh): each
+  // combine launched k times -- its in-graph cost is the slope of the
+  // iteration time in k (the combines are idempotent but for statistics)
+  static const int rep = (int)std::max<long long>(1, env_ll("SCS_COMBINE_REPEAT", 1));
+  for (int r = 0; r < rep; ++r)
   if (S.splits > 1 && combine) {
     k_split_combine<Epi><<<elem_grid(h, r1 - r0), kBlock, 0, h->st>>>(h->Pstm, S.splits, F.rows, r0,
                                                                      r1, epi);

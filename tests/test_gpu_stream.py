@@ -21,6 +21,7 @@ VARIANTS = {
     "narrow": {"SCS_STREAM_W": "64"},
     "pieces": {"SCS_STREAM_W": "512", "SCS_STREAM_CAP": "6208"},
     "splits": {"SCS_STREAM_W": "128", "SCS_STREAM_SPLITS": "3"},
+    "splits9": {"SCS_STREAM_W": "64", "SCS_STREAM_SPLITS": "11"},
     "csr": {"SCS_STREAM_MIN": "1000000000"},
     "mixed": {"SCS_STREAM_W": "256", "SCS_STREAM_MIN": "300", "SCS_STREAM_SPLITS": "2"},
 }
