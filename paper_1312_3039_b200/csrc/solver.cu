@@ -22,6 +22,7 @@
 #include <cstring>
 #include <condition_variable>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <queue>
 #include <string>
@@ -1540,6 +1541,29 @@ void allreduce(scs_handle* h, double* d, size_t n) {
   if (h->sharded && n) h->comm->allreduce(h->st, d, n);
 }
 
+// A kernel's dynamic shared-memory ceiling is one attribute per device,
+// shared by every handle in the process: it is raised once per (kernel,
+// device) to the device's opt-in maximum and never lowered -- a handle
+// setting its own, smaller need would break another handle's larger
+// launches (two workspaces with different PSD sides on one GPU).  Returns
+// the dynamic bytes available to the kernel.
+int smem_optin(scs_handle* h, const void* fn) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(fn, h->dev);
+  const auto it = done.find(key);
+  if (it != done.end()) return it->second;
+  int dev_optin = 0;
+  CK(cudaDeviceGetAttribute(&dev_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+  cudaFuncAttributes fa{};
+  CK(cudaFuncGetAttributes(&fa, fn));
+  const int avail = dev_optin - (int)fa.sharedSizeBytes;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, avail));
+  done[key] = avail;
+  return avail;
+}
+
 // CSR SpMV launch.  When the gathered vector is large (A^T passes of the
 // 1e9-nonzero problem gather 80-160 MB, comparable to the 126 MB L2), the
 // launch carries an L2 access-policy window marking it persisting, so the
@@ -1598,17 +1622,7 @@ int launch_stream(scs_handle* h, int mat, const Epi& epi, int chunk = -1, bool c
   const auto& S = chunk < 0 ? h->ssch[mat][pair] : h->at_sch[chunk][pair];
   const long long r0 = chunk < 0 ? 0 : h->at_row[chunk], r1 = chunk < 0 ? F.rows : h->at_row[chunk + 1];
   const int accb = (pair ? 2 : 1) * kStmRS * NV * 8;
-  static std::once_flag once;
-  static int optin = 0;
-  std::call_once(once, [&] {
-    int dev_optin = 0;
-    cudaDeviceGetAttribute(&dev_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev);
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_stream<NV, STRIDE, Epi>);
-    optin = dev_optin - (int)fa.sharedSizeBytes;
-    cudaFuncSetAttribute(k_stream<NV, STRIDE, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-    cudaGetLastError();
-  });
+  const int optin = smem_optin(h, (const void*)k_stream<NV, STRIDE, Epi>);
   // two slab buffers (the next slab loads while the current one is read)
   // when at least 3 stages fit beside them, else one buffer (NV = 2 with
   // 4096-column slabs: 64 KB per slab)
@@ -2552,9 +2566,8 @@ void build_cones(scs_handle* h, const scs_problem* P) {
       h->n_psd_grid = (int)big.size();
       h->psd_grid_list = up_i(big);
       h->psd_grid_smem = std::max(kPsdTileSmem, psd_grid_pair_bytes(kmax));
-      if (h->psd_grid_smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(k_psd_grid, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)h->psd_grid_smem));
+      if ((size_t)smem_optin(h, (const void*)k_psd_grid) < h->psd_grid_smem)
+        throw Fail{SCS_ECUDA, "k_psd_grid: shared memory budget exceeded"};
       int occ = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_psd_grid, kBlock,
                                                        h->psd_grid_smem));
@@ -2568,9 +2581,8 @@ void build_cones(scs_handle* h, const scs_problem* P) {
       h->psd_grid_part = dalloc<double>(h, h->psd_grid_ctas);
     }
   }
-  if (h->cone_smem > 48 * 1024)
-    CK(cudaFuncSetAttribute(k_cone_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)h->cone_smem));
+  if ((size_t)smem_optin(h, (const void*)k_cone_apply) < h->cone_smem)
+    throw Fail{SCS_ECUDA, "k_cone_apply: shared memory budget exceeded"};
 }
 
 // ---------------------------------------------------------------------------

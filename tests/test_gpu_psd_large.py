@@ -151,3 +151,23 @@ def test_sdp_sharded_paths_match_single():
     res = parallel.emulated_solve(_tuple(prob), st, 2, bounds=np.array([0, 1, m], np.int64))
     for _, s in res:
         assert s.status == sol1.status and s.info.iterations == sol1.info.iterations
+
+
+def test_two_workspaces_different_psd_smem():
+    """Two live workspaces on one GPU whose PSD blocks need different dynamic
+    shared memory (sides 100 and 60: 160 KB and 58 KB in k_cone_apply): the
+    per-device kernel attribute is raised once and never lowered, so the
+    first workspace still solves after the second one's setup, and each
+    equals a solve alone."""
+    big, _ = _min_eig_sdp(100, 21)
+    small, _ = _min_eig_sdp(60, 22)
+    st = P.Settings(max_iters=40)
+    alone_big = P.Workspace(big, st).solve()
+    alone_small = P.Workspace(small, st).solve()
+    wa = P.Workspace(big, st)
+    wb = P.Workspace(small, st)
+    ra = wa.solve()
+    rb = wb.solve()
+    ra2 = wa.solve()
+    assert np.array_equal(ra.x, alone_big.x) and np.array_equal(ra2.x, alone_big.x)
+    assert np.array_equal(rb.x, alone_small.x)
