@@ -469,11 +469,11 @@ __global__ void __launch_bounds__(kBlock) k_cone_apply(Vec V, Cones K, double* p
 // PSD blocks of side <= kWarpPsd: one warp each over a list of block
 // indices (largest sides first), per-warp slices of the dynamic smem.
 // (Measured on config 4's 11,111 blocks of side 3-8: a single launch with
-// a warp per block beat 8- or 16-lane groups with one launch per side --
-// the per-block Jacobi is latency-bound on its fp64 sqrt/div chain, so
-// concurrency across blocks matters more than lanes per block.)
+// a warp per block beat 8- or 16-lane groups with one launch per side.
+// r02 ncu: the kernel is issue-bound -- 72% of issue slots, FP64 12% of the
+// instructions -- hence the per-side template bodies below.)
 constexpr size_t kPsdSmallSmem = (size_t)(kBlock / 32) * 2 * kWarpPsd * kWarpPsd * sizeof(double);
-__global__ void __launch_bounds__(kBlock) k_psd_small(Vec V, Cones K, const int* list, int count) {
+__global__ void __launch_bounds__(kBlock, 4) k_psd_small(Vec V, Cones K, const int* list, int count) {
   Ctl* c = V.ctl;
   if (c->stop) return;
   const double corr = c->corr, al = c->alpha;
@@ -486,8 +486,26 @@ __global__ void __launch_bounds__(kBlock) k_psd_small(Vec V, Cones K, const int*
   for (long long t = (long long)blockIdx.x * kW + wi; t < count; t += (long long)gridDim.x * kW) {
     const int b = list[t];
     const int k = K.psd_side[b];
-    psd_block<0>(WarpGroup{}, V, c, K.psd_off[b], k, corr, al, M, M + k * k, wcs[wi], wsn[wi],
-                 wpp[wi], wqq[wi], wdp[wi], wdq[wi]);
+    // the side as a compile-time constant: the Jacobi's index arithmetic
+    // (/ k, % k, the round-robin % (k - 1)) folds to multiplies -- with a
+    // runtime side, integer division was most of the kernel's instructions
+    // (config 4: IMAD/ISETP/I2F/F2I 40% of 129M, FP64 12%; issue slots 72%).
+    // The unrolled bodies want 120 registers; capped at 64 (4 CTAs per SM,
+    // as before) the kernel takes 127 us instead of 170 (uncapped: 158).
+    switch (k) {
+#define SCS_PSD_SIDE(KK)                                                                   \
+  case KK:                                                                                 \
+    psd_block<KK>(WarpGroup{}, V, c, K.psd_off[b], k, corr, al, M, M + k * k, wcs[wi], wsn[wi], \
+                  wpp[wi], wqq[wi], wdp[wi], wdq[wi]);                                     \
+    break;
+      SCS_PSD_SIDE(2) SCS_PSD_SIDE(3) SCS_PSD_SIDE(4) SCS_PSD_SIDE(5) SCS_PSD_SIDE(6)
+      SCS_PSD_SIDE(7) SCS_PSD_SIDE(8) SCS_PSD_SIDE(9) SCS_PSD_SIDE(10) SCS_PSD_SIDE(11)
+      SCS_PSD_SIDE(12) SCS_PSD_SIDE(13) SCS_PSD_SIDE(14) SCS_PSD_SIDE(15) SCS_PSD_SIDE(16)
+#undef SCS_PSD_SIDE
+      default:
+        psd_block<0>(WarpGroup{}, V, c, K.psd_off[b], k, corr, al, M, M + k * k, wcs[wi], wsn[wi],
+                     wpp[wi], wqq[wi], wdp[wi], wdq[wi]);
+    }
   }
 }
 

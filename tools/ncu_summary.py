@@ -37,6 +37,8 @@ def launches(path, out, title):
         st = idx[0]
         tail = [j for j, s in enumerate(seq) if j > st and "k_cone_apply" in s["name"]]
         en = (tail[0] + 1) if tail else len(seq)
+        while en < len(seq) and "k_psd" in seq[en]["name"]:  # PSD kernels after k_cone_apply
+            en += 1
     lines = [f"# {title}", "# one ADMM iteration (the last complete one in the capture);",
              "# ncu per-launch times are cold-cache and serialised: compare shares",
              f"{'kernel':64s} {'us':>9s} {'share':>6s} {'DRAM rd GB':>10s} {'wr GB':>7s} {'L2 hit %':>8s}"]
