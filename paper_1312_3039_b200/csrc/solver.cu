@@ -418,8 +418,8 @@ __device__ void psd_block(const G& g, const Vec& V, Ctl* c, long long o, int k_r
 }
 
 __global__ void __launch_bounds__(kBlock) k_cone_apply(Vec V, Cones K, double* psd_scratch,
-                                                       int smem_side, int warp_side,
-                                                       int grid_max) {
+                                                       int smem_side, const int* cta_list,
+                                                       int n_cta) {
   Ctl* c = V.ctl;
   if (c->stop) return;
   const double corr = c->corr, al = c->alpha;
@@ -438,15 +438,16 @@ __global__ void __launch_bounds__(kBlock) k_cone_apply(Vec V, Cones K, double* p
       store_y(V, o + e, r.ub, up);
     }
   }
-  if (K.n_psd == 0) return;
+  if (n_cta == 0) return;
   extern __shared__ double smem[];
   __shared__ double cs[128], sn[128], dpp[128], dqq[128];
   __shared__ int pp[128], qq[128];
-  // blocks of side > kWarpPsd: one CTA each
-  for (int b = blockIdx.x; b < K.n_psd; b += gridDim.x) {
+  // blocks of side > kWarpPsd not on the cooperative grid: one CTA each (a
+  // list -- r01 walked all blocks, and config 4's 11,111 warp-sized ones
+  // cost each CTA ~75 dependent loads: 52 us for nothing)
+  for (int t = blockIdx.x; t < n_cta; t += gridDim.x) {
+    const int b = cta_list[t];
     const int k = K.psd_side[b];
-    if (k <= warp_side) continue;
-    if (k > smem_side && k <= grid_max) continue;  // k_psd_grid
     const long long o = K.psd_off[b];
     double* M;
     double* Vv;
@@ -1388,6 +1389,8 @@ struct scs_handle {
   const int* psd_small_list = nullptr;  // their block indices, largest side first
   int n_psd_grid = 0;                   // blocks beyond smem_side: cooperative grid each
   const int* psd_grid_list = nullptr;
+  int n_psd_cta = 0;                    // the others: one CTA each in k_cone_apply
+  const int* psd_cta_list = nullptr;
   int psd_grid_ctas = 0;
   int psd_grid_max = 0;                 // largest side k_psd_grid takes (0: off)
   size_t psd_grid_smem = 0;
@@ -2599,6 +2602,19 @@ void build_cones(scs_handle* h, const scs_problem* P) {
       h->psd_grid_part = dalloc<double>(h, h->psd_grid_ctas);
     }
   }
+  {
+    std::vector<int> cta;
+    const int gmax = h->n_psd_grid > 0 ? h->psd_grid_max : 0;
+    for (size_t b = 0; b < psd_side.size(); ++b) {
+      const int k = psd_side[b];
+      if (k <= h->warp_side || (k > h->smem_side && k <= gmax)) continue;
+      cta.push_back((int)b);
+    }
+    h->n_psd_cta = (int)cta.size();
+    if (!cta.empty()) h->psd_cta_list = up_i(cta);
+    if (h->n_psd_cta + h->n_psd_small + h->n_psd_grid != (int)psd_side.size())
+      throw Fail{SCS_EINVAL, "PSD block lists do not cover every block"};
+  }
   if ((size_t)smem_optin(h, (const void*)k_cone_apply) < h->cone_smem)
     throw Fail{SCS_ECUDA, "k_cone_apply: shared memory budget exceeded"};
 }
@@ -2994,11 +3010,11 @@ void enqueue_iteration(scs_handle* h) {
 
 // big SOCs and large PSD blocks (CTA each), then small PSD blocks (warp each)
 void launch_cone_apply(scs_handle* h, const Vec& V) {
-  const int n_big = h->K.n_psd - h->n_psd_small - h->n_psd_grid;
+  const int n_big = h->n_psd_cta;
   if (h->K.n_chunk > 0 || n_big > 0) {
     const int g = std::max(1, std::min(std::max(h->K.n_chunk, n_big), h->grid_full));
     k_cone_apply<<<g, kBlock, h->cone_smem, h->st>>>(V, h->K, h->psd_scratch, h->smem_side,
-                                                      h->warp_side, h->psd_grid_max);
+                                                      h->psd_cta_list, h->n_psd_cta);
     h->launches++;
   }
   if (h->n_psd_small > 0) {
