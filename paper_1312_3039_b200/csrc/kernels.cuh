@@ -247,30 +247,11 @@ struct EpiRaw : Inner {
   __device__ void finish(const double*) const {}
 };
 
-// Split long rows with more than kLongSeg pieces: one warp per such row sums
-// its pieces (lane-strided, then a butterfly: a fixed order) into the first
-// piece's slot before k_rows runs the epilogue.
+// Split long rows with more than kLongSeg pieces: in k_rows, one warp per
+// such row sums its pieces (lane-strided, then a butterfly: a fixed order)
+// and its lane 0 runs the row's epilogue (r01: a separate k_seg_long launch
+// wrote the sums back for k_rows -- 11 us of config 4's 41-us A pass).
 constexpr int kLongSeg = 32;
-template <int NV>
-__global__ void k_seg_long(double* T, const long long* seg, const long long* long_rows, long long n) {
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  for (long long r = w; r < n; r += nw) {
-    const long long j = long_rows[r], v0 = seg[j], v1 = seg[j + 1];
-    double s[NV];
-#pragma unroll
-    for (int t = 0; t < NV; ++t) s[t] = 0.0;
-    for (long long v = v0 + lane; v < v1; v += 32)
-#pragma unroll
-      for (int t = 0; t < NV; ++t) s[t] += T[v * NV + t];
-#pragma unroll
-    for (int t = 0; t < NV; ++t) s[t] = warp_sum(s[t]);
-    if (lane == 0)
-#pragma unroll
-      for (int t = 0; t < NV; ++t) T[v0 * NV + t] = s[t];
-  }
-}
 
 // Row-sharded or row-banded A^T pass, part 2: the epilogue over the
 // all-reduced products, or over the sum of `nsum` band partials (in band
@@ -278,7 +259,9 @@ __global__ void k_seg_long(double* T, const long long* seg, const long long* lon
 // the sum of row i's pieces seg[i] .. seg[i+1]-1 (in order).
 template <class Epi>
 __global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows, int nsum, Epi epi0,
-                                                 const long long* seg = nullptr) {
+                                                 const long long* seg = nullptr,
+                                                 const long long* long_rows = nullptr,
+                                                 long long n_long = 0) {
   Epi epi = epi0;
   if (!epi.load()) return;
   constexpr int NR = Epi::NR > 0 ? Epi::NR : 1;
@@ -287,18 +270,41 @@ __global__ void __launch_bounds__(kBlock) k_rows(const double* T, long long rows
   for (int t = 0; t < NR; ++t) red[t] = 0.0;
   const long long tid = (long long)blockIdx.x * kBlock + threadIdx.x;
   const long long nt = (long long)gridDim.x * kBlock;
+  if (seg && n_long) {  // long rows: a warp each
+    const int lane = threadIdx.x & 31;
+    for (long long r = tid >> 5; r < n_long; r += nt >> 5) {
+      const long long j = long_rows[r], v0 = seg[j], v1 = seg[j + 1];
+      double s[Epi::NV];
+#pragma unroll
+      for (int t = 0; t < Epi::NV; ++t) s[t] = 0.0;
+      for (long long v = v0 + lane; v < v1; v += 32)
+#pragma unroll
+        for (int t = 0; t < Epi::NV; ++t) s[t] += T[v * Epi::NV + t];
+#pragma unroll
+      for (int t = 0; t < Epi::NV; ++t) s[t] = warp_sum(s[t]);
+      if (lane == 0) {
+        typename Epi::Pre pre;
+        epi.pre(j, pre);
+        epi.row(j, s, pre, red);
+      }
+    }
+  }
   for (long long j = tid; j < rows; j += nt) {
+    long long v0 = 0, v1 = 0;
+    if (seg) {
+      v0 = seg[j];
+      v1 = seg[j + 1];
+      if (v1 - v0 > kLongSeg) continue;  // a warp's (above)
+    }
     typename Epi::Pre pre;
     epi.pre(j, pre);
     double s[Epi::NV];
     if (seg) {
-      const long long v0 = seg[j], v1 = seg[j + 1];
 #pragma unroll
       for (int t = 0; t < Epi::NV; ++t) s[t] = T[v0 * Epi::NV + t];
-      if (v1 - v0 <= kLongSeg)  // longer rows were pre-summed by k_seg_long
-        for (long long v = v0 + 1; v < v1; ++v)
+      for (long long v = v0 + 1; v < v1; ++v)
 #pragma unroll
-          for (int t = 0; t < Epi::NV; ++t) s[t] += T[v * Epi::NV + t];
+        for (int t = 0; t < Epi::NV; ++t) s[t] += T[v * Epi::NV + t];
     } else {
 #pragma unroll
       for (int t = 0; t < Epi::NV; ++t) s[t] = T[j * Epi::NV + t];

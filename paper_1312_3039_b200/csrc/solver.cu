@@ -1688,13 +1688,9 @@ void launch_mat(scs_handle* h, int mat, const Epi& epi) {
     static_cast<Epi&>(raw) = epi;
     raw.T = h->Psplit;
     launch_spmv(h, h->Asp[mat], h->Lsp[mat], raw);
-    if (h->n_long[mat]) {
-      k_seg_long<Epi::NV><<<elem_grid(h, h->n_long[mat] * 32), kBlock, 0, h->st>>>(
-          h->Psplit, h->seg[mat], h->long_rows[mat], h->n_long[mat]);
-      h->launches++;
-    }
     const long long rows = mat == 0 ? h->m : h->n;
-    k_rows<Epi><<<elem_grid(h, rows), kBlock, 0, h->st>>>(h->Psplit, rows, 1, epi, h->seg[mat]);
+    k_rows<Epi><<<elem_grid(h, rows), kBlock, 0, h->st>>>(h->Psplit, rows, 1, epi, h->seg[mat],
+                                                          h->long_rows[mat], h->n_long[mat]);
     h->launches++;
     return;
   }

@@ -395,3 +395,26 @@ def test_pinned_pool_recycles():
     gc.collect()
     b = P.pinned_zeros(1000)
     assert b.ctypes.data == addr and not b.any()
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_split_long_rows_vs_oracle(monkeypatch, split):
+    """Rows split into pieces (SCS_SPLIT=1: every row longer than the piece
+    cap; the portfolio's budget row of 3000 assets has > 32 pieces and is
+    summed by one warp inside k_rows) against the oracle's iterates, and the
+    unsplit CSR path (SCS_SPLIT=0) against the same."""
+    monkeypatch.setenv("SCS_SPLIT", split)
+    colptr, rowidx, vals, b, c, cone = G.gen_portfolio_c4(3000, 5, 0, n_groups=0, seed=3)
+    cone = {k: v for k, v in cone.items() if k != "ep"}
+    data = P.ProblemData(P.SparseMatrix(b.size, colptr.size - 1, colptr, rowidx, vals), b, c,
+                         P.ConeSpec.from_any(cone))
+    A = O.Csc(b.size, colptr.size - 1, colptr, rowidx, vals)
+    orc = O.OracleSolver(A, b, c, cone, max_iters=30)
+    ref = {}
+    orc.solve(on_iteration=lambda k, u, v: ref.__setitem__(k, u.copy()))
+    got = {}
+    P.Workspace(data, P.Settings(max_iters=30)).solve(
+        on_iteration=lambda s: got.__setitem__(s.iter, s.u.copy()))
+    assert sorted(got) == sorted(ref)
+    for k in ref:
+        assert rel(got[k], ref[k]) < 1e-9, (split, k, rel(got[k], ref[k]))
