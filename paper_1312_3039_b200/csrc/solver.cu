@@ -1826,6 +1826,11 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T, long l
     cta[top.second].push_back(i);
     pq.push({top.first + all[i].cost, top.second});
   }
+  // each CTA's parts in slab-range order (SCS_STREAM_ORDER=1), so that the
+  // CTAs sweep the gathered vector's slab ranges roughly together
+  if (splits > 1 && env_ll("SCS_STREAM_ORDER", 1))
+    for (auto& l : cta)
+      std::stable_sort(l.begin(), l.end(), [&](int a, int b) { return all[a].s_lo < all[b].s_lo; });
   std::vector<StmCmd> cmds;
   std::vector<long long> coff(G + 1, 0);
   for (int g = 0; g < G; ++g) {
