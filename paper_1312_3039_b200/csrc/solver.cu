@@ -235,7 +235,9 @@ __global__ void k_cone_finish(Vec V, Cones K) {
   cone_finish(V, K);
 }
 
-__global__ void __launch_bounds__(kBlock) k_cone_tail(Vec V, Cones K, int defer) {
+// (64-register cap: 4 CTAs per SM instead of 3 -- config 5's streaming
+// loops 228 -> 197 us; a 40-register cap spills and is slower)
+__global__ void __launch_bounds__(kBlock, 4) k_cone_tail(Vec V, Cones K, int defer) {
   Ctl* c = V.ctl;
   if (c->stop) return;
   const long long n = V.n, m = V.m;
