@@ -1773,6 +1773,7 @@ void build_stm_sched(scs_handle* h, int mat, int pair, const StmTiles& T, long l
     }
   }
   splits = (int)env_ll("SCS_STREAM_SPLITS", splits);
+  splits = (int)env_ll(mat == 0 ? "SCS_STREAM_SPLITS_A" : "SCS_STREAM_SPLITS_AT", splits);
   splits = std::max(1, std::min(splits, std::max(1, T.S)));
   if (splits > 255) splits = 255;
   const double slab_cost = (double)F.W * 8.0 * (pair ? 1.5 : 2.0);
