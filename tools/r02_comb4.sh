@@ -1,4 +1,5 @@
 #!/bin/bash
+# (historical: measured and reverted; the variant and its knob are no longer in the tree -- DESIGN §5.1)
 # k_split_combine4 (four threads per row) vs the one-thread-per-row combine
 timeout 900 python -m pytest tests/test_gpu_stream.py -q -x --timeout 800 > gpurun_out/c4_tests.log 2>&1; echo tests_rc=$?; tail -2 gpurun_out/c4_tests.log
 for m in 8 1000; do

@@ -1,4 +1,5 @@
 #!/bin/bash
+# (historical: measured and reverted; the variant and its knob are no longer in the tree -- DESIGN §5.1)
 # hybrid split schedules (whole units beside split ones) vs uniform splits
 timeout 1200 python -m pytest tests/test_gpu_stream.py tests/test_gpu_parity.py tests/test_gpu_sharded.py -q -x --timeout 1100 > gpurun_out/hy_tests.log 2>&1; echo tests_rc=$?; tail -2 gpurun_out/hy_tests.log
 for hy in 1 0 1; do

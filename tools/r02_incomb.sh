@@ -1,4 +1,5 @@
 #!/bin/bash
+# (historical: measured and reverted; the variant and its knob are no longer in the tree -- DESIGN §5.1)
 # in-kernel combine of split partials (StmOut mode 2) vs the combine kernel
 timeout 900 python -m pytest tests/test_gpu_stream.py tests/test_gpu_parity.py -q -x --timeout 800 > gpurun_out/ic_tests.log 2>&1; echo tests_rc=$?; tail -2 gpurun_out/ic_tests.log
 for ic in 1 0; do

@@ -1,4 +1,5 @@
 #!/bin/bash
+# (historical: measured and reverted; the variant and its knob are no longer in the tree -- DESIGN §5.1)
 # lane-major 4-step slot-word groups (one 8-byte load per batch)
 timeout 900 python -m pytest tests/test_gpu_stream.py tests/test_gpu_parity.py -q -x --timeout 800 > gpurun_out/wg_tests.log 2>&1; echo tests_rc=$?; tail -2 gpurun_out/wg_tests.log
 for c in c5 c3 c5; do
