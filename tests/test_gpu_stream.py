@@ -146,3 +146,39 @@ def test_stream_row_shards_match_reference(monkeypatch, name, world):
         if k in traj:
             assert rel(traj[k], d["us"][i]) < 1e-9, (name, world, k)
     assert all(s.status.value == d["status"] for _, s in res)
+
+
+def _unique_coo(m, n, nz, seed):
+    rng = np.random.default_rng(seed)
+    key = np.unique(rng.integers(0, n, nz).astype(np.int64) * m + rng.integers(0, m, nz))
+    cols, rows = np.divmod(key, m)
+    return rows, cols, rng.standard_normal(key.size)
+
+
+@pytest.mark.parametrize("name,m,n,nz,streamed", [
+    ("dense_tiles", 1_000_000, 100_000, 21_000_000, 1),     # ~3400 entries per tile
+    ("sparse_tiles", 2_000_000, 1_000_000, 21_000_000, 0),  # ~175 entries per tile: CSR kernel
+    ("short_wide", 16, 4_000_000, 25_000_000, 1),           # 16 rows of ~1.4e6 entries
+    ("tall_thin", 30_000_000, 6, 24_000_000, 1),            # 6 columns of ~4e6 entries
+])
+def test_default_format_by_tile_density(name, m, n, nz, streamed):
+    """Production heuristic (no SCS_STREAM knob): >= 2e7 nonzeros streams a
+    matrix only when its average tile holds >= 800 entries (sparser tiles
+    ran 2-3x slower than the CSR kernel); extreme row / column lengths go
+    through the dense-section handling.  Products against numpy sums."""
+    rows, cols, vals = _unique_coo(m, n, nz, 5)
+    assert rows.size >= 20_000_000
+    colptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(cols, minlength=n), out=colptr[1:])
+    data = P.ProblemData(P.SparseMatrix(m, n, colptr, rows, vals), np.ones(m), np.ones(n),
+                         P.ConeSpec(nonneg_dim=m))
+    ws = P.Workspace(data, P.Settings(normalize=False))
+    from paper_1312_3039_b200 import native
+    assert native.query(ws._h, native.Q_FORMAT_A) == streamed
+    assert native.query(ws._h, native.Q_FORMAT_AT) == streamed
+    rng = np.random.default_rng(9)
+    x, y = rng.standard_normal(n), rng.standard_normal(m)
+    ax = np.bincount(rows, vals * x[cols], minlength=m)
+    aty = np.bincount(cols, vals * y[rows], minlength=n)
+    assert np.abs(ws.apply_a(x) - ax).max() <= 1e-12 * (1 + np.abs(ax).max())
+    assert np.abs(ws.apply_a(y, transpose=True) - aty).max() <= 1e-12 * (1 + np.abs(aty).max())
