@@ -2212,9 +2212,10 @@ void setup_stream(scs_handle* h) {
   // the gathered vector) and a piece header per tile, so it only wins when
   // the average tile holds enough entries -- measured at 2.1e7 nonzeros:
   // 3428 entries per tile 1.6x faster than the CSR kernel, 175 / 88 / 22
-  // entries per tile 2-3x slower (tools/r02_stream_vs_csr.py); config 5:
-  // 1671, config 3: 16,300.  Below the threshold the matrix stays CSR.
-  const long long tile_min = env_ll("SCS_STREAM_TILE_MIN", 800);
+  // entries per tile 2-3x slower, crossover near 1000 (800: 15% slower,
+  // 1200: 13% faster; tools/r02_stream_vs_csr.py); config 5: 1671, config
+  // 3: 16,300.  Below the threshold the matrix stays CSR.
+  const long long tile_min = env_ll("SCS_STREAM_TILE_MIN", 1000);
   for (int mat = 0; mat < 2; ++mat) {
     const long long rows = mat == 0 ? h->m : h->n, cols = mat == 0 ? h->n : h->m;
     const double tiles = (double)((rows + kStmRS - 1) / kStmRS) * (double)((cols + kStmMaxW - 1) / kStmMaxW);

@@ -163,7 +163,7 @@ def _unique_coo(m, n, nz, seed):
 ])
 def test_default_format_by_tile_density(name, m, n, nz, streamed):
     """Production heuristic (no SCS_STREAM knob): >= 2e7 nonzeros streams a
-    matrix only when its average tile holds >= 800 entries (sparser tiles
+    matrix only when its average tile holds >= 1000 entries (sparser tiles
     ran 2-3x slower than the CSR kernel); extreme row / column lengths go
     through the dense-section handling.  Products against numpy sums."""
     rows, cols, vals = _unique_coo(m, n, nz, 5)

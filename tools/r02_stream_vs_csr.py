@@ -35,10 +35,14 @@ def timed(data, stream):
     return ms.value * 1e3 / 10, fa
 
 
-for name, m, n, nz in [("rows10_cols1e6", 2_000_000, 1_000_000, 21_000_000),
-                       ("rows20_cols1e5", 1_000_000, 100_000, 21_000_000),
-                       ("rows50_cols1e7", 400_000, 10_000_000, 21_000_000),
-                       ("rows5_cols4e6", 4_000_000, 4_000_000, 21_000_000)]:
+SHAPES = [("rows10_cols1e6", 2_000_000, 1_000_000, 21_000_000),
+          ("rows20_cols1e5", 1_000_000, 100_000, 21_000_000),
+          ("rows50_cols1e7", 400_000, 10_000_000, 21_000_000),
+          ("rows5_cols4e6", 4_000_000, 4_000_000, 21_000_000)]
+if "--crossover" in sys.argv:  # square shapes at ~400 / 800 / 1200 / 1700 entries per tile
+    SHAPES = [(f"tile{e}", s, s, 21_000_000) for e, s in
+              ((400, 940_000), (800, 660_000), (1200, 540_000), (1700, 455_000))]
+for name, m, n, nz in SHAPES:
     d = problem(m, n, nz, 1)
     us1, f1 = timed(d, "1")
     us0, f0 = timed(d, "0")
