@@ -2203,7 +2203,10 @@ void setup_stream(scs_handle* h) {
   const long long force = env_ll("SCS_STREAM", -1);
   h->stm_pair = env_ll("SCS_STREAM_PAIR", 0) != 0;
   if (force == 0 || h->nnz == 0) return;
-  if (force < 0 && h->nnz < 20000000LL) return;
+  // (r02) from 4e6 nonzeros (dense tiles, tools/r02_stream_vs_csr.py --small:
+  // 2.7e6 181 vs 168 us per iteration for the CSR kernel, 5.3e6 218 vs 246,
+  // 1.05e7 291 vs 433; r01: from 2e7)
+  if (force < 0 && h->nnz < env_ll("SCS_STREAM_NNZ_MIN", 4000000LL)) return;
   h->at_chunks = h->sharded ? (int)std::max<long long>(1, std::min<long long>(
                                     scs_handle::kMaxChunks, env_ll("SCS_AT_CHUNKS", 2)))
                              : 1;
@@ -2221,6 +2224,13 @@ void setup_stream(scs_handle* h) {
     const double tiles = (double)((rows + kStmRS - 1) / kStmRS) * (double)((cols + kStmMaxW - 1) / kStmMaxW);
     if (force < 0 && (double)h->nnz < (double)tile_min * tiles) {
       dbg("stream mat=%d: %.0f entries per tile < %lld, CSR kernel", mat, (double)h->nnz / tiles, tile_min);
+      continue;
+    }
+    // ... and enough tiles to spread over the persistent CTAs (units x slab
+    // ranges): bench config s1e7 (1e7 nonzeros in 25 x 3 tiles) ran at half
+    // the CSR kernel's rate streamed; 124 tiles 8% slower, 434 tiles 12% faster
+    if (force < 0 && tiles < (double)env_ll("SCS_STREAM_TILES_MIN", 2LL * h->sms)) {
+      dbg("stream mat=%d: %.0f tiles < 2 per SM, CSR kernel", mat, tiles);
       continue;
     }
     build_stream(h, mat);

@@ -366,7 +366,7 @@ def test_pinned_buffers_roundtrip():
 
 
 def test_query_and_cache_counter():
-    """scs_query: the production format switch (CSR below 2e7 nonzeros), the
+    """scs_query: the production format switch (CSR below 4e6 nonzeros), the
     per-iteration launch count, and EmbeddingCache.cg_iters_total kept in
     step with the reference's (setup solve, then every solve; update_vectors
     re-solves g, embedding.py:145-162)."""

@@ -1,5 +1,5 @@
 """Parity at the benchmarked scale (BASELINE configs 3 and 5), through the
-production SpMV format (TMA-streamed tiles, chosen automatically above 2e7
+production SpMV format (TMA-streamed tiles, chosen automatically from 4e6
 nonzeros) with no SCS_STREAM_* overrides.
 
 * Config 3 (1e8 nonzeros) against conesplit itself: the fixture

@@ -1,6 +1,6 @@
 """GPU tests of the TMA-streamed tile SpMV (csrc/stream.cuh), forced on for
 small problems (SCS_STREAM=1 is read at Workspace creation; the size
-heuristic only enables it from 2e7 nonzeros).  The knobs shrink the format
+heuristic only enables it from 4e6 nonzeros and dense tiles).  The knobs shrink the format
 so that small matrices exercise every path: many slabs (SCS_STREAM_W),
 tiles cut into several pieces (SCS_STREAM_CAP), slab-range splits with the
 combine kernel (SCS_STREAM_SPLITS), and CSR units for sparse sub-blocks
@@ -160,14 +160,17 @@ def _unique_coo(m, n, nz, seed):
     ("sparse_tiles", 2_000_000, 1_000_000, 21_000_000, 0),  # ~175 entries per tile: CSR kernel
     ("short_wide", 16, 4_000_000, 25_000_000, 1),           # 16 rows of ~1.4e6 entries
     ("tall_thin", 30_000_000, 6, 24_000_000, 1),            # 6 columns of ~4e6 entries
+    ("mid_dense", 500_000, 50_000, 10_500_000, 1),          # 1.05e7 nonzeros, ~6500 per tile
+    ("small", 125_000, 12_500, 2_700_000, 0),               # below 4e6 nonzeros: CSR kernel
+    ("few_tiles", 100_000, 10_000, 10_000_000, 0),          # dense, but 25 x 3 tiles: CSR kernel
 ])
 def test_default_format_by_tile_density(name, m, n, nz, streamed):
-    """Production heuristic (no SCS_STREAM knob): >= 2e7 nonzeros streams a
-    matrix only when its average tile holds >= 1000 entries (sparser tiles
+    """Production heuristic (no SCS_STREAM knob): >= 4e6 nonzeros streams a
+    matrix only when its average tile holds >= 1000 entries and it has at
+    least 2 tiles per SM (sparser tiles
     ran 2-3x slower than the CSR kernel); extreme row / column lengths go
     through the dense-section handling.  Products against numpy sums."""
     rows, cols, vals = _unique_coo(m, n, nz, 5)
-    assert rows.size >= 20_000_000
     colptr = np.zeros(n + 1, np.int64)
     np.cumsum(np.bincount(cols, minlength=n), out=colptr[1:])
     data = P.ProblemData(P.SparseMatrix(m, n, colptr, rows, vals), np.ones(m), np.ones(n),

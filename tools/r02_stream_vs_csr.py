@@ -42,6 +42,9 @@ SHAPES = [("rows10_cols1e6", 2_000_000, 1_000_000, 21_000_000),
 if "--crossover" in sys.argv:  # square shapes at ~400 / 800 / 1200 / 1700 entries per tile
     SHAPES = [(f"tile{e}", s, s, 21_000_000) for e, s in
               ((400, 940_000), (800, 660_000), (1200, 540_000), (1700, 455_000))]
+if "--small" in sys.argv:  # dense tiles below the 2e7-nonzero gate
+    SHAPES = [("nnz2.6e6", 125_000, 12_500, 2_700_000), ("nnz5.2e6", 250_000, 25_000, 5_300_000),
+              ("nnz1e7", 500_000, 50_000, 10_500_000)]
 for name, m, n, nz in SHAPES:
     d = problem(m, n, nz, 1)
     us1, f1 = timed(d, "1")
