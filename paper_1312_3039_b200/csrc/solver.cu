@@ -2202,15 +2202,10 @@ void stm_selfcheck(scs_handle* h) {
 void setup_stream(scs_handle* h) {
   const long long force = env_ll("SCS_STREAM", -1);
   h->stm_pair = env_ll("SCS_STREAM_PAIR", 0) != 0;
-  if (force == 0 || h->nnz == 0) return;
   // (r02) from 4e6 nonzeros (dense tiles, tools/r02_stream_vs_csr.py --small:
   // 2.7e6 181 vs 168 us per iteration for the CSR kernel, 5.3e6 218 vs 246,
   // 1.05e7 291 vs 433; r01: from 2e7)
-  if (force < 0 && h->nnz < env_ll("SCS_STREAM_NNZ_MIN", 4000000LL)) return;
-  h->at_chunks = h->sharded ? (int)std::max<long long>(1, std::min<long long>(
-                                    scs_handle::kMaxChunks, env_ll("SCS_AT_CHUNKS", 2)))
-                             : 1;
-  size_t need = 0;
+  const bool gate = force > 0 || (force < 0 && h->nnz >= env_ll("SCS_STREAM_NNZ_MIN", 4000000LL));
   // (r02) per matrix: the streamed format pays a slab load (W columns of
   // the gathered vector) and a piece header per tile, so it only wins when
   // the average tile holds enough entries -- measured at 2.1e7 nonzeros:
@@ -2219,20 +2214,44 @@ void setup_stream(scs_handle* h) {
   // 1200: 13% faster; tools/r02_stream_vs_csr.py); config 5: 1671, config
   // 3: 16,300.  Below the threshold the matrix stays CSR.
   const long long tile_min = env_ll("SCS_STREAM_TILE_MIN", 1000);
-  for (int mat = 0; mat < 2; ++mat) {
+  bool want[2] = {false, false};
+  for (int mat = 0; mat < 2 && gate && h->nnz > 0; ++mat) {
+    want[mat] = true;
+    if (force > 0) continue;
     const long long rows = mat == 0 ? h->m : h->n, cols = mat == 0 ? h->n : h->m;
     const double tiles = (double)((rows + kStmRS - 1) / kStmRS) * (double)((cols + kStmMaxW - 1) / kStmMaxW);
-    if (force < 0 && (double)h->nnz < (double)tile_min * tiles) {
+    if ((double)h->nnz < (double)tile_min * tiles) {
       dbg("stream mat=%d: %.0f entries per tile < %lld, CSR kernel", mat, (double)h->nnz / tiles, tile_min);
-      continue;
+      want[mat] = false;
     }
     // ... and enough tiles to spread over the persistent CTAs (units x slab
     // ranges): bench config s1e7 (1e7 nonzeros in 25 x 3 tiles) ran at half
     // the CSR kernel's rate streamed; 124 tiles 8% slower, 434 tiles 12% faster
-    if (force < 0 && tiles < (double)env_ll("SCS_STREAM_TILES_MIN", 2LL * h->sms)) {
+    else if (tiles < (double)env_ll("SCS_STREAM_TILES_MIN", 2LL * h->sms)) {
       dbg("stream mat=%d: %.0f tiles < 2 per SM, CSR kernel", mat, tiles);
-      continue;
+      want[mat] = false;
     }
+  }
+  // Row-sharded: the A^T pass's collectives follow its format (chunked
+  // all-reduces when streamed), so every rank makes the same choice -- a
+  // matrix is streamed only where every rank's shard wants it.
+  if (h->sharded) {
+    double w[2] = {want[0] ? 1.0 : 0.0, want[1] ? 1.0 : 0.0};
+    double* d = dalloc<double>(h, 2);
+    h2d(h, d, w, 2);
+    allreduce(h, d, 2);
+    CK(cudaMemcpyAsync(w, d, sizeof(w), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    dfree(h, d);
+    for (int mat = 0; mat < 2; ++mat) want[mat] = w[mat] >= (double)h->world - 0.5;
+  }
+  if (!want[0] && !want[1]) return;
+  h->at_chunks = h->sharded ? (int)std::max<long long>(1, std::min<long long>(
+                                    scs_handle::kMaxChunks, env_ll("SCS_AT_CHUNKS", 2)))
+                             : 1;
+  size_t need = 0;
+  for (int mat = 0; mat < 2; ++mat) {
+    if (!want[mat]) continue;
     build_stream(h, mat);
     h->stm_m[mat] = true;
     for (int pair = 0; pair < 2; ++pair) {

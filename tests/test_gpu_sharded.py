@@ -142,3 +142,32 @@ def test_nccl_one_rank_sharded_code_path():
     # the graph-launched loop (NCCL is capturable) gives the same answer
     sol2 = ws.solve()
     assert sol2.status == sol1.status and sol2.info.iterations == sol1.info.iterations
+
+
+def test_shards_agree_on_the_streamed_format():
+    """Production heuristic per shard (no SCS_STREAM knob): shard 0 holds
+    5e6 nonzeros in dense tiles (it alone would stream), shard 1 3e6 (below
+    the 4e6 gate).  The A^T pass's all-reduces follow its format (chunked when
+    streamed), so both shards must choose the same -- here the CSR kernel --
+    and the iterates equal the single-GPU solve's."""
+    from paper_1312_3039_b200 import native
+    rng = np.random.default_rng(17)
+    m0, m1, n = 500_000, 500_000, 50_000
+    rows = np.concatenate([rng.integers(0, m0, 5_200_000), m0 + rng.integers(0, m1, 3_000_000)])
+    cols = rng.integers(0, n, rows.size)
+    key = np.unique(cols.astype(np.int64) * (m0 + m1) + rows)
+    cols, rows = np.divmod(key, m0 + m1)
+    vals = rng.standard_normal(key.size)
+    colptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(cols, minlength=n), out=colptr[1:])
+    m = m0 + m1
+    prob = (colptr, rows, vals, rng.standard_normal(m), rng.standard_normal(n), {"l": m})
+    st = P.Settings(max_iters=8)
+    ws1, sol1, traj1 = single(prob, st, upto=8)
+    assert native.query(ws1._h, native.Q_FORMAT_A) == 1  # 8.2e6 nonzeros in one piece: streamed
+    res, trajk = sharded(prob, st, 2, bounds=[0, m0, m], upto=8)
+    fmts = {(native.query(ws._h, native.Q_FORMAT_A), native.query(ws._h, native.Q_FORMAT_AT))
+            for ws, _ in res}
+    assert fmts == {(0, 0)}, fmts
+    for k in sorted(traj1):
+        assert rel(trajk[k], traj1[k]) < TOL, (k, rel(trajk[k], traj1[k]))
