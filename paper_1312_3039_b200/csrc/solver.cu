@@ -2679,6 +2679,7 @@ void build_matrices(scs_handle* h, const scs_problem* P) {
   double* tv = dalloc<double>(h, nnz);
   h2d(h, tp, (const long long*)P->colptr, n + 1);
   h2d(h, tv, P->vals, nnz);
+  dbg("values copied (%.2f GB)", 8e-9 * (double)nnz);
   // row indices arrive as int64: stage in chunks and narrow on the device
   {
     const long long chunk = 1LL << 26;
@@ -2691,6 +2692,7 @@ void build_matrices(scs_handle* h, const scs_problem* P) {
     CK(cudaStreamSynchronize(h->st));
     dfree(h, stage);
   }
+  dbg("row indices copied (%.2f GB)", 8e-9 * (double)nnz);
   h->At = Csr{tp, ti, tv, n};
   long long* rp = dalloc<long long>(h, m + 1);
   int* ci = dalloc<int>(h, nnz);
