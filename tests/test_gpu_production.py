@@ -162,3 +162,32 @@ def test_c5_streamed_matches_csr():
         assert _rel(ts["snap"][k][1], tc["snap"][k][1]) < 1e-12, k
     assert ts["cg"] == tc["cg"]
     assert ts["status"] == tc["status"] and ts["iterations"] == tc["iterations"]
+
+
+def test_mid_size_default_streamed_matches_csr():
+    """The mid-size regime the r02 gate now streams (1e7 nonzeros, ~600
+    dense tiles): default format against the CSR kernel, 30 iterates."""
+    data = _data(dict(p=15_000, q=270_000, nnz=10_000_000, seed=3))
+    ell = data.n + data.m + 1
+    idx = np.sort(np.random.default_rng(6).choice(ell, 20_000, replace=False))
+    snap = (1, 5, 30)
+    st = P.Settings(max_iters=30, eps_pri=1e-3, eps_dual=1e-3, eps_gap=1e-3)
+    ws = P.Workspace(data, st)
+    assert native.query(ws._h, native.Q_FORMAT_A) == 1
+    assert native.query(ws._h, native.Q_FORMAT_AT) == 1
+    ts = _trajectory(ws, 30, snap, idx)
+    del ws
+    os.environ["SCS_STREAM"] = "0"
+    try:
+        wc = P.Workspace(data, st)
+    finally:
+        del os.environ["SCS_STREAM"]
+    tc = _trajectory(wc, 30, snap, idx)
+    del wc
+    for k in range(len(tc["unorm"])):
+        assert abs(ts["unorm"][k] - tc["unorm"][k]) <= 1e-12 * tc["unorm"][k], k
+        assert abs(ts["vnorm"][k] - tc["vnorm"][k]) <= 1e-12 * tc["vnorm"][k], k
+    for k in snap:
+        assert _rel(ts["snap"][k][0], tc["snap"][k][0]) < 1e-12, k
+    assert ts["cg"] == tc["cg"]
+    assert ts["status"] == tc["status"] and ts["iterations"] == tc["iterations"]
